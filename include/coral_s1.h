@@ -1,0 +1,197 @@
+/*
+ * coral_s1.h — C ABI of the B200-native stage-1 Serving-Template generator.
+ *
+ * The hot path replaced is Coral's stage 1 (arXiv 2605.04357), implemented in the
+ * reference by `hetserve.templates.build_library`
+ * (/root/reference/pkg/src/hetserve/templates.py:417-505). Every entry point below
+ * names the reference function whose behaviour it reproduces. All arguments are
+ * plain pointers and sizes; no torch types cross this boundary. Device work runs on
+ * the stream given to coral_s1_set_stream (default: the legacy stream).
+ *
+ * Error convention: every call returns an int status.
+ *   CORAL_S1_OK (0)              success
+ *   CORAL_S1_EINVAL (1)          invalid argument      -> DomainError / ValueError
+ *   CORAL_S1_ENOTEMPLATE (2)     a (model, phase) has no feasible template
+ *                                                      -> LibraryGenError
+ *   CORAL_S1_ECUDA (3)           CUDA failure          -> RuntimeError
+ *   CORAL_S1_EUNSUPPORTED (4)    input outside the GPU path's envelope
+ *                                (n_max > 6, > 63 configs, > 128 layer units)
+ * The message of the last failure on the calling thread is coral_s1_last_error().
+ * The library never aborts the process.
+ */
+#ifndef CORAL_S1_H
+#define CORAL_S1_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CORAL_S1_OK 0
+#define CORAL_S1_EINVAL 1
+#define CORAL_S1_ENOTEMPLATE 2
+#define CORAL_S1_ECUDA 3
+#define CORAL_S1_EUNSUPPORTED 4
+
+#define CORAL_S1_PHASE_PREFILL 0
+#define CORAL_S1_PHASE_DECODE 1
+
+/* Largest envelope of the GPU path. n_max <= 6 keeps every node multiset's
+ * sub-multiset lattice within 64 codes (kernels.py:147-150: M = prod(counts+1)). */
+#define CORAL_S1_MAX_NODES 6
+#define CORAL_S1_MAX_CONFIGS 63
+#define CORAL_S1_MAX_LAYER_UNITS 128
+
+typedef struct coral_s1_handle coral_s1_handle;
+
+/* Spec tables in (SoA). Mirrors the reference inputs of build_library
+ * (templates.py:417-421): NodeConfig (domain.py:32-50), ModelSpec
+ * (domain.py:64-88), SloSpec (domain.py:91-101), PerfParams (perf.py:17-54),
+ * GenContext (templates.py:52-65), LibraryCaps (templates.py:38-49), and the
+ * optional ProfileTable overrides (perf.py:94-116). */
+typedef struct coral_s1_problem {
+  /* node configs, sorted by name (templates.py:429) */
+  int32_t num_configs;
+  const int32_t* cfg_gpu_count;   /* NodeConfig.gpu_count */
+  const double* cfg_mem_gb;       /* GpuSpec.mem_gb (GiB per GPU) */
+  const double* cfg_bw_tbps;      /* GpuSpec.bw_tbps */
+  const double* cfg_tflops;       /* GpuSpec.tflops */
+  const int32_t* cfg_str_rank;    /* rank of (name + '*') in code-point order:
+                                     makes the packed combo key sort exactly like
+                                     str(NodeComboKey) (domain.py:127-129) */
+  /* models, in the caller's order */
+  int32_t num_models;
+  const int32_t* mdl_num_layers;
+  const int32_t* mdl_granularity; /* resolved GenContext.layer_granularity */
+  const double* mdl_params_total_b;
+  const double* mdl_params_active_b;
+  const double* mdl_hidden_size;
+  const double* mdl_bytes_per_param;
+  const double* mdl_kv_bytes;     /* kv_bytes_per_token_per_layer */
+  const double* slo_prefill_ms;   /* SloSpec of each model */
+  const double* slo_decode_ms;
+  /* phases, in the caller's order (templates.py:441) */
+  int32_t num_phases;
+  const int32_t* phases;          /* CORAL_S1_PHASE_* */
+  /* PerfParams */
+  double mfu, mbu, net_eff, fixed_overhead_ms;
+  double avg_prompt_tokens, avg_ctx_tokens, slo_budget_frac;
+  /* GenContext network assumption */
+  double net_gbps, net_latency_ms;
+  /* LibraryCaps */
+  int32_t n_max;
+  double rho;
+  /* ProfileTable overrides (perf.py:110-116); bucket -1 matches any budget */
+  int32_t num_profile;
+  const int32_t* prof_model;
+  const int32_t* prof_phase;
+  const int32_t* prof_cfg;
+  const int32_t* prof_j;          /* layers (not units) */
+  const int32_t* prof_bucket;     /* integer milliseconds or -1 */
+  const double* prof_tps;
+} coral_s1_problem;
+
+/* One evaluated candidate (model, phase, combo): the ServingTemplate payload
+ * (domain.py:183-202) in canonical placement form (templates.py:209-228).
+ * num_stages == 0 means "no feasible template" (templates.py:487-490). */
+typedef struct coral_s1_record {
+  double throughput_tps;
+  uint8_t num_stages;
+  uint8_t num_nodes;
+  uint16_t layers_per_stage[CORAL_S1_MAX_NODES];
+  uint8_t stage_of_node[CORAL_S1_MAX_NODES];
+  uint8_t _pad[2];
+} coral_s1_record; /* 32 bytes */
+
+/* One frontier survivor (new output). */
+typedef struct coral_s1_frontier_item {
+  double price_usd_h;             /* allocation.py:91-98 sequential sum */
+  double throughput_tps;
+  uint64_t combo_key;             /* packed tokens, str(combo) order */
+  int32_t mp;                     /* model * num_phases + phase slot */
+  int32_t region;
+  coral_s1_record rec;
+} coral_s1_frontier_item; /* 64 bytes */
+
+/* ---- lifecycle -------------------------------------------------------- */
+int coral_s1_create(int device, coral_s1_handle** out);
+int coral_s1_destroy(coral_s1_handle* h);
+const char* coral_s1_last_error(void);
+int coral_s1_version(void);
+int coral_s1_set_stream(coral_s1_handle* h, void* cuda_stream);
+/* number of kernel launches issued on the handle since creation */
+int64_t coral_s1_launch_count(const coral_s1_handle* h);
+
+/* ---- problem ---------------------------------------------------------- */
+/* Upload the spec tables (host -> device). Validates like the reference
+ * constructors (LibraryCaps.__post_init__ templates.py:45-49). */
+int coral_s1_set_problem(coral_s1_handle* h, const coral_s1_problem* p);
+
+/* ---- T-hat tables: throughput_table (templates.py:83-96) for every
+ * (model, phase, S = 1..min(n_max, L)), node_max_throughput (perf.py:159-175)
+ * and stage_budget_s (templates.py:68-80) on device. */
+int coral_s1_tables(coral_s1_handle* h);
+/* layout: per mp = model*num_phases + phase slot, S-major, config, layer unit.
+ * offsets[mp] (num_models*num_phases + 1 entries) index into the flat table. */
+int coral_s1_table_layout(const coral_s1_handle* h, int64_t* offsets, int32_t* lsteps,
+                          int32_t* smax);
+int coral_s1_get_tables(coral_s1_handle* h, double* out, int64_t n);
+int coral_s1_get_budgets(coral_s1_handle* h, double* out, int64_t n); /* [mp][n_max] */
+
+/* ---- enumeration: enumerate_combos (templates.py:99-113) -------------- */
+int coral_s1_enumerate(coral_s1_handle* h);
+int coral_s1_num_combos(const coral_s1_handle* h, int64_t* counts /* [num_models] */);
+/* keys of model m in str(combo) order (the library order, templates.py:340);
+ * with enumeration_order != 0 in the reference's (num_nodes, str) order
+ * (templates.py:112). key = 6 tokens x 9 bits, token = (rank'+1)<<3 | count,
+ * first token most significant. */
+int coral_s1_get_combos(coral_s1_handle* h, int model, int enumeration_order,
+                        uint64_t* keys, int64_t n);
+
+/* ---- evaluation: _solve_chunk (templates.py:308-326) over candidates
+ * [lo, hi) of the global (model, phase, combo) list (mp-major, library order);
+ * hi < 0 means all. Placement DP = _placement_dp_nb (kernels.py:143-276). */
+int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi);
+/* multi-GPU shard: candidates rank, rank+world, rank+2*world, ... (interleaving
+ * balances the ~100x per-candidate cost spread across ranks) */
+int coral_s1_evaluate_shard(coral_s1_handle* h, int rank, int world);
+int coral_s1_num_candidates(const coral_s1_handle* h, int64_t* n);
+/* records of one (model, phase slot), library order; n = its combo count */
+int coral_s1_get_records(coral_s1_handle* h, int mp, coral_s1_record* out, int64_t n);
+
+/* ---- frontier (new): per (model, phase, region) the skyline of
+ * (price ascending, throughput descending, key ascending) over the evaluated
+ * candidates; prices[r * num_configs + c] in USD/h, NaN = not offered
+ * (allocation.py:91-98 returns None). */
+int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices,
+                      int64_t* num_survivors);
+int coral_s1_get_frontier(coral_s1_handle* h, coral_s1_frontier_item* out, int64_t n);
+/* multi-GPU: copy the local survivors into a device buffer (capacity cap), and
+ * re-run the skyline over n gathered device items (from all ranks). */
+int coral_s1_frontier_export_device(coral_s1_handle* h, void* dev_items, int64_t cap,
+                                    int64_t* n);
+int coral_s1_frontier_merge_device(coral_s1_handle* h, const void* dev_items, int64_t n,
+                                   int64_t* num_survivors);
+
+/* ---- operator: placement_search (kernels.py:279-295), batched ----------
+ * case i: counts[i*6 .. +C_i) (int64), C_i = ncfg[i] <= 6, tput rows at
+ * tput + tput_off[i] (C_i x L_i doubles, row-major), S_i. Outputs raw (not
+ * canonicalised) results exactly as the numba kernel returns them:
+ * best[i] (NEG_INF = -1e300 when infeasible), stage_j[i*6 + s],
+ * stage_counts[(i*6 + s)*6 + c]. Host buffers. */
+int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t* ncfg,
+                              const int64_t* counts, const int32_t* lsteps,
+                              const int64_t* tput_off, const double* tput,
+                              int64_t tput_len, const int32_t* S, double* best,
+                              int64_t* stage_j, int64_t* stage_counts);
+
+/* ---- timing: device milliseconds of the last call of each stage ---------- */
+int coral_s1_stage_ms(const coral_s1_handle* h, double* tables_ms, double* enumerate_ms,
+                      double* evaluate_ms, double* frontier_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CORAL_S1_H */

@@ -1,0 +1,320 @@
+"""ctypes binding of the C ABI in include/coral_s1.h (libcoral_s1.so, built in-tree).
+
+There is no fallback: if the shared library is missing or no CUDA device is usable,
+every entry point raises. The product path is the CUDA path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .specs import DomainError
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libcoral_s1.so")
+
+OK, EINVAL, ENOTEMPLATE, ECUDA, EUNSUPPORTED = 0, 1, 2, 3, 4
+PHASE_CODE = {"prefill": 0, "decode": 1}
+MAX_NODES = 6
+NEG_INF = -1e300
+
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_f64p = C.POINTER(C.c_double)
+_u64p = C.POINTER(C.c_uint64)
+
+
+class Problem(C.Structure):
+    _fields_ = [
+        ("num_configs", C.c_int32), ("cfg_gpu_count", _i32p), ("cfg_mem_gb", _f64p),
+        ("cfg_bw_tbps", _f64p), ("cfg_tflops", _f64p), ("cfg_str_rank", _i32p),
+        ("num_models", C.c_int32), ("mdl_num_layers", _i32p), ("mdl_granularity", _i32p),
+        ("mdl_params_total_b", _f64p), ("mdl_params_active_b", _f64p),
+        ("mdl_hidden_size", _f64p), ("mdl_bytes_per_param", _f64p), ("mdl_kv_bytes", _f64p),
+        ("slo_prefill_ms", _f64p), ("slo_decode_ms", _f64p),
+        ("num_phases", C.c_int32), ("phases", _i32p),
+        ("mfu", C.c_double), ("mbu", C.c_double), ("net_eff", C.c_double),
+        ("fixed_overhead_ms", C.c_double), ("avg_prompt_tokens", C.c_double),
+        ("avg_ctx_tokens", C.c_double), ("slo_budget_frac", C.c_double),
+        ("net_gbps", C.c_double), ("net_latency_ms", C.c_double),
+        ("n_max", C.c_int32), ("rho", C.c_double),
+        ("num_profile", C.c_int32), ("prof_model", _i32p), ("prof_phase", _i32p),
+        ("prof_cfg", _i32p), ("prof_j", _i32p), ("prof_bucket", _i32p), ("prof_tps", _f64p),
+    ]
+
+
+RECORD_DTYPE = np.dtype([("throughput_tps", "<f8"), ("num_stages", "u1"), ("num_nodes", "u1"),
+                         ("layers_per_stage", "<u2", (MAX_NODES,)),
+                         ("stage_of_node", "u1", (MAX_NODES,)), ("_pad", "u1", (2,))], align=True)
+FRONTIER_DTYPE = np.dtype([("price_usd_h", "<f8"), ("throughput_tps", "<f8"),
+                           ("combo_key", "<u8"), ("mp", "<i4"), ("region", "<i4"),
+                           ("rec", RECORD_DTYPE)], align=True)
+assert RECORD_DTYPE.itemsize == 32 and FRONTIER_DTYPE.itemsize == 64
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def _ptr(arr, ctype):
+    return arr.ctypes.data_as(C.POINTER(ctype))
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load libcoral_s1.so (raises if it was not built)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} missing: run `python __graft_entry__.py build` "
+                              "(the CUDA extension is the only implementation)")
+        lib = C.CDLL(_LIB_PATH)
+        vp = C.c_void_p
+        sig = {
+            "coral_s1_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+            "coral_s1_destroy": (C.c_int, [vp]),
+            "coral_s1_last_error": (C.c_char_p, []),
+            "coral_s1_version": (C.c_int, []),
+            "coral_s1_set_stream": (C.c_int, [vp, vp]),
+            "coral_s1_launch_count": (C.c_int64, [vp]),
+            "coral_s1_set_problem": (C.c_int, [vp, C.POINTER(Problem)]),
+            "coral_s1_tables": (C.c_int, [vp]),
+            "coral_s1_table_layout": (C.c_int, [vp, _i64p, _i32p, _i32p]),
+            "coral_s1_get_tables": (C.c_int, [vp, _f64p, C.c_int64]),
+            "coral_s1_get_budgets": (C.c_int, [vp, _f64p, C.c_int64]),
+            "coral_s1_enumerate": (C.c_int, [vp]),
+            "coral_s1_num_combos": (C.c_int, [vp, _i64p]),
+            "coral_s1_get_combos": (C.c_int, [vp, C.c_int, C.c_int, _u64p, C.c_int64]),
+            "coral_s1_evaluate": (C.c_int, [vp, C.c_int64, C.c_int64]),
+            "coral_s1_evaluate_shard": (C.c_int, [vp, C.c_int, C.c_int]),
+            "coral_s1_num_candidates": (C.c_int, [vp, _i64p]),
+            "coral_s1_get_records": (C.c_int, [vp, C.c_int, vp, C.c_int64]),
+            "coral_s1_frontier": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
+            "coral_s1_get_frontier": (C.c_int, [vp, vp, C.c_int64]),
+            "coral_s1_frontier_export_device": (C.c_int, [vp, vp, C.c_int64, _i64p]),
+            "coral_s1_frontier_merge_device": (C.c_int, [vp, vp, C.c_int64, _i64p]),
+            "coral_s1_placement_search": (C.c_int, [vp, C.c_int64, _i32p, _i64p, _i32p, _i64p,
+                                                    _f64p, C.c_int64, _i32p, _f64p, _i64p, _i64p]),
+            "coral_s1_stage_ms": (C.c_int, [vp, _f64p, _f64p, _f64p, _f64p]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def exported_symbols() -> list:
+    """Every coral_s1_* function declared in include/coral_s1.h."""
+    import re
+    hdr = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "include", "coral_s1.h")
+    with open(hdr) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"\b(coral_s1_[a-z_0-9]+)\s*\(", text)))
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+class LibraryGenErrorNative(RuntimeError):
+    pass
+
+
+def _check(rc: int) -> None:
+    if rc == OK:
+        return
+    msg = load().coral_s1_last_error().decode(errors="replace")
+    if rc == EINVAL:
+        raise DomainError(msg)
+    if rc == EUNSUPPORTED:
+        raise DomainError(f"outside the GPU path's envelope: {msg}")
+    if rc == ENOTEMPLATE:
+        raise LibraryGenErrorNative(msg)
+    raise NativeError(msg)
+
+
+class Handle:
+    """One device context (coral_s1_create/destroy) bound to torch's current stream."""
+
+    def __init__(self, device: int = 0):
+        lib = load()
+        self._lib = lib
+        self.device = device
+        h = C.c_void_p()
+        _check(lib.coral_s1_create(device, C.byref(h)))
+        self._h = h
+        self._keep = []
+        self.NM = self.NP = self.K = 0
+
+    def close(self):
+        if self._h:
+            self._lib.coral_s1_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int):
+        _check(self._lib.coral_s1_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    @property
+    def launches(self) -> int:
+        return int(self._lib.coral_s1_launch_count(self._h))
+
+    def set_problem(self, arrays: dict, scalars: dict):
+        p = Problem()
+        keep = []
+        for name, ctype in (("cfg_gpu_count", C.c_int32), ("cfg_mem_gb", C.c_double),
+                            ("cfg_bw_tbps", C.c_double), ("cfg_tflops", C.c_double),
+                            ("cfg_str_rank", C.c_int32), ("mdl_num_layers", C.c_int32),
+                            ("mdl_granularity", C.c_int32), ("mdl_params_total_b", C.c_double),
+                            ("mdl_params_active_b", C.c_double), ("mdl_hidden_size", C.c_double),
+                            ("mdl_bytes_per_param", C.c_double), ("mdl_kv_bytes", C.c_double),
+                            ("slo_prefill_ms", C.c_double), ("slo_decode_ms", C.c_double),
+                            ("phases", C.c_int32), ("prof_model", C.c_int32),
+                            ("prof_phase", C.c_int32), ("prof_cfg", C.c_int32),
+                            ("prof_j", C.c_int32), ("prof_bucket", C.c_int32),
+                            ("prof_tps", C.c_double)):
+            dt = np.int32 if ctype is C.c_int32 else np.float64
+            arr = np.ascontiguousarray(arrays[name], dtype=dt)
+            if arr.size == 0:
+                arr = np.zeros(1, dtype=dt)
+            keep.append(arr)
+            setattr(p, name, _ptr(arr, ctype))
+        for name, value in scalars.items():
+            setattr(p, name, value)
+        self._keep = keep
+        self.NM, self.NP, self.K = p.num_models, p.num_phases, p.num_configs
+        self.n_max = p.n_max
+        _check(self._lib.coral_s1_set_problem(self._h, C.byref(p)))
+
+    def tables(self):
+        _check(self._lib.coral_s1_tables(self._h))
+
+    def table_layout(self):
+        offs = np.zeros(self.NM * self.NP + 1, dtype=np.int64)
+        ls = np.zeros(max(self.NM, 1), dtype=np.int32)
+        sm = np.zeros(max(self.NM, 1), dtype=np.int32)
+        _check(self._lib.coral_s1_table_layout(self._h, _ptr(offs, C.c_int64), _ptr(ls, C.c_int32),
+                                               _ptr(sm, C.c_int32)))
+        return offs, ls[:self.NM], sm[:self.NM]
+
+    def get_tables(self):
+        offs, ls, sm = self.table_layout()
+        out = np.zeros(max(int(offs[-1]), 1))
+        _check(self._lib.coral_s1_get_tables(self._h, _ptr(out, C.c_double), out.size))
+        return out, offs, ls
+
+    def get_budgets(self):
+        out = np.zeros(max(self.NM * self.NP * self.n_max, 1))
+        _check(self._lib.coral_s1_get_budgets(self._h, _ptr(out, C.c_double), out.size))
+        return out[:self.NM * self.NP * self.n_max].reshape(self.NM * self.NP, self.n_max)
+
+    def enumerate(self):
+        _check(self._lib.coral_s1_enumerate(self._h))
+
+    def num_combos(self):
+        out = np.zeros(max(self.NM, 1), dtype=np.int64)
+        _check(self._lib.coral_s1_num_combos(self._h, _ptr(out, C.c_int64)))
+        return out[:self.NM]
+
+    def get_combos(self, model: int, enumeration_order: bool = False, count=None):
+        if count is None:
+            count = int(self.num_combos()[model])
+        out = np.zeros(max(count, 1), dtype=np.uint64)
+        _check(self._lib.coral_s1_get_combos(self._h, model, int(enumeration_order),
+                                             _ptr(out, C.c_uint64), out.size))
+        return out[:count]
+
+    def evaluate(self, lo: int = 0, hi: int = -1):
+        _check(self._lib.coral_s1_evaluate(self._h, lo, hi))
+
+    def evaluate_shard(self, rank: int, world: int):
+        _check(self._lib.coral_s1_evaluate_shard(self._h, rank, world))
+
+    def num_candidates(self) -> int:
+        n = C.c_int64()
+        _check(self._lib.coral_s1_num_candidates(self._h, C.byref(n)))
+        return n.value
+
+    def get_records(self, mp: int, count: int):
+        out = np.zeros(max(count, 1), dtype=RECORD_DTYPE)
+        _check(self._lib.coral_s1_get_records(self._h, mp, out.ctypes.data_as(C.c_void_p), out.size))
+        return out[:count]
+
+    def frontier(self, prices: np.ndarray) -> int:
+        prices = np.ascontiguousarray(prices, dtype=np.float64)
+        n = C.c_int64()
+        _check(self._lib.coral_s1_frontier(self._h, prices.shape[0], _ptr(prices, C.c_double),
+                                           C.byref(n)))
+        return n.value
+
+    def get_frontier(self, count: int):
+        out = np.zeros(max(count, 1), dtype=FRONTIER_DTYPE)
+        _check(self._lib.coral_s1_get_frontier(self._h, out.ctypes.data_as(C.c_void_p), out.size))
+        return out[:count]
+
+    def frontier_export_device(self, dev_ptr: int, cap: int) -> int:
+        n = C.c_int64()
+        _check(self._lib.coral_s1_frontier_export_device(self._h, C.c_void_p(dev_ptr), cap, C.byref(n)))
+        return n.value
+
+    def frontier_merge_device(self, dev_ptr: int, n_items: int) -> int:
+        n = C.c_int64()
+        _check(self._lib.coral_s1_frontier_merge_device(self._h, C.c_void_p(dev_ptr), n_items,
+                                                        C.byref(n)))
+        return n.value
+
+    def placement_search(self, ncfg, counts, lsteps, tput_off, tput, S):
+        ncases = len(ncfg)
+        ncfg = np.ascontiguousarray(ncfg, dtype=np.int32)
+        counts = np.ascontiguousarray(counts, dtype=np.int64)
+        lsteps = np.ascontiguousarray(lsteps, dtype=np.int32)
+        tput_off = np.ascontiguousarray(tput_off, dtype=np.int64)
+        tput = np.ascontiguousarray(tput, dtype=np.float64)
+        S = np.ascontiguousarray(S, dtype=np.int32)
+        best = np.zeros(ncases)
+        sj = np.zeros((ncases, MAX_NODES), dtype=np.int64)
+        sc = np.zeros((ncases, MAX_NODES, MAX_NODES), dtype=np.int64)
+        tp = tput if tput.size else np.zeros(1)
+        _check(self._lib.coral_s1_placement_search(
+            self._h, ncases, _ptr(ncfg, C.c_int32), _ptr(counts, C.c_int64), _ptr(lsteps, C.c_int32),
+            _ptr(tput_off, C.c_int64), _ptr(tp, C.c_double), tput.size, _ptr(S, C.c_int32),
+            _ptr(best, C.c_double), _ptr(sj, C.c_int64), _ptr(sc, C.c_int64)))
+        return best, sj, sc
+
+    def stage_ms(self) -> dict:
+        vals = [C.c_double() for _ in range(4)]
+        _check(self._lib.coral_s1_stage_ms(self._h, *[C.byref(v) for v in vals]))
+        return dict(zip(("tables", "enumerate", "evaluate", "frontier"), [v.value for v in vals]))
+
+
+_handles: dict = {}
+
+
+def handle(device: int | None = None) -> Handle:
+    """Process-wide handle per CUDA device, bound to torch's current stream."""
+    import torch
+    if not torch.cuda.is_available():
+        raise NativeError("no CUDA device: the stage-1 generator runs only on the GPU")
+    if device is None:
+        device = torch.cuda.current_device()
+    h = _handles.get(device)
+    if h is None:
+        h = Handle(device)
+        _handles[device] = h
+    h.set_stream(torch.cuda.current_stream(device).cuda_stream)
+    return h

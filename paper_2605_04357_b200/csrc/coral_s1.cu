@@ -1,0 +1,1147 @@
+// coral_s1.cu — B200-native stage-1 Serving-Template generator: kernels + C ABI.
+//
+// Pipeline (one stream):
+//   tables_kernel      T-hat rows per (model, phase, S, config)      templates.py:83-96
+//   enumerate_kernel   unrank multiset -> memory window -> key        templates.py:99-113
+//   segmented radix sort of keys per model (str(combo) order)         templates.py:112, 340
+//   evaluate_kernel    per candidate: DP for every S, best S, decode  templates.py:308-326
+//   frontier           price -> 4 stable radix passes -> segmented
+//                      running max -> compaction
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/coral_s1.h"
+#include "placement_dp.cuh"
+#include "roofline.cuh"
+
+using namespace coral;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(CORAL_S1_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+#define LAUNCH_CHECK(h)                                                               \
+  do {                                                                                \
+    (h)->launches++;                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                              \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(CORAL_S1_ECUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kKeyTokenBits = 9;
+constexpr unsigned long long kNoCombo = ~0ull;
+
+__constant__ unsigned long long c_binom[160][8];  // C(N, k), N < 160, k <= 7
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) return fail(CORAL_S1_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    cap = want;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct coral_s1_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  long long launches = 0;
+  bool have_problem = false, have_tables = false, have_enum = false, have_eval = false;
+  // host copy of the problem shape
+  int K = 0, NM = 0, NP = 0, n_max = 0;
+  std::vector<int> L, g, Lu, smax, phases;
+  std::vector<int64_t> tab_off;  // [NM*NP + 1]
+  int maxLu = 0;
+  int64_t U = 0;                 // multiset universe size per model
+  std::vector<int64_t> counts;   // combos per model
+  std::vector<int64_t> cand_off; // [NM*NP + 1]
+  int64_t ncand = 0;
+  int64_t nfront = 0;
+  int num_regions = 0;
+  DevProblem dp{};
+  // device buffers
+  DevBuf prob, tab, flags, budget, keys_raw, keys, seg_off, nvalid, cand_off_d, rec, cub_tmp;
+  DevBuf items, items_sorted, sort_a, sort_b, perm_a, perm_b, segk, scanv, flagsel, nsel, front,
+      prices, enum_tmp;
+  DevBuf op_in, op_out, tab_off_d;
+  cudaEvent_t ev[8] = {};
+  float ms[4] = {0, 0, 0, 0};
+};
+
+namespace {
+
+// --------------------------------------------------------------------------------
+// T-hat tables. One block per (mp, S, config); threads over layer units jj.
+// Also the per-row monotone flags kernels.py:291 needs:
+//   bit0: all(diff <= 1e-12) (the reference's test), bit1: all(diff <= 0).
+// --------------------------------------------------------------------------------
+__global__ void tables_kernel(DevProblem P, const int64_t* __restrict__ tab_off,
+                              double* __restrict__ tab, unsigned char* __restrict__ flags,
+                              double* __restrict__ budgets) {
+  const int c = blockIdx.x;
+  const int S = blockIdx.y + 1;
+  const int mp = blockIdx.z;
+  const int m = mp / P.NP;
+  const int phase = P.phases[mp % P.NP];
+  if (S > P.smax[m]) return;
+  const int Lu = P.Lu[m];
+  const int g = P.g[m];
+  const double budget = stage_budget(P, m, phase, S);
+  if (c == 0 && threadIdx.x == 0) budgets[mp * P.n_max + (S - 1)] = budget;
+  double* row = tab + tab_off[mp] + ((int64_t)(S - 1) * P.K + c) * Lu;
+  for (int jj = threadIdx.x; jj < Lu; jj += blockDim.x) {
+    // templates.py:89-95: zeros when the budget is exhausted
+    row[jj] = (budget <= 0.0) ? 0.0 : node_max_throughput(P, c, m, phase, (jj + 1) * g, budget);
+  }
+  __syncthreads();
+  int tol = 1, exact = 1;
+  for (int jj = threadIdx.x; jj + 1 < Lu; jj += blockDim.x) {
+    const double d = rn_sub(row[jj + 1], row[jj]);  // np.diff
+    tol &= (d <= 1e-12);
+    exact &= (d <= 0.0);
+  }
+  tol = __syncthreads_and(tol);
+  exact = __syncthreads_and(exact);
+  if (threadIdx.x == 0)
+    flags[((int64_t)mp * P.n_max + (S - 1)) * P.K + c] = (unsigned char)(tol | (exact << 1));
+}
+
+// --------------------------------------------------------------------------------
+// Enumeration: thread per (model, universe rank). Universe = multisets of 1..n_max
+// of K configs, ranked size-major, lexicographic within a size (stars and bars).
+// --------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long binom(int N, int k) {
+  if (k < 0 || N < k) return 0ull;
+  return c_binom[N][k];
+}
+
+__global__ void enumerate_kernel(DevProblem P, int64_t U, unsigned long long* __restrict__ keys,
+                                 unsigned long long* __restrict__ nvalid) {
+  const int m = blockIdx.y;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool pass = false;
+  unsigned long long key = kNoCombo;
+  if (r < U) {
+    const int K = P.K;
+    int n = 1;
+    int64_t rr = r;
+    for (; n <= P.n_max; ++n) {
+      const int64_t cnt = (int64_t)binom(K + n - 1, n);
+      if (rr < cnt) break;
+      rr -= cnt;
+    }
+    // unrank combination b_0 < ... < b_{n-1} of [0, N), N = K + n - 1 (lexicographic)
+    const int N = K + n - 1;
+    int picks[kMaxC];
+    int v = 0;
+    for (int i = 0; i < n; ++i) {
+      for (;;) {
+        const int64_t c = (int64_t)binom(N - v - 1, n - i - 1);
+        if (rr < c) break;
+        rr -= c;
+        ++v;
+      }
+      picks[i] = v - i;  // non-decreasing config index (pool sorted by name)
+      ++v;
+    }
+    // templates.py:109 mem = sum(c.mem_bytes for c in pick): sequential, pick order
+    double mem = 0.0;
+    for (int i = 0; i < n; ++i) mem = rn_add(mem, P.mem_bytes[picks[i]]);
+    const double wbytes = rn_mul(rn_mul(P.ptb[m], 1e9), P.bpp[m]);
+    const double lo = wbytes;
+    const double hi = rn_mul(P.rho, wbytes);
+    if (lo <= mem && mem < hi) {
+      pass = true;
+      key = 0ull;
+      int ntok = 0;
+      int i = 0;
+      while (i < n) {
+        int j = i;
+        while (j < n && picks[j] == picks[i]) ++j;
+        const unsigned long long tok =
+            ((unsigned long long)P.rank1[picks[i]] << 3) | (unsigned long long)(j - i);
+        key = (key << kKeyTokenBits) | tok;
+        ++ntok;
+        i = j;
+      }
+      key <<= kKeyTokenBits * (kMaxC - ntok);
+    }
+  }
+  if (r < U) keys[(int64_t)m * U + r] = key;
+  const unsigned ballot = __ballot_sync(0xffffffffu, pass);
+  if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(nvalid + m, (unsigned long long)__popc(ballot));
+}
+
+__global__ void seg_offsets_kernel(int NM, int64_t U, const unsigned long long* nvalid,
+                                   int64_t* begin, int64_t* end) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < NM) {
+    begin[m] = (int64_t)m * U;
+    end[m] = (int64_t)m * U + U;
+  }
+}
+
+__device__ __forceinline__ int decode_key(const DevProblem& P, unsigned long long key,
+                                          int* cfg, int* cnt) {
+  int C = 0;
+  for (int t = 0; t < kMaxC; ++t) {
+    const unsigned tok = (unsigned)(key >> (kKeyTokenBits * (kMaxC - 1 - t))) & 511u;
+    if (!tok) break;
+    cfg[C] = P.inv_rank[(tok >> 3) - 1];
+    cnt[C] = tok & 7u;
+    ++C;
+  }
+  return C;
+}
+
+// --------------------------------------------------------------------------------
+// Evaluator: one CTA per candidate (model, phase, combo). templates.py:308-326 for
+// the S loop and best-S rule, kernels.py:143-276 for the DP, templates.py:209-228
+// for the canonical placement written to the record.
+// --------------------------------------------------------------------------------
+struct EvalArgs {
+  DevProblem P;
+  const unsigned long long* keys;  // sorted per model at m*U
+  int64_t U;
+  const int64_t* cand_off;         // [NMP+1]
+  int NMP;
+  int64_t lo, hi, stride;          // candidates lo, lo+stride, ... < hi
+  const double* tab;
+  const int64_t* tab_off;
+  const unsigned char* flags;
+  coral_s1_record* rec;            // indexed by global candidate index
+};
+
+__global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ DpShared sh;
+  __shared__ int s_mp, s_cfg[kMaxC];
+  __shared__ double s_best;
+  __shared__ coral_s1_record s_rec;
+  const int64_t ci = A.lo + (int64_t)blockIdx.x * A.stride;
+  if (ci >= A.hi) return;
+  const int tid = threadIdx.x;
+  const DevProblem& P = A.P;
+  if (tid == 0) {
+    int lo = 0, hi = A.NMP;  // last mp with cand_off[mp] <= ci
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (A.cand_off[mid] <= ci) lo = mid; else hi = mid;
+    }
+    s_mp = lo;
+    const int m = lo / P.NP;
+    const int64_t idx = ci - A.cand_off[lo];
+    int cfg[kMaxC], cnt[kMaxC];
+    const int C = decode_key(P, A.keys[(int64_t)m * A.U + idx], cfg, cnt);
+    sh.C = C;
+    for (int c = 0; c < C; ++c) { s_cfg[c] = cfg[c]; sh.cnt[c] = cnt[c]; }
+    sh.Lu = P.Lu[m];
+    sh.LuP = sh.Lu + 1;
+    s_best = kNegInf;
+    memset(&s_rec, 0, sizeof(s_rec));
+    s_rec.throughput_tps = kNegInf;
+  }
+  __syncthreads();
+  dp_setup_lattice(sh);
+  const int mp = s_mp;
+  const int m = mp / P.NP;
+  const int K = P.K;
+  const int Lu = sh.Lu, LuP = sh.LuP, C = sh.C, M = sh.M, n = sh.n;
+  const DpBuffers B = dp_carve(smem, M, LuP, Lu);
+  const int Smax = min(n, Lu);
+  for (int S = 1; S <= Smax; ++S) {
+    // tables[S][cfg_rows, :] (templates.py:320)
+    const double* base = A.tab + A.tab_off[mp] + (int64_t)(S - 1) * K * Lu;
+    for (int idx = tid; idx < C * Lu; idx += blockDim.x) {
+      const int c = idx / Lu;
+      const int jj = idx - c * Lu;
+      B.tputS[idx] = base[(int64_t)s_cfg[c] * Lu + jj];
+    }
+    if (tid == 0) {
+      int mono = 1;
+      for (int c = 0; c < C; ++c)
+        mono &= A.flags[((int64_t)mp * P.n_max + (S - 1)) * K + s_cfg[c]] & 1;
+      sh.mono = mono;
+    }
+    __syncthreads();
+    dp_build_value(sh, B);
+    __syncthreads();
+    double val;
+    if (S == 1) {
+      val = B.value[(M - 1) * LuP + Lu];  // f[1][L][full]
+      if (tid == 0) { sh.top_val = val; sh.top_u = M - 1; sh.top_j = Lu; }
+    } else {
+      dp_run(sh, B, S);
+      val = sh.top_val;
+    }
+    // templates.py:322: strictly better and > 1e-9 (ties keep the smaller S)
+    if (tid == 0 && val > s_best && val > 1e-9) {
+      s_best = val;
+      if (S == 1) { sh.stage_j[0] = Lu; sh.stage_u[0] = M - 1; }
+      else dp_decode(sh, B, S);
+      // canonical placement (templates.py:209-228): stages by (-j, -counts)
+      int order[kMaxC];
+      for (int s = 0; s < S; ++s) order[s] = s;
+      for (int a = 1; a < S; ++a) {  // stable insertion sort
+        const int x = order[a];
+        int b = a - 1;
+        while (b >= 0) {
+          const int y = order[b];
+          bool less;  // key(x) < key(y)
+          if (sh.stage_j[x] != sh.stage_j[y]) less = sh.stage_j[x] > sh.stage_j[y];
+          else {
+            less = false;
+            for (int c = 0; c < C; ++c) {
+              const int dx = sh.digits[sh.stage_u[x]][c], dy = sh.digits[sh.stage_u[y]][c];
+              if (dx != dy) { less = dx > dy; break; }
+            }
+          }
+          if (!less) break;
+          order[b + 1] = y;
+          --b;
+        }
+        order[b + 1] = x;
+      }
+      const int g = P.g[m];
+      int next_free[kMaxC];
+      int offc = 0;
+      for (int c = 0; c < C; ++c) { next_free[c] = offc; offc += sh.cnt[c]; }
+      s_rec.throughput_tps = val;
+      s_rec.num_stages = (unsigned char)S;
+      s_rec.num_nodes = (unsigned char)n;
+      for (int pos = 0; pos < kMaxC; ++pos) s_rec.layers_per_stage[pos] = 0;
+      for (int pos = 0; pos < S; ++pos) {
+        const int s = order[pos];
+        s_rec.layers_per_stage[pos] = (unsigned short)(sh.stage_j[s] * g);
+        for (int c = 0; c < C; ++c)
+          for (int k = 0; k < sh.digits[sh.stage_u[s]][c]; ++k)
+            s_rec.stage_of_node[next_free[c]++] = (unsigned char)pos;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) A.rec[ci] = s_rec;
+}
+
+// --------------------------------------------------------------------------------
+// placement_search operator (kernels.py:279-295), one CTA per case, raw outputs.
+// --------------------------------------------------------------------------------
+struct OpArgs {
+  const int* ncfg;
+  const long long* counts;  // [n*6]
+  const int* lsteps;
+  const long long* tput_off;
+  const double* tput;
+  const int* S;
+  double* best;
+  long long* stage_j;       // [n*6]
+  long long* stage_counts;  // [n*36]
+  int64_t ncases;
+};
+
+__global__ void __launch_bounds__(kDpThreads) placement_op_kernel(OpArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ DpShared sh;
+  const int64_t i = blockIdx.x;
+  if (i >= A.ncases) return;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    sh.C = A.ncfg[i];
+    for (int c = 0; c < sh.C; ++c) sh.cnt[c] = (int)A.counts[i * kMaxC + c];
+    sh.Lu = A.lsteps[i];
+    sh.LuP = sh.Lu + 1;
+  }
+  __syncthreads();
+  dp_setup_lattice(sh);
+  const int S = A.S[i];
+  const int Lu = sh.Lu, LuP = sh.LuP, C = sh.C, M = sh.M, n = sh.n;
+  for (int s = tid; s < kMaxC; s += blockDim.x) {
+    A.stage_j[i * kMaxC + s] = 0;
+    for (int c = 0; c < kMaxC; ++c) A.stage_counts[(i * kMaxC + s) * kMaxC + c] = 0;
+  }
+  if (S > n || S > Lu || S < 1) {  // kernels.py:174-175
+    if (tid == 0) A.best[i] = kNegInf;
+    return;
+  }
+  const DpBuffers B = dp_carve(smem, M, LuP, Lu);
+  const double* rows = A.tput + A.tput_off[i];
+  for (int idx = tid; idx < C * Lu; idx += blockDim.x) B.tputS[idx] = rows[idx];
+  __syncthreads();
+  if (tid == 0) {
+    int mono = 1;  // kernels.py:291
+    for (int c = 0; c < C; ++c)
+      for (int j = 0; j + 1 < Lu; ++j) mono &= (rn_sub(B.tputS[c * Lu + j + 1], B.tputS[c * Lu + j]) <= 1e-12);
+    sh.mono = mono;
+  }
+  dp_build_value(sh, B);
+  __syncthreads();
+  if (S == 1) {
+    if (tid == 0) { sh.top_val = B.value[(M - 1) * LuP + Lu]; sh.top_u = M - 1; sh.top_j = Lu; }
+    __syncthreads();
+  } else {
+    dp_run(sh, B, S);
+  }
+  if (tid == 0) {
+    const double best = sh.top_val;
+    if (best <= kNegInf / 2) { A.best[i] = kNegInf; return; }
+    if (S == 1) { sh.stage_j[0] = Lu; sh.stage_u[0] = M - 1; }
+    else dp_decode(sh, B, S);
+    A.best[i] = best;
+    for (int s = 0; s < S; ++s) {
+      A.stage_j[i * kMaxC + s] = sh.stage_j[s];
+      for (int c = 0; c < C; ++c) A.stage_counts[(i * kMaxC + s) * kMaxC + c] = sh.digits[sh.stage_u[s]][c];
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------
+// Frontier
+// --------------------------------------------------------------------------------
+struct FrontArgs {
+  DevProblem P;
+  const unsigned long long* keys;
+  int64_t U;
+  const int64_t* cand_off;
+  int NMP;
+  const coral_s1_record* rec;
+  int64_t ncand;
+  const double* prices;  // [R][K], NaN = not offered
+  int R;
+  coral_s1_frontier_item* items;
+  unsigned long long* nitems;
+};
+
+// allocation.py:91-98 _template_price, per (candidate, region)
+__global__ void frontier_items_kernel(FrontArgs A) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ci = t / A.R;
+  const int r = (int)(t - ci * A.R);
+  bool keep = false;
+  coral_s1_frontier_item it;
+  if (ci < A.ncand) {
+    const coral_s1_record rc = A.rec[ci];
+    if (rc.num_stages > 0) {
+      int lo = 0, hi = A.NMP;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (A.cand_off[mid] <= ci) lo = mid; else hi = mid;
+      }
+      const int m = lo / A.P.NP;
+      const unsigned long long key = A.keys[(int64_t)m * A.U + (ci - A.cand_off[lo])];
+      int cfg[kMaxC], cnt[kMaxC];
+      const int C = decode_key(A.P, key, cfg, cnt);
+      double total = 0.0;
+      bool priced = true;
+      for (int c = 0; c < C; ++c) {
+        const double p = A.prices[(int64_t)r * A.P.K + cfg[c]];
+        if (isnan(p)) { priced = false; break; }
+        total = rn_add(total, rn_mul((double)cnt[c], p));
+      }
+      if (priced) {
+        keep = true;
+        it.price_usd_h = total;
+        it.throughput_tps = rc.throughput_tps;
+        it.combo_key = key;
+        it.mp = lo;
+        it.region = r;
+        it.rec = rc;
+      }
+    }
+  }
+  const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+  if (!ballot) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == __ffs(ballot) - 1) base = atomicAdd(A.nitems, (unsigned long long)__popc(ballot));
+  base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
+  if (keep) A.items[base + __popc(ballot & ((1u << lane) - 1u))] = it;
+}
+
+// sort-key extraction for the 4 stable LSD passes
+__global__ void sortkey_kernel(const coral_s1_frontier_item* __restrict__ items,
+                               const unsigned* __restrict__ perm, int64_t n, int field, int R,
+                               unsigned long long* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const coral_s1_frontier_item& it = items[perm ? perm[i] : i];
+  unsigned long long k;
+  switch (field) {
+    case 0: k = it.combo_key; break;                                               // key asc
+    case 1: k = ~(unsigned long long)__double_as_longlong(it.throughput_tps); break; // T desc (T > 0)
+    case 2: k = (unsigned long long)__double_as_longlong(it.price_usd_h); break;     // p asc (p >= 0)
+    default: k = (unsigned long long)it.mp * (unsigned long long)R + (unsigned long long)it.region;
+  }
+  out[i] = k;
+}
+
+__global__ void iota_kernel(unsigned* p, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = (unsigned)i;
+}
+
+__global__ void gather_items_kernel(const coral_s1_frontier_item* __restrict__ in,
+                                    const unsigned* __restrict__ perm, int64_t n, int R,
+                                    coral_s1_frontier_item* __restrict__ out,
+                                    unsigned long long* __restrict__ seg, double* __restrict__ tv) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const coral_s1_frontier_item it = in[perm[i]];
+  out[i] = it;
+  seg[i] = (unsigned long long)it.mp * (unsigned long long)R + (unsigned long long)it.region;
+  tv[i] = it.throughput_tps;
+}
+
+struct MaxOp {
+  __device__ __forceinline__ double operator()(double a, double b) const { return b > a ? b : a; }
+};
+
+// keep iff T > running max of the earlier items of the segment (strict)
+__global__ void skyline_flags_kernel(const unsigned long long* __restrict__ seg,
+                                     const double* __restrict__ tv, const double* __restrict__ incl,
+                                     int64_t n, unsigned char* __restrict__ flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  flag[i] = (i == 0 || seg[i] != seg[i - 1] || tv[i] > incl[i - 1]) ? 1 : 0;
+}
+
+int ensure_tmp(coral_s1_handle* h, size_t bytes) { return h->cub_tmp.ensure(bytes); }
+
+// Frontier over n items already in h->items; survivors -> h->front, count -> h->nfront.
+int frontier_from_items(coral_s1_handle* h, int64_t n, int R) {
+  cudaStream_t st = h->stream;
+  h->nfront = 0;
+  if (n == 0) return 0;
+  int rc;
+  if ((rc = h->sort_a.ensure(n * 8)) || (rc = h->sort_b.ensure(n * 8)) ||
+      (rc = h->perm_a.ensure(n * 4)) || (rc = h->perm_b.ensure(n * 4)) ||
+      (rc = h->items_sorted.ensure(n * sizeof(coral_s1_frontier_item))) ||
+      (rc = h->segk.ensure(n * 8)) || (rc = h->scanv.ensure(n * 8)) ||
+      (rc = h->flagsel.ensure(n)) || (rc = h->nsel.ensure(16)))
+    return rc;
+  const int TB = 256;
+  const unsigned gb = (unsigned)((n + TB - 1) / TB);
+  unsigned* perm = h->perm_a.as<unsigned>();
+  unsigned* perm_out = h->perm_b.as<unsigned>();
+  iota_kernel<<<gb, TB, 0, st>>>(perm, n);
+  LAUNCH_CHECK(h);
+  const coral_s1_frontier_item* items = h->items.as<coral_s1_frontier_item>();
+  // LSD: key asc, T desc, price asc, segment asc (all stable)
+  const int nseg = h->NM * h->NP * R;
+  int seg_bits = 1;
+  while ((1ll << seg_bits) < (long long)nseg) ++seg_bits;
+  for (int field = 0; field < 4; ++field) {
+    sortkey_kernel<<<gb, TB, 0, st>>>(items, field == 0 ? nullptr : perm, n, field, R,
+                                      h->sort_a.as<unsigned long long>());
+    LAUNCH_CHECK(h);
+    const int end_bit = field == 3 ? seg_bits : (field == 0 ? kKeyTokenBits * kMaxC : 64);
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, h->sort_a.as<unsigned long long>(),
+                                    h->sort_b.as<unsigned long long>(), perm, perm_out, (int)n, 0,
+                                    end_bit, st);
+    if ((rc = ensure_tmp(h, tmp))) return rc;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, h->sort_a.as<unsigned long long>(),
+                                             h->sort_b.as<unsigned long long>(), perm, perm_out,
+                                             (int)n, 0, end_bit, st));
+    h->launches += 4;
+    std::swap(perm, perm_out);
+  }
+  coral_s1_frontier_item* sorted = h->items_sorted.as<coral_s1_frontier_item>();
+  gather_items_kernel<<<gb, TB, 0, st>>>(items, perm, n, R, sorted, h->segk.as<unsigned long long>(),
+                                         h->sort_a.as<double>());
+  LAUNCH_CHECK(h);
+  size_t tmp = 0;
+  cub::DeviceScan::InclusiveScanByKey(nullptr, tmp, h->segk.as<unsigned long long>(),
+                                      h->sort_a.as<double>(), h->scanv.as<double>(), MaxOp(),
+                                      (int)n, cub::Equality(), st);
+  if ((rc = ensure_tmp(h, tmp))) return rc;
+  CUDA_TRY(cub::DeviceScan::InclusiveScanByKey(h->cub_tmp.p, tmp, h->segk.as<unsigned long long>(),
+                                               h->sort_a.as<double>(), h->scanv.as<double>(),
+                                               MaxOp(), (int)n, cub::Equality(), st));
+  h->launches += 2;
+  skyline_flags_kernel<<<gb, TB, 0, st>>>(h->segk.as<unsigned long long>(), h->sort_a.as<double>(),
+                                          h->scanv.as<double>(), n, h->flagsel.as<unsigned char>());
+  LAUNCH_CHECK(h);
+  if ((rc = h->front.ensure(n * sizeof(coral_s1_frontier_item)))) return rc;
+  tmp = 0;
+  cub::DeviceSelect::Flagged(nullptr, tmp, sorted, h->flagsel.as<unsigned char>(),
+                             h->front.as<coral_s1_frontier_item>(), h->nsel.as<long long>(),
+                             (int)n, st);
+  if ((rc = ensure_tmp(h, tmp))) return rc;
+  CUDA_TRY(cub::DeviceSelect::Flagged(h->cub_tmp.p, tmp, sorted, h->flagsel.as<unsigned char>(),
+                                      h->front.as<coral_s1_frontier_item>(),
+                                      h->nsel.as<long long>(), (int)n, st));
+  h->launches += 2;
+  long long ns = 0;
+  CUDA_TRY(cudaMemcpyAsync(&ns, h->nsel.p, sizeof(ns), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  h->nfront = ns;
+  return 0;
+}
+
+template <class T>
+int upload(coral_s1_handle* h, DevBuf& buf, const std::vector<T>& v) {
+  int rc = buf.ensure(std::max<size_t>(v.size() * sizeof(T), 8));
+  if (rc) return rc;
+  if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+  return 0;
+}
+
+int64_t universe_size(int K, int n_max) {
+  // sum_{n=1}^{n_max} C(K+n-1, n)
+  int64_t tot = 0;
+  for (int n = 1; n <= n_max; ++n) {
+    long double c = 1;
+    for (int i = 1; i <= n; ++i) c = c * (K + n - 1 - n + i) / i;
+    tot += (int64_t)(c + 0.5L);
+  }
+  return tot;
+}
+
+}  // namespace
+
+// ================================================================================
+// C ABI
+// ================================================================================
+extern "C" {
+
+const char* coral_s1_last_error(void) { return g_err.c_str(); }
+int coral_s1_version(void) { return 1; }
+
+int coral_s1_create(int device, coral_s1_handle** out) {
+  if (!out) return fail(CORAL_S1_EINVAL, "out is null");
+  *out = nullptr;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(CORAL_S1_EINVAL, "bad device ordinal");
+  CUDA_TRY(cudaSetDevice(device));
+  auto* h = new coral_s1_handle();
+  h->device = device;
+  static unsigned long long tab[160][8];
+  for (int N = 0; N < 160; ++N)
+    for (int k = 0; k < 8; ++k) {
+      if (k > N) { tab[N][k] = 0; continue; }
+      unsigned long long c = 1;
+      for (int i = 1; i <= k; ++i) c = c * (unsigned long long)(N - k + i) / (unsigned long long)i;
+      tab[N][k] = c;
+    }
+  cudaError_t e = cudaMemcpyToSymbol(c_binom, tab, sizeof(tab));
+  if (e != cudaSuccess) { delete h; return fail(CORAL_S1_ECUDA, cudaGetErrorString(e)); }
+  for (auto& ev : h->ev) cudaEventCreate(&ev);
+  const size_t smem_max = dp_smem_bytes(kMaxM, CORAL_S1_MAX_LAYER_UNITS + 1, CORAL_S1_MAX_LAYER_UNITS);
+  cudaFuncSetAttribute(evaluate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+  cudaFuncSetAttribute(placement_op_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { delete h; return fail(CORAL_S1_ECUDA, cudaGetErrorString(e)); }
+  *out = h;
+  return 0;
+}
+
+int coral_s1_destroy(coral_s1_handle* h) {
+  if (!h) return 0;
+  cudaSetDevice(h->device);
+  DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->seg_off,
+                    &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
+                    &h->sort_a, &h->sort_b, &h->perm_a, &h->perm_b, &h->segk, &h->scanv,
+                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d};
+  for (DevBuf* b : bufs) b->release();
+  for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
+  delete h;
+  return 0;
+}
+
+int coral_s1_set_stream(coral_s1_handle* h, void* stream) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  h->stream = reinterpret_cast<cudaStream_t>(stream);
+  return 0;
+}
+
+int64_t coral_s1_launch_count(const coral_s1_handle* h) { return h ? h->launches : 0; }
+
+int coral_s1_set_problem(coral_s1_handle* h, const coral_s1_problem* p) {
+  if (!h || !p) return fail(CORAL_S1_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  // LibraryCaps.__post_init__ (templates.py:45-49)
+  if (p->n_max < 1) return fail(CORAL_S1_EINVAL, "n_max must be >= 1");
+  if (!(p->rho > 1)) return fail(CORAL_S1_EINVAL, "rho must be > 1");
+  if (p->n_max > CORAL_S1_MAX_NODES)
+    return fail(CORAL_S1_EUNSUPPORTED, "GPU path supports n_max <= 6");
+  if (p->num_configs < 0 || p->num_configs > CORAL_S1_MAX_CONFIGS)
+    return fail(CORAL_S1_EUNSUPPORTED, "GPU path supports <= 63 node configs");
+  if (p->num_models < 0 || p->num_phases < 0 || p->num_phases > 2)
+    return fail(CORAL_S1_EINVAL, "bad model/phase count");
+  const int K = p->num_configs, NM = p->num_models, NP = p->num_phases;
+  h->K = K; h->NM = NM; h->NP = NP; h->n_max = p->n_max;
+  h->L.assign(NM, 0); h->g.assign(NM, 1); h->Lu.assign(NM, 0); h->smax.assign(NM, 0);
+  h->phases.assign(p->phases, p->phases + NP);
+  for (int i = 0; i < NP; ++i)
+    if (h->phases[i] != CORAL_S1_PHASE_PREFILL && h->phases[i] != CORAL_S1_PHASE_DECODE)
+      return fail(CORAL_S1_EINVAL, "phase must be prefill or decode");
+  h->maxLu = 1;
+  for (int m = 0; m < NM; ++m) {
+    h->L[m] = p->mdl_num_layers[m];
+    h->g[m] = p->mdl_granularity[m];
+    if (h->L[m] < 1 || h->g[m] < 1) return fail(CORAL_S1_EINVAL, "num_layers and granularity must be >= 1");
+    h->Lu[m] = h->L[m] / h->g[m];
+    if (h->Lu[m] < 1) return fail(CORAL_S1_EINVAL, "granularity larger than num_layers");
+    if (h->Lu[m] > CORAL_S1_MAX_LAYER_UNITS)
+      return fail(CORAL_S1_EUNSUPPORTED, "GPU path supports <= 128 layer units per model");
+    h->smax[m] = std::min(p->n_max, h->L[m]);
+    h->maxLu = std::max(h->maxLu, h->Lu[m]);
+  }
+  h->tab_off.assign(NM * NP + 1, 0);
+  for (int mp = 0; mp < NM * NP; ++mp) {
+    const int m = mp / std::max(NP, 1);
+    h->tab_off[mp + 1] = h->tab_off[mp] + (int64_t)p->n_max * K * h->Lu[m];
+  }
+  std::vector<double> memb(K);
+  std::vector<int> inv(64, 0), rank1(K);
+  for (int c = 0; c < K; ++c) {
+    if (p->cfg_gpu_count[c] < 1) return fail(CORAL_S1_EINVAL, "gpu_count must be >= 1");
+    memb[c] = ((double)p->cfg_gpu_count[c] * p->cfg_mem_gb[c]) * 1073741824.0;
+    const int r = p->cfg_str_rank[c];
+    if (r < 0 || r >= K) return fail(CORAL_S1_EINVAL, "cfg_str_rank out of range");
+    rank1[c] = r + 1;
+    inv[r] = c;
+  }
+  // pack every array into one device blob
+  std::vector<unsigned char> blob;
+  auto put = [&](const void* src, size_t bytes) {
+    size_t off = (blob.size() + 15) & ~(size_t)15;
+    blob.resize(off + std::max<size_t>(bytes, 8));
+    if (bytes) memcpy(blob.data() + off, src, bytes);
+    return off;
+  };
+  std::vector<int> ph(h->phases);
+  const size_t o_gc = put(p->cfg_gpu_count, K * 4), o_mem = put(p->cfg_mem_gb, K * 8),
+               o_bw = put(p->cfg_bw_tbps, K * 8), o_tf = put(p->cfg_tflops, K * 8),
+               o_memb = put(memb.data(), K * 8), o_rank = put(rank1.data(), K * 4),
+               o_inv = put(inv.data(), 64 * 4), o_L = put(h->L.data(), NM * 4),
+               o_g = put(h->g.data(), NM * 4), o_Lu = put(h->Lu.data(), NM * 4),
+               o_smax = put(h->smax.data(), NM * 4), o_ptb = put(p->mdl_params_total_b, NM * 8),
+               o_pab = put(p->mdl_params_active_b, NM * 8), o_hid = put(p->mdl_hidden_size, NM * 8),
+               o_bpp = put(p->mdl_bytes_per_param, NM * 8), o_kv = put(p->mdl_kv_bytes, NM * 8),
+               o_spf = put(p->slo_prefill_ms, NM * 8), o_sdc = put(p->slo_decode_ms, NM * 8),
+               o_ph = put(ph.data(), NP * 4);
+  const int NPR = std::max(p->num_profile, 0);
+  const size_t o_pm = put(p->prof_model, NPR * 4), o_pp = put(p->prof_phase, NPR * 4),
+               o_pc = put(p->prof_cfg, NPR * 4), o_pj = put(p->prof_j, NPR * 4),
+               o_pb = put(p->prof_bucket, NPR * 4), o_pt = put(p->prof_tps, NPR * 8);
+  int rc = h->prob.ensure(blob.size());
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(h->prob.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, h->stream));
+  auto* b = h->prob.as<unsigned char>();
+  DevProblem& d = h->dp;
+  d.K = K; d.NM = NM; d.NP = NP; d.n_max = p->n_max; d.rho = p->rho;
+  d.gc = (const int*)(b + o_gc); d.mem_gb = (const double*)(b + o_mem);
+  d.bw = (const double*)(b + o_bw); d.tflops = (const double*)(b + o_tf);
+  d.mem_bytes = (const double*)(b + o_memb); d.rank1 = (const int*)(b + o_rank);
+  d.inv_rank = (const int*)(b + o_inv); d.L = (const int*)(b + o_L); d.g = (const int*)(b + o_g);
+  d.Lu = (const int*)(b + o_Lu); d.smax = (const int*)(b + o_smax);
+  d.ptb = (const double*)(b + o_ptb); d.pab = (const double*)(b + o_pab);
+  d.hidden = (const double*)(b + o_hid); d.bpp = (const double*)(b + o_bpp);
+  d.kv = (const double*)(b + o_kv); d.slo_pf = (const double*)(b + o_spf);
+  d.slo_dc = (const double*)(b + o_sdc); d.phases = (const int*)(b + o_ph);
+  d.mfu = p->mfu; d.mbu = p->mbu; d.net_eff = p->net_eff; d.fixed_ms = p->fixed_overhead_ms;
+  d.prompt = p->avg_prompt_tokens; d.ctxd = p->avg_ctx_tokens; d.frac = p->slo_budget_frac;
+  d.gbps = p->net_gbps; d.lat_ms = p->net_latency_ms;
+  d.nprof = NPR;
+  d.pm = (const int*)(b + o_pm); d.pp = (const int*)(b + o_pp); d.pc = (const int*)(b + o_pc);
+  d.pj = (const int*)(b + o_pj); d.pb = (const int*)(b + o_pb); d.pt = (const double*)(b + o_pt);
+  h->U = universe_size(K, p->n_max);
+  h->have_problem = true;
+  h->have_tables = h->have_enum = h->have_eval = false;
+  h->nfront = 0;
+  return 0;
+}
+
+int coral_s1_tables(coral_s1_handle* h) {
+  if (!h || !h->have_problem) return fail(CORAL_S1_EINVAL, "set_problem first");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const int NMP = h->NM * h->NP;
+  int rc;
+  if ((rc = h->tab.ensure(std::max<int64_t>(h->tab_off[NMP], 1) * 8)) ||
+      (rc = h->flags.ensure(std::max<int64_t>((int64_t)NMP * h->n_max * h->K, 1))) ||
+      (rc = h->budget.ensure(std::max<int64_t>((int64_t)NMP * h->n_max, 1) * 8)) ||
+      (rc = upload(h, h->tab_off_d, h->tab_off)))
+    return rc;
+  CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
+  if (NMP > 0 && h->K > 0) {
+    CUDA_TRY(cudaMemsetAsync(h->budget.p, 0, (size_t)NMP * h->n_max * 8, h->stream));
+    const int tpb = std::min(128, ((h->maxLu + 31) / 32) * 32);
+    dim3 grid(h->K, h->n_max, NMP);
+    tables_kernel<<<grid, tpb, 0, h->stream>>>(h->dp, h->tab_off_d.as<int64_t>(), h->tab.as<double>(),
+                                               h->flags.as<unsigned char>(), h->budget.as<double>());
+    LAUNCH_CHECK(h);
+  }
+  CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+  h->have_tables = true;
+  h->have_eval = false;
+  return 0;
+}
+
+int coral_s1_table_layout(const coral_s1_handle* h, int64_t* offsets, int32_t* lsteps,
+                          int32_t* smax) {
+  if (!h || !h->have_problem) return fail(CORAL_S1_EINVAL, "set_problem first");
+  const int NMP = h->NM * h->NP;
+  if (offsets) for (int i = 0; i <= NMP; ++i) offsets[i] = h->tab_off[i];
+  if (lsteps) for (int m = 0; m < h->NM; ++m) lsteps[m] = h->Lu[m];
+  if (smax) for (int m = 0; m < h->NM; ++m) smax[m] = h->smax[m];
+  return 0;
+}
+
+int coral_s1_get_tables(coral_s1_handle* h, double* out, int64_t n) {
+  if (!h || !h->have_tables) return fail(CORAL_S1_EINVAL, "tables not computed");
+  const int64_t tot = h->tab_off[h->NM * h->NP];
+  if (n < tot) return fail(CORAL_S1_EINVAL, "output too small");
+  if (tot) CUDA_TRY(cudaMemcpyAsync(out, h->tab.p, tot * 8, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int coral_s1_get_budgets(coral_s1_handle* h, double* out, int64_t n) {
+  if (!h || !h->have_tables) return fail(CORAL_S1_EINVAL, "tables not computed");
+  const int64_t tot = (int64_t)h->NM * h->NP * h->n_max;
+  if (n < tot) return fail(CORAL_S1_EINVAL, "output too small");
+  if (tot) CUDA_TRY(cudaMemcpyAsync(out, h->budget.p, tot * 8, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int coral_s1_enumerate(coral_s1_handle* h) {
+  if (!h || !h->have_problem) return fail(CORAL_S1_EINVAL, "set_problem first");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const int NM = h->NM;
+  const int64_t U = h->U;
+  const int64_t tot = std::max<int64_t>((int64_t)NM * U, 1);
+  int rc;
+  if ((rc = h->keys_raw.ensure(tot * 8)) || (rc = h->keys.ensure(tot * 8)) ||
+      (rc = h->nvalid.ensure(std::max(NM, 1) * 8)) || (rc = h->seg_off.ensure(std::max(NM, 1) * 16)))
+    return rc;
+  cudaStream_t st = h->stream;
+  CUDA_TRY(cudaEventRecord(h->ev[2], st));
+  h->counts.assign(NM, 0);
+  if (NM > 0 && U > 0) {
+    CUDA_TRY(cudaMemsetAsync(h->nvalid.p, 0, NM * 8, st));
+    dim3 grid((unsigned)((U + 255) / 256), NM);
+    enumerate_kernel<<<grid, 256, 0, st>>>(h->dp, U, h->keys_raw.as<unsigned long long>(),
+                                           h->nvalid.as<unsigned long long>());
+    LAUNCH_CHECK(h);
+    int64_t* beg = h->seg_off.as<int64_t>();
+    int64_t* end = beg + NM;
+    seg_offsets_kernel<<<(NM + 127) / 128, 128, 0, st>>>(NM, U, h->nvalid.as<unsigned long long>(), beg, end);
+    LAUNCH_CHECK(h);
+    size_t tmp = 0;
+    cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp, h->keys_raw.as<unsigned long long>(),
+                                            h->keys.as<unsigned long long>(), (int)(NM * U), NM, beg,
+                                            end, 0, 64, st);
+    if ((rc = ensure_tmp(h, tmp))) return rc;
+    CUDA_TRY(cub::DeviceSegmentedRadixSort::SortKeys(h->cub_tmp.p, tmp, h->keys_raw.as<unsigned long long>(),
+                                                     h->keys.as<unsigned long long>(), (int)(NM * U), NM,
+                                                     beg, end, 0, 64, st));
+    h->launches += 4;
+    std::vector<unsigned long long> nv(NM);
+    CUDA_TRY(cudaMemcpyAsync(nv.data(), h->nvalid.p, NM * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int m = 0; m < NM; ++m) h->counts[m] = (int64_t)nv[m];
+  }
+  CUDA_TRY(cudaEventRecord(h->ev[3], st));
+  // candidate list: mp-major, library order within each (model, phase)
+  const int NMP = NM * h->NP;
+  h->cand_off.assign(NMP + 1, 0);
+  for (int mp = 0; mp < NMP; ++mp) h->cand_off[mp + 1] = h->cand_off[mp] + h->counts[mp / h->NP];
+  h->ncand = h->cand_off[NMP];
+  if ((rc = upload(h, h->cand_off_d, h->cand_off))) return rc;
+  h->have_enum = true;
+  h->have_eval = false;
+  return 0;
+}
+
+int coral_s1_num_combos(const coral_s1_handle* h, int64_t* counts) {
+  if (!h || !h->have_enum) return fail(CORAL_S1_EINVAL, "enumerate first");
+  for (int m = 0; m < h->NM; ++m) counts[m] = h->counts[m];
+  return 0;
+}
+
+int coral_s1_get_combos(coral_s1_handle* h, int model, int enumeration_order, uint64_t* keys,
+                        int64_t n) {
+  if (!h || !h->have_enum) return fail(CORAL_S1_EINVAL, "enumerate first");
+  if (model < 0 || model >= h->NM) return fail(CORAL_S1_EINVAL, "bad model index");
+  const int64_t cnt = h->counts[model];
+  if (n < cnt) return fail(CORAL_S1_EINVAL, "output too small");
+  if (cnt)
+    CUDA_TRY(cudaMemcpyAsync(keys, h->keys.as<unsigned long long>() + (int64_t)model * h->U, cnt * 8,
+                             cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (enumeration_order) {
+    // templates.py:112 (num_nodes, str): stable partition of the str-sorted list
+    std::stable_sort(keys, keys + cnt, [](uint64_t a, uint64_t b) {
+      auto nodes = [](uint64_t k) {
+        int s = 0;
+        for (int t = 0; t < kMaxC; ++t) s += (int)((k >> (kKeyTokenBits * t)) & 7u);
+        return s;
+      };
+      return nodes(a) < nodes(b);
+    });
+  }
+  return 0;
+}
+
+int coral_s1_num_candidates(const coral_s1_handle* h, int64_t* n) {
+  if (!h || !h->have_enum) return fail(CORAL_S1_EINVAL, "enumerate first");
+  *n = h->ncand;
+  return 0;
+}
+
+static int evaluate_impl(coral_s1_handle* h, int64_t lo, int64_t hi, int64_t stride) {
+  if (!h || !h->have_tables || !h->have_enum) return fail(CORAL_S1_EINVAL, "tables and enumerate first");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (hi < 0 || hi > h->ncand) hi = h->ncand;
+  if (lo < 0) lo = 0;
+  if (stride < 1) return fail(CORAL_S1_EINVAL, "stride must be >= 1");
+  int rc;
+  if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record)))) return rc;
+  cudaStream_t st = h->stream;
+  // records not evaluated by this call read as infeasible (num_stages 0)
+  CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), st));
+  CUDA_TRY(cudaEventRecord(h->ev[4], st));
+  if (hi > lo) {
+    EvalArgs A;
+    A.P = h->dp;
+    A.keys = h->keys.as<unsigned long long>();
+    A.U = h->U;
+    A.cand_off = h->cand_off_d.as<int64_t>();
+    A.NMP = h->NM * h->NP;
+    A.hi = hi;
+    A.stride = stride;
+    A.tab = h->tab.as<double>();
+    A.tab_off = h->tab_off_d.as<int64_t>();
+    A.flags = h->flags.as<unsigned char>();
+    A.rec = h->rec.as<coral_s1_record>();
+    const size_t smem = dp_smem_bytes(kMaxM, h->maxLu + 1, h->maxLu);
+    const int64_t nblocks = (hi - lo + stride - 1) / stride;
+    const int64_t chunk = 1ll << 30;
+    for (int64_t b0 = 0; b0 < nblocks; b0 += chunk) {
+      A.lo = lo + b0 * stride;
+      const int64_t nb = std::min(chunk, nblocks - b0);
+      evaluate_kernel<<<(unsigned)nb, kDpThreads, smem, st>>>(A);
+      LAUNCH_CHECK(h);
+    }
+  }
+  CUDA_TRY(cudaEventRecord(h->ev[5], st));
+  h->have_eval = true;
+  return 0;
+}
+
+int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi) { return evaluate_impl(h, lo, hi, 1); }
+
+int coral_s1_evaluate_shard(coral_s1_handle* h, int rank, int world) {
+  if (world < 1 || rank < 0 || rank >= world) return fail(CORAL_S1_EINVAL, "bad rank/world");
+  return evaluate_impl(h, rank, -1, world);
+}
+
+int coral_s1_get_records(coral_s1_handle* h, int mp, coral_s1_record* out, int64_t n) {
+  if (!h || !h->have_eval) return fail(CORAL_S1_EINVAL, "evaluate first");
+  if (mp < 0 || mp >= h->NM * h->NP) return fail(CORAL_S1_EINVAL, "bad mp index");
+  const int64_t cnt = h->cand_off[mp + 1] - h->cand_off[mp];
+  if (n < cnt) return fail(CORAL_S1_EINVAL, "output too small");
+  if (cnt)
+    CUDA_TRY(cudaMemcpyAsync(out, h->rec.as<coral_s1_record>() + h->cand_off[mp],
+                             cnt * sizeof(coral_s1_record), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices, int64_t* num_survivors) {
+  if (!h || !h->have_eval) return fail(CORAL_S1_EINVAL, "evaluate first");
+  if (num_regions < 0) return fail(CORAL_S1_EINVAL, "num_regions < 0");
+  CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  h->num_regions = num_regions;
+  CUDA_TRY(cudaEventRecord(h->ev[6], st));
+  const int64_t nmax = h->ncand * num_regions;
+  int rc;
+  std::vector<double> pv(prices, prices + (size_t)num_regions * h->K);
+  if ((rc = upload(h, h->prices, pv)) ||
+      (rc = h->items.ensure(std::max<int64_t>(nmax, 1) * sizeof(coral_s1_frontier_item))) ||
+      (rc = h->nsel.ensure(16)))
+    return rc;
+  int64_t n = 0;
+  if (nmax > 0) {
+    CUDA_TRY(cudaMemsetAsync(h->nsel.p, 0, 8, st));
+    FrontArgs A;
+    A.P = h->dp;
+    A.keys = h->keys.as<unsigned long long>();
+    A.U = h->U;
+    A.cand_off = h->cand_off_d.as<int64_t>();
+    A.NMP = h->NM * h->NP;
+    A.rec = h->rec.as<coral_s1_record>();
+    A.ncand = h->ncand;
+    A.prices = h->prices.as<double>();
+    A.R = num_regions;
+    A.items = h->items.as<coral_s1_frontier_item>();
+    A.nitems = h->nsel.as<unsigned long long>();
+    frontier_items_kernel<<<(unsigned)((nmax + 255) / 256), 256, 0, st>>>(A);
+    LAUNCH_CHECK(h);
+    unsigned long long ni = 0;
+    CUDA_TRY(cudaMemcpyAsync(&ni, h->nsel.p, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    n = (int64_t)ni;
+  }
+  if ((rc = frontier_from_items(h, n, num_regions))) return rc;
+  CUDA_TRY(cudaEventRecord(h->ev[7], st));
+  if (num_survivors) *num_survivors = h->nfront;
+  return 0;
+}
+
+int coral_s1_get_frontier(coral_s1_handle* h, coral_s1_frontier_item* out, int64_t n) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  if (n < h->nfront) return fail(CORAL_S1_EINVAL, "output too small");
+  if (h->nfront)
+    CUDA_TRY(cudaMemcpyAsync(out, h->front.p, h->nfront * sizeof(coral_s1_frontier_item),
+                             cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int coral_s1_frontier_export_device(coral_s1_handle* h, void* dev_items, int64_t cap, int64_t* n) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  if (n) *n = h->nfront;
+  if (cap < h->nfront) return fail(CORAL_S1_EINVAL, "export capacity too small");
+  if (h->nfront)
+    CUDA_TRY(cudaMemcpyAsync(dev_items, h->front.p, h->nfront * sizeof(coral_s1_frontier_item),
+                             cudaMemcpyDeviceToDevice, h->stream));
+  return 0;
+}
+
+int coral_s1_frontier_merge_device(coral_s1_handle* h, const void* dev_items, int64_t n,
+                                   int64_t* num_survivors) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  int rc;
+  if ((rc = h->items.ensure(std::max<int64_t>(n, 1) * sizeof(coral_s1_frontier_item)))) return rc;
+  if (n)
+    CUDA_TRY(cudaMemcpyAsync(h->items.p, dev_items, n * sizeof(coral_s1_frontier_item),
+                             cudaMemcpyDeviceToDevice, h->stream));
+  if ((rc = frontier_from_items(h, n, h->num_regions))) return rc;
+  if (num_survivors) *num_survivors = h->nfront;
+  return 0;
+}
+
+int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t* ncfg,
+                              const int64_t* counts, const int32_t* lsteps, const int64_t* tput_off,
+                              const double* tput, int64_t tput_len, const int32_t* S, double* best,
+                              int64_t* stage_j, int64_t* stage_counts) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  if (ncases <= 0) return 0;
+  CUDA_TRY(cudaSetDevice(h->device));
+  int maxLu = 1;
+  for (int64_t i = 0; i < ncases; ++i) {
+    if (ncfg[i] < 1 || ncfg[i] > kMaxC) return fail(CORAL_S1_EUNSUPPORTED, "placement_search: 1..6 configs");
+    long long M = 1;
+    for (int c = 0; c < ncfg[i]; ++c) {
+      if (counts[i * kMaxC + c] < 0) return fail(CORAL_S1_EINVAL, "negative count");
+      M *= counts[i * kMaxC + c] + 1;
+    }
+    if (M > kMaxM) return fail(CORAL_S1_EUNSUPPORTED, "placement_search: prod(counts+1) must be <= 64");
+    if (lsteps[i] < 1 || lsteps[i] > CORAL_S1_MAX_LAYER_UNITS)
+      return fail(CORAL_S1_EUNSUPPORTED, "placement_search: 1..128 layer units");
+    if (tput_off[i] < 0 || tput_off[i] + (int64_t)ncfg[i] * lsteps[i] > tput_len)
+      return fail(CORAL_S1_EINVAL, "tput offset out of range");
+    maxLu = std::max(maxLu, (int)lsteps[i]);
+  }
+  for (int64_t i = 0; i < tput_len; ++i)
+    if (tput[i] < 0) return fail(CORAL_S1_EINVAL, "throughput table must be non-negative");
+  cudaStream_t st = h->stream;
+  // pack inputs: ncfg | lsteps | S | counts | tput_off | tput
+  const size_t b_ncfg = ncases * 4, b_counts = ncases * kMaxC * 8, b_off = ncases * 8,
+               b_tput = std::max<int64_t>(tput_len, 1) * 8;
+  size_t o = 0;
+  const size_t o_ncfg = o; o += (b_ncfg + 15) & ~15ull;
+  const size_t o_ls = o; o += (b_ncfg + 15) & ~15ull;
+  const size_t o_S = o; o += (b_ncfg + 15) & ~15ull;
+  const size_t o_cnt = o; o += (b_counts + 15) & ~15ull;
+  const size_t o_off = o; o += (b_off + 15) & ~15ull;
+  const size_t o_tp = o; o += b_tput;
+  const size_t ob_best = 0, ob_sj = (ncases * 8 + 15) & ~15ull,
+               ob_sc = ob_sj + ((ncases * kMaxC * 8 + 15) & ~15ull),
+               ob_end = ob_sc + ncases * kMaxC * kMaxC * 8;
+  int rc;
+  if ((rc = h->op_in.ensure(o)) || (rc = h->op_out.ensure(ob_end))) return rc;
+  auto* in = h->op_in.as<unsigned char>();
+  CUDA_TRY(cudaMemcpyAsync(in + o_ncfg, ncfg, b_ncfg, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(in + o_ls, lsteps, b_ncfg, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(in + o_S, S, b_ncfg, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(in + o_cnt, counts, b_counts, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(in + o_off, tput_off, b_off, cudaMemcpyHostToDevice, st));
+  if (tput_len) CUDA_TRY(cudaMemcpyAsync(in + o_tp, tput, tput_len * 8, cudaMemcpyHostToDevice, st));
+  auto* out = h->op_out.as<unsigned char>();
+  OpArgs A;
+  A.ncfg = (const int*)(in + o_ncfg);
+  A.lsteps = (const int*)(in + o_ls);
+  A.S = (const int*)(in + o_S);
+  A.counts = (const long long*)(in + o_cnt);
+  A.tput_off = (const long long*)(in + o_off);
+  A.tput = (const double*)(in + o_tp);
+  A.best = (double*)(out + ob_best);
+  A.stage_j = (long long*)(out + ob_sj);
+  A.stage_counts = (long long*)(out + ob_sc);
+  A.ncases = ncases;
+  const size_t smem = dp_smem_bytes(kMaxM, maxLu + 1, maxLu);
+  placement_op_kernel<<<(unsigned)ncases, kDpThreads, smem, st>>>(A);
+  LAUNCH_CHECK(h);
+  CUDA_TRY(cudaMemcpyAsync(best, out + ob_best, ncases * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(stage_j, out + ob_sj, ncases * kMaxC * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(stage_counts, out + ob_sc, ncases * kMaxC * kMaxC * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int coral_s1_stage_ms(const coral_s1_handle* h, double* tables_ms, double* enumerate_ms,
+                      double* evaluate_ms, double* frontier_ms) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  float t = 0;
+  double* outs[4] = {tables_ms, enumerate_ms, evaluate_ms, frontier_ms};
+  for (int i = 0; i < 4; ++i) {
+    if (!outs[i]) continue;
+    *outs[i] = -1.0;
+    if (cudaEventElapsedTime(&t, h->ev[2 * i], h->ev[2 * i + 1]) == cudaSuccess) *outs[i] = t;
+    else cudaGetLastError();
+  }
+  return 0;
+}
+
+}  // extern "C"

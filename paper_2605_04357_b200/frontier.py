@@ -1,0 +1,165 @@
+"""Per-(model, phase, region) throughput-vs-cost Pareto frontier of stage 1.
+
+The reference has no frontier step; its nearest analogues are the
+stage-2 cost-efficiency prune (allocation.py:131-153) and the sweep's best
+tokens/s per USD-h (cli.py:253-260). This module is the new output the north star
+asks for, defined exactly as the oracle in SURVEY.md 8c:
+
+  for each (model, phase) and region r, over templates t whose price
+  p = sum_(cfg, n) n * price[r, cfg] (allocation.py:91-98, sequential in combo order;
+  unpriced configs drop the template) exists, sort by (p asc, T desc, str(combo) asc)
+  and keep t iff T > the running max of T over the earlier ones.
+
+Everything runs on the device (pricing, 4 stable radix passes, segmented running max,
+compaction); with torch.distributed initialised the candidates are interleaved over
+ranks and the per-rank frontiers are merged after ONE NCCL all-gather.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .library import GenContext, Stage1Problem, TemplateLibrary, decode_key, library_meta
+from .specs import PHASES, NodeComboKey
+
+
+@dataclass
+class FrontierEntry:
+    template: object      # ServingTemplate
+    price_usd_h: float    # one instance in this region
+
+    @property
+    def throughput_tps(self) -> float:
+        return self.template.throughput_tps
+
+
+@dataclass
+class TemplateFrontier:
+    """Frontier survivors per (model, phase, region), each list in ascending price."""
+
+    segments: dict = field(default_factory=dict)
+    meta: dict = field(default_factory=dict)
+    num_candidates: int = 0
+
+    def templates_for(self, model: str, phase: str, region: str) -> list:
+        return self.segments.get((model, phase, region), [])
+
+    def __len__(self) -> int:
+        return sum(len(v) for v in self.segments.values())
+
+    def library(self) -> TemplateLibrary:
+        """Union of the survivors over regions as a TemplateLibrary, the input the
+        unchanged stage-2 MILP (allocation.build_allocation_model) consumes."""
+        seen = {}
+        for entries in self.segments.values():
+            for e in entries:
+                seen[id(e.template)] = e.template
+        return TemplateLibrary(entries=list(seen.values()), meta=dict(self.meta))
+
+
+def _price_matrix(configs, prices, regions):
+    """prices: {(region, config name): USD/h} or an object with .prices -> [R, K]."""
+    table = getattr(prices, "prices", prices)
+    if regions is None:
+        regions = sorted({r for r, _ in table})
+    regions = [getattr(r, "name", r) for r in regions]
+    mat = np.full((len(regions), len(configs)), np.nan)
+    for i, r in enumerate(regions):
+        for k, c in enumerate(configs):
+            p = table.get((r, c.name))
+            if p is not None:
+                mat[i, k] = float(p)
+    return regions, mat
+
+
+def _dist_info(dist):
+    if dist is False:
+        return None
+    import torch.distributed as tdist
+    if not (tdist.is_available() and tdist.is_initialized()):
+        return None
+    if tdist.get_world_size() <= 1:
+        return None
+    return tdist
+
+
+def _merge_across_ranks(prob: Stage1Problem, n_local: int, tdist) -> int:
+    """ONE all-gather of the fixed-capacity partial frontiers, then the same skyline
+    over their union on every rank (associative: all ranks end identical)."""
+    import torch
+    dev = torch.device("cuda", prob.h.device)
+    world = tdist.get_world_size()
+    cnt = torch.tensor([n_local], dtype=torch.int64, device=dev)
+    counts = torch.empty(world, dtype=torch.int64, device=dev)
+    tdist.all_gather_into_tensor(counts, cnt)
+    counts_h = counts.tolist()
+    cap = max(1, max(counts_h))
+    item = _native.FRONTIER_DTYPE.itemsize
+    send = torch.zeros(cap * item, dtype=torch.uint8, device=dev)
+    prob.h.frontier_export_device(send.data_ptr(), cap)
+    recv = torch.empty(world * cap * item, dtype=torch.uint8, device=dev)
+    tdist.all_gather_into_tensor(recv, send)
+    parts = recv.view(world, cap, item)
+    union = torch.cat([parts[r, :counts_h[r]] for r in range(world)]).contiguous()
+    return prob.h.frontier_merge_device(union.data_ptr(), int(sum(counts_h)))
+
+
+def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,
+                   phases=PHASES, dist=None, return_problem: bool = False):
+    """Stage 1 end to end on the GPU: spec tables in, frontier templates out.
+
+    `prices` is a MarketState-like object (`.prices`) or its dict
+    {(region, config name): USD/h}; `regions` defaults to every region priced.
+    """
+    ctx = ctx or GenContext()
+    configs_sorted = sorted(configs, key=lambda c: c.name)
+    meta = library_meta(configs_sorted, models, slos, caps, ctx)
+    region_names, pmat = _price_matrix(configs_sorted, prices, regions)
+    if not models:
+        return TemplateFrontier(meta=meta)
+    prob = Stage1Problem(configs, models, slos, caps, ctx, phases)
+    tdist = _dist_info(dist)
+    if tdist is not None:
+        prob.h.tables()
+        prob.h.enumerate()
+        prob.counts = prob.h.num_combos()
+        NP = len(prob.phases)
+        prob.cand_off = np.zeros(len(prob.models) * NP + 1, dtype=np.int64)
+        for mp in range(len(prob.models) * NP):
+            prob.cand_off[mp + 1] = prob.cand_off[mp] + prob.counts[mp // NP]
+        prob.h.evaluate_shard(tdist.get_rank(), tdist.get_world_size())
+        n_local = prob.h.frontier(pmat)
+        n = _merge_across_ranks(prob, n_local, tdist)
+    else:
+        prob.run()
+        n = prob.h.frontier(pmat)
+    items = prob.h.get_frontier(n)
+    front = materialise(prob, items, region_names, meta)
+    return (front, prob) if return_problem else front
+
+
+def materialise(prob: Stage1Problem, items: np.ndarray, region_names, meta) -> TemplateFrontier:
+    """Survivor records -> ServingTemplate objects (one object per (mp, combo))."""
+    NP = len(prob.phases)
+    cbr = prob.cfg_by_rank
+    cache = {}
+    segments = {}
+    for it in items:
+        mp = int(it["mp"])
+        key = int(it["combo_key"])
+        t = cache.get((mp, key))
+        if t is None:
+            combo = object.__new__(NodeComboKey)
+            combo.__dict__["items"] = tuple((cbr[r], n) for r, n in decode_key(key))
+            t = prob.make_template(prob.models[mp // NP], prob.phases[mp % NP], combo, it["rec"])
+            cache[(mp, key)] = t
+        seg = (t.model, t.phase, region_names[int(it["region"])])
+        segments.setdefault(seg, []).append(FrontierEntry(t, float(it["price_usd_h"])))
+    return TemplateFrontier(segments=segments, meta=meta,
+                            num_candidates=int(prob.cand_off[-1]) if prob.cand_off is not None else 0)
+
+
+__all__ = ["FrontierEntry", "TemplateFrontier", "build_frontier", "materialise"]

@@ -1,0 +1,105 @@
+"""Shared test helpers: golden fixtures, canonical record lines, workload inputs."""
+
+from __future__ import annotations
+
+import gzip
+import hashlib
+import json
+import os
+
+import numpy as np
+
+from paper_2605_04357_b200 import catalog
+from paper_2605_04357_b200.library import GenContext, LibraryCaps, decode_key
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def golden(name):
+    with gzip.open(os.path.join(GOLDEN, name), "rt") as fh:
+        return json.load(fh)
+
+
+def digest(lines) -> str:
+    h = hashlib.sha256()
+    for ln in lines:
+        h.update(ln.encode())
+        h.update(b"\n")
+    return h.hexdigest()
+
+
+def line(model, phase, combo_str, S, layers, son, T) -> str:
+    return (f"{model}|{phase}|{combo_str}|{S}|{','.join(map(str, layers))}|"
+            f"{','.join(map(str, son))}|{float(T)!r}")
+
+
+def template_line(t) -> str:
+    return line(t.model, t.phase, str(t.combo), t.placement.num_stages,
+                t.placement.layers_per_stage, t.placement.stage_of_node, t.throughput_tps)
+
+
+def key_str(key, cfg_by_rank) -> str:
+    return "+".join(f"{cfg_by_rank[r].name}*{n}" for r, n in decode_key(int(key)))
+
+
+def record_line(model, phase, key, rec, cfg_by_rank) -> str:
+    S = int(rec["num_stages"])
+    n = int(rec["num_nodes"])
+    return line(model, phase, key_str(key, cfg_by_rank), S,
+                [int(x) for x in rec["layers_per_stage"][:S]],
+                [int(x) for x in rec["stage_of_node"][:n]], rec["throughput_tps"])
+
+
+def workload(name):
+    """(configs, models, slos, caps, ctx, regions, prices) exactly as
+    tests/golden/run_reference_library.py builds them from the reference."""
+    w = catalog.WORKLOADS[name]()
+    return (w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho),
+            GenContext(perf=w.perf, granularity=w.granularity), w.regions, w.prices)
+
+
+def cfg_by_rank(configs):
+    from paper_2605_04357_b200.library import str_ranks
+    configs = sorted(configs, key=lambda c: c.name)
+    ranks = str_ranks([c.name for c in configs])
+    out = [None] * len(configs)
+    for i, r in enumerate(ranks):
+        out[r] = configs[i]
+    return out
+
+
+def oracle_problem(name_or_inputs, phases=("prefill", "decode")):
+    from oracle.oracle import OracleProblem
+    if isinstance(name_or_inputs, str):
+        configs, models, slos, caps, ctx, regions, prices = workload(name_or_inputs)
+    else:
+        configs, models, slos, caps, ctx = name_or_inputs[:5]
+    return OracleProblem.from_specs(configs, models, slos, caps, ctx, phases)
+
+
+def oracle_library_lines(op, stride=1, threads=0):
+    """Oracle records of every (model, phase) as canonical lines in library order,
+    solving every `stride`-th combo only."""
+    cbr = cfg_by_rank(op.configs)
+    lines = []
+    order = sorted(((m.name, ph, mi, pi) for mi, m in enumerate(op.models)
+                    for pi, ph in enumerate(op.phases)))
+    for mname, ph, mi, pi in order:
+        keys = op.enumerate(mi)
+        code = 0 if ph == "prefill" else 1
+        recs = op.solve(mi, code, keys, 0, stride, threads=threads)
+        for i in range(0, len(keys), stride):
+            if recs[i]["num_stages"] > 0:
+                lines.append(record_line(mname, ph, keys[i], recs[i], cbr))
+    return lines
+
+
+def price_matrix(configs, prices, regions):
+    configs = sorted(configs, key=lambda c: c.name)
+    mat = np.full((len(regions), len(configs)), np.nan)
+    for i, r in enumerate(regions):
+        for k, c in enumerate(configs):
+            p = prices.get((getattr(r, "name", r), c.name))
+            if p is not None:
+                mat[i, k] = p
+    return mat
