@@ -102,7 +102,7 @@ typedef struct coral_s1_record {
   uint8_t num_nodes;
   uint16_t layers_per_stage[CORAL_S1_MAX_NODES];
   uint8_t stage_of_node[CORAL_S1_MAX_NODES];
-  uint8_t _pad[2];
+  uint8_t _pad[4]; /* explicit, always zero: records compare bytewise */
 } coral_s1_record; /* 32 bytes */
 
 /* One frontier survivor (new output). */

@@ -48,7 +48,7 @@ class Problem(C.Structure):
 
 RECORD_DTYPE = np.dtype([("throughput_tps", "<f8"), ("num_stages", "u1"), ("num_nodes", "u1"),
                          ("layers_per_stage", "<u2", (MAX_NODES,)),
-                         ("stage_of_node", "u1", (MAX_NODES,)), ("_pad", "u1", (2,))], align=True)
+                         ("stage_of_node", "u1", (MAX_NODES,)), ("_pad", "u1", (4,))], align=True)
 FRONTIER_DTYPE = np.dtype([("price_usd_h", "<f8"), ("throughput_tps", "<f8"),
                            ("combo_key", "<u8"), ("mp", "<i4"), ("region", "<i4"),
                            ("rec", RECORD_DTYPE)], align=True)

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/coral_s1.h"
+#include "lattice.cuh"
 #include "placement_dp.cuh"
 #include "roofline.cuh"
 
@@ -97,6 +98,16 @@ struct coral_s1_handle {
   DevBuf items, items_sorted, sort_a, sort_b, perm_a, perm_b, segk, scanv, flagsel, nsel, front,
       prices, enum_tmp;
   DevBuf op_in, op_out, tab_off_d;
+  // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
+  static constexpr int kStreams = 4;
+  long long lat_states = 0;
+  std::vector<long long> lat_base;     // [R + 2]
+  DevBuf lat_base_d, lat_binom_d, lat_key, lat_nsub, lat_off, lat_sub, lat_maxn, lat_flags_h;
+  DevBuf ws_value[kStreams], ws_f0[kStreams], ws_f1[kStreams], ws_ch[kStreams];
+  cudaStream_t side[kStreams] = {};
+  cudaEvent_t side_ev[kStreams] = {};
+  cudaEvent_t fork_ev = nullptr;
+  std::vector<unsigned char> flags_h;
   cudaEvent_t ev[8] = {};
   float ms[4] = {0, 0, 0, 0};
 };
@@ -228,9 +239,59 @@ __device__ __forceinline__ int decode_key(const DevProblem& P, unsigned long lon
 }
 
 // --------------------------------------------------------------------------------
-// Evaluator: one CTA per candidate (model, phase, combo). templates.py:308-326 for
-// the S loop and best-S rule, kernels.py:143-276 for the DP, templates.py:209-228
-// for the canonical placement written to the record.
+// Canonical placement (templates.py:209-228): stages ordered by (-j, -counts tuple),
+// layers = j * g, nodes assigned config by config in combo order.
+// stage_cnt[s][c] = nodes of combo config c in raw stage s.
+// --------------------------------------------------------------------------------
+__device__ void canonical_record(int S, const int* stage_j, const int (*stage_cnt)[kMaxC], int C,
+                                 const int* cnt, int g, double val, int n, coral_s1_record* rec) {
+  int order[kMaxC];
+  for (int s = 0; s < S; ++s) order[s] = s;
+  for (int a = 1; a < S; ++a) {  // stable insertion sort == sorted(range(S), key=...)
+    const int x = order[a];
+    int b = a - 1;
+    while (b >= 0) {
+      const int y = order[b];
+      bool less;  // key(x) < key(y)
+      if (stage_j[x] != stage_j[y]) less = stage_j[x] > stage_j[y];
+      else {
+        less = false;
+        for (int c = 0; c < C; ++c)
+          if (stage_cnt[x][c] != stage_cnt[y][c]) { less = stage_cnt[x][c] > stage_cnt[y][c]; break; }
+      }
+      if (!less) break;
+      order[b + 1] = y;
+      --b;
+    }
+    order[b + 1] = x;
+  }
+  int next_free[kMaxC];
+  int offc = 0;
+  for (int c = 0; c < C; ++c) { next_free[c] = offc; offc += cnt[c]; }
+  coral_s1_record r;
+  memset(&r, 0, sizeof(r));
+  r.throughput_tps = val;
+  r.num_stages = (unsigned char)S;
+  r.num_nodes = (unsigned char)n;
+  for (int pos = 0; pos < S; ++pos) {
+    const int s = order[pos];
+    r.layers_per_stage[pos] = (unsigned short)(stage_j[s] * g);
+    for (int c = 0; c < C; ++c)
+      for (int k = 0; k < stage_cnt[s][c]; ++k) r.stage_of_node[next_free[c]++] = (unsigned char)pos;
+  }
+  *rec = r;
+}
+
+__device__ __forceinline__ double record_best(const coral_s1_record& r) {
+  return r.num_stages ? r.throughput_tps : kNegInf;
+}
+
+// --------------------------------------------------------------------------------
+// Per-candidate evaluator (exact fallback): one CTA per candidate (model, phase,
+// combo) for S in [S_lo, S_hi], continuing from the candidate's current record.
+// templates.py:308-326 for the S loop and best-S rule (strictly better, > 1e-9),
+// kernels.py:143-276 for the DP (placement_dp.cuh). Used where the lattice path
+// does not apply (a row outside the monotone test at this S) and for sub-ranges.
 // --------------------------------------------------------------------------------
 struct EvalArgs {
   DevProblem P;
@@ -239,6 +300,7 @@ struct EvalArgs {
   const int64_t* cand_off;         // [NMP+1]
   int NMP;
   int64_t lo, hi, stride;          // candidates lo, lo+stride, ... < hi
+  int S_lo, S_hi;
   const double* tab;
   const int64_t* tab_off;
   const unsigned char* flags;
@@ -270,9 +332,8 @@ __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
     for (int c = 0; c < C; ++c) { s_cfg[c] = cfg[c]; sh.cnt[c] = cnt[c]; }
     sh.Lu = P.Lu[m];
     sh.LuP = sh.Lu + 1;
-    s_best = kNegInf;
-    memset(&s_rec, 0, sizeof(s_rec));
-    s_rec.throughput_tps = kNegInf;
+    s_rec = A.rec[ci];
+    s_best = record_best(s_rec);
   }
   __syncthreads();
   dp_setup_lattice(sh);
@@ -281,8 +342,8 @@ __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
   const int K = P.K;
   const int Lu = sh.Lu, LuP = sh.LuP, C = sh.C, M = sh.M, n = sh.n;
   const DpBuffers B = dp_carve(smem, M, LuP, Lu);
-  const int Smax = min(n, Lu);
-  for (int S = 1; S <= Smax; ++S) {
+  const int Smax = min(min(n, Lu), A.S_hi);
+  for (int S = A.S_lo; S <= Smax; ++S) {
     // tables[S][cfg_rows, :] (templates.py:320)
     const double* base = A.tab + A.tab_off[mp] + (int64_t)(S - 1) * K * Lu;
     for (int idx = tid; idx < C * Lu; idx += blockDim.x) {
@@ -312,48 +373,125 @@ __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
       s_best = val;
       if (S == 1) { sh.stage_j[0] = Lu; sh.stage_u[0] = M - 1; }
       else dp_decode(sh, B, S);
-      // canonical placement (templates.py:209-228): stages by (-j, -counts)
-      int order[kMaxC];
-      for (int s = 0; s < S; ++s) order[s] = s;
-      for (int a = 1; a < S; ++a) {  // stable insertion sort
-        const int x = order[a];
-        int b = a - 1;
-        while (b >= 0) {
-          const int y = order[b];
-          bool less;  // key(x) < key(y)
-          if (sh.stage_j[x] != sh.stage_j[y]) less = sh.stage_j[x] > sh.stage_j[y];
-          else {
-            less = false;
-            for (int c = 0; c < C; ++c) {
-              const int dx = sh.digits[sh.stage_u[x]][c], dy = sh.digits[sh.stage_u[y]][c];
-              if (dx != dy) { less = dx > dy; break; }
-            }
-          }
-          if (!less) break;
-          order[b + 1] = y;
-          --b;
-        }
-        order[b + 1] = x;
-      }
-      const int g = P.g[m];
-      int next_free[kMaxC];
-      int offc = 0;
-      for (int c = 0; c < C; ++c) { next_free[c] = offc; offc += sh.cnt[c]; }
-      s_rec.throughput_tps = val;
-      s_rec.num_stages = (unsigned char)S;
-      s_rec.num_nodes = (unsigned char)n;
-      for (int pos = 0; pos < kMaxC; ++pos) s_rec.layers_per_stage[pos] = 0;
-      for (int pos = 0; pos < S; ++pos) {
-        const int s = order[pos];
-        s_rec.layers_per_stage[pos] = (unsigned short)(sh.stage_j[s] * g);
-        for (int c = 0; c < C; ++c)
-          for (int k = 0; k < sh.digits[sh.stage_u[s]][c]; ++k)
-            s_rec.stage_of_node[next_free[c]++] = (unsigned char)pos;
-      }
+      int stage_cnt[kMaxC][kMaxC];
+      for (int s = 0; s < S; ++s)
+        for (int c = 0; c < C; ++c) stage_cnt[s][c] = sh.digits[sh.stage_u[s]][c];
+      canonical_record(S, sh.stage_j, stage_cnt, C, sh.cnt, P.g[m], val, n, &s_rec);
     }
     __syncthreads();
   }
   if (tid == 0) A.rec[ci] = s_rec;
+}
+
+// --------------------------------------------------------------------------------
+// Lattice top cell: one warp per candidate of one (model, phase) at stage count S.
+// f_S[S][Lu][full] = max over u (lanes) of the crossing with f_S[S-1][.][full-u]
+// (or value for S == 2); reduce with the reference tie rule (value desc, u code
+// asc). On a strict improvement (> 1e-9) walk the stored choices back through the
+// lattice layers and write the canonical record.
+// --------------------------------------------------------------------------------
+struct TopArgs {
+  LatModel L;
+  const int* inv_rank;
+  const unsigned long long* keys;   // this model's combos (library order)
+  long long ncombo;
+  int S, Lu, g;
+  const double* tabS;               // [K][Lu] at S
+  const double* value;              // [states][Lu+1] at S
+  const double* fprev;              // layer S-1 (value when S == 2)
+  const unsigned short* ch;         // layers 2..S-1, stride layer_stride
+  long long layer_stride;
+  const unsigned long long* state_key;
+  const long long* off;
+  const uint2* subtab;
+  coral_s1_record* rec;             // this (model, phase)'s records
+};
+
+__global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
+  const int lane = threadIdx.x & 31;
+  const long long ci = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ci >= A.ncombo) return;
+  int cfg[kMaxC], cnt[kMaxC];
+  const int C = lat_tokens(A.inv_rank, A.keys[ci], cfg, cnt);
+  int M = 1, n = 0;
+  for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; }
+  const int S = A.S, Lu = A.Lu, LuP = Lu + 1;
+  if (S > n || S > Lu) return;
+  if (S == 1) {  // f[1][L][full] = value[full][L], summed in config order
+    if (lane) return;
+    double v = 0.0;
+    for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], A.tabS[cfg[c] * Lu + (Lu - 1)]));
+    coral_s1_record& r = A.rec[ci];
+    if (v > record_best(r) && v > 1e-9) {
+      int sj[kMaxC] = {Lu};
+      int sc[kMaxC][kMaxC];
+      for (int c = 0; c < C; ++c) sc[0][c] = cnt[c];
+      canonical_record(1, sj, sc, C, cnt, A.g, v, n, &r);
+    }
+    return;
+  }
+  const int jmax = Lu - (S - 1);
+  const int umax = n - (S - 1);
+  double best = kNegInf;
+  int bu = 1 << 20, bj = 0;
+  long long brem = 0;
+  for (int code = lane + 1; code < M; code += 32) {
+    int d[kMaxC], e[kMaxC], rest = code;
+    for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; e[c] = cnt[c] - d[c]; }
+    int su, sr;
+    const long long ru = lat_rank_tokens(A.L, cfg, d, C, &su);
+    if (su > umax) continue;
+    const long long rr = lat_rank_tokens(A.L, cfg, e, C, &sr);
+    double cand;
+    int cj;
+    dp_pair(A.value + ru * LuP, A.fprev + rr * LuP, Lu, jmax, true, cand, cj);
+    if (cand > best) { best = cand; bu = code; bj = cj; brem = rr; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_down_sync(0xffffffffu, best, o);
+    const int ou = __shfl_down_sync(0xffffffffu, bu, o);
+    const int oj = __shfl_down_sync(0xffffffffu, bj, o);
+    const long long orr = __shfl_down_sync(0xffffffffu, brem, o);
+    if (ob > best || (ob == best && ou < bu)) { best = ob; bu = ou; bj = oj; brem = orr; }
+  }
+  if (lane) return;
+  coral_s1_record& r = A.rec[ci];
+  if (!(best > record_best(r) && best > 1e-9)) return;
+  // walk back (kernels.py:258-275): stage 0 is the top choice
+  int sj[kMaxC], sc[kMaxC][kMaxC];
+  {
+    int rest = bu;
+    for (int c = 0; c < C; ++c) { sc[0][c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; }
+    sj[0] = bj;
+  }
+  long long X = brem;
+  int l = Lu - bj;
+  for (int s = 1; s < S; ++s) {
+    const int sg = S - s;
+    int xc[kMaxC], xn[kMaxC];
+    const int XC = lat_tokens(A.inv_rank, A.state_key[X], xc, xn);
+    int ucode, j;
+    if (sg == 1) { ucode = -1; j = l; }
+    else {
+      const unsigned short chv = A.ch[(long long)(sg - 2) * A.layer_stride + X * LuP + l];
+      ucode = chv >> 10;
+      j = chv & 1023;
+    }
+    int ud[kMaxC];
+    if (ucode < 0) { for (int t = 0; t < XC; ++t) ud[t] = xn[t]; }
+    else {
+      int rest = ucode;
+      for (int t = 0; t < XC; ++t) { ud[t] = rest % (xn[t] + 1); rest /= xn[t] + 1; }
+    }
+    for (int c = 0; c < C; ++c) {
+      sc[s][c] = 0;
+      for (int t = 0; t < XC; ++t) if (xc[t] == cfg[c]) sc[s][c] = ud[t];
+    }
+    sj[s] = j;
+    if (ucode >= 0) X = A.subtab[A.off[X] + ucode].y;
+    l -= j;
+  }
+  canonical_record(S, sj, sc, C, cnt, A.g, best, n, &r);
 }
 
 // --------------------------------------------------------------------------------
@@ -502,6 +640,7 @@ __global__ void sortkey_kernel(const coral_s1_frontier_item* __restrict__ items,
     case 0: k = it.combo_key; break;                                               // key asc
     case 1: k = ~(unsigned long long)__double_as_longlong(it.throughput_tps); break; // T desc (T > 0)
     case 2: k = (unsigned long long)__double_as_longlong(it.price_usd_h); break;     // p asc (p >= 0)
+    case 4: k = it.rec.num_stages; break;  // fewer stages first (templates.py:322 tie rule)
     default: k = (unsigned long long)it.mp * (unsigned long long)R + (unsigned long long)it.region;
   }
   out[i] = k;
@@ -558,15 +697,17 @@ int frontier_from_items(coral_s1_handle* h, int64_t n, int R) {
   iota_kernel<<<gb, TB, 0, st>>>(perm, n);
   LAUNCH_CHECK(h);
   const coral_s1_frontier_item* items = h->items.as<coral_s1_frontier_item>();
-  // LSD: key asc, T desc, price asc, segment asc (all stable)
+  // LSD: stages asc, key asc, T desc, price asc, segment asc (all stable)
   const int nseg = h->NM * h->NP * R;
   int seg_bits = 1;
   while ((1ll << seg_bits) < (long long)nseg) ++seg_bits;
-  for (int field = 0; field < 4; ++field) {
-    sortkey_kernel<<<gb, TB, 0, st>>>(items, field == 0 ? nullptr : perm, n, field, R,
+  const int passes[5] = {4, 0, 1, 2, 3};
+  for (int pi = 0; pi < 5; ++pi) {
+    const int field = passes[pi];
+    sortkey_kernel<<<gb, TB, 0, st>>>(items, pi == 0 ? nullptr : perm, n, field, R,
                                       h->sort_a.as<unsigned long long>());
     LAUNCH_CHECK(h);
-    const int end_bit = field == 3 ? seg_bits : (field == 0 ? kKeyTokenBits * kMaxC : 64);
+    const int end_bit = field == 3 ? seg_bits : (field == 0 ? kKeyTokenBits * kMaxC : (field == 4 ? 3 : 64));
     size_t tmp = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp, h->sort_a.as<unsigned long long>(),
                                     h->sort_b.as<unsigned long long>(), perm, perm_out, (int)n, 0,
@@ -660,6 +801,13 @@ int coral_s1_create(int device, coral_s1_handle** out) {
   cudaError_t e = cudaMemcpyToSymbol(c_binom, tab, sizeof(tab));
   if (e != cudaSuccess) { delete h; return fail(CORAL_S1_ECUDA, cudaGetErrorString(e)); }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
+  for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
+    cudaStreamCreateWithFlags(&h->side[i], cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&h->side_ev[i], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
+  if (h->lat_binom_d.ensure(sizeof(tab)) == 0)
+    cudaMemcpy(h->lat_binom_d.p, tab, sizeof(tab), cudaMemcpyHostToDevice);
   const size_t smem_max = dp_smem_bytes(kMaxM, CORAL_S1_MAX_LAYER_UNITS + 1, CORAL_S1_MAX_LAYER_UNITS);
   cudaFuncSetAttribute(evaluate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
   cudaFuncSetAttribute(placement_op_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
@@ -675,8 +823,16 @@ int coral_s1_destroy(coral_s1_handle* h) {
   DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->seg_off,
                     &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
                     &h->sort_a, &h->sort_b, &h->perm_a, &h->perm_b, &h->segk, &h->scanv,
-                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d};
+                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d,
+                    &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
+                    &h->lat_sub, &h->lat_maxn, &h->lat_flags_h};
   for (DevBuf* b : bufs) b->release();
+  for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
+    h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_f1[i].release(); h->ws_ch[i].release();
+    if (h->side[i]) cudaStreamDestroy(h->side[i]);
+    if (h->side_ev[i]) cudaEventDestroy(h->side_ev[i]);
+  }
+  if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
   delete h;
   return 0;
@@ -925,51 +1081,251 @@ int coral_s1_num_candidates(const coral_s1_handle* h, int64_t* n) {
   return 0;
 }
 
-static int evaluate_impl(coral_s1_handle* h, int64_t lo, int64_t hi, int64_t stride) {
+}  // extern "C"
+
+// Per-combo kernel over candidates lo, lo+stride, ... < hi for S in [S_lo, S_hi].
+static int launch_percombo(coral_s1_handle* h, cudaStream_t st, int64_t lo, int64_t hi, int64_t stride,
+                           int S_lo, int S_hi) {
+  if (hi <= lo) return 0;
+  EvalArgs A;
+  A.P = h->dp;
+  A.keys = h->keys.as<unsigned long long>();
+  A.U = h->U;
+  A.cand_off = h->cand_off_d.as<int64_t>();
+  A.NMP = h->NM * h->NP;
+  A.hi = hi;
+  A.stride = stride;
+  A.S_lo = S_lo;
+  A.S_hi = S_hi;
+  A.tab = h->tab.as<double>();
+  A.tab_off = h->tab_off_d.as<int64_t>();
+  A.flags = h->flags.as<unsigned char>();
+  A.rec = h->rec.as<coral_s1_record>();
+  const size_t smem = dp_smem_bytes(kMaxM, h->maxLu + 1, h->maxLu);
+  const int64_t nblocks = (hi - lo + stride - 1) / stride;
+  const int64_t chunk = 1ll << 30;
+  for (int64_t b0 = 0; b0 < nblocks; b0 += chunk) {
+    A.lo = lo + b0 * stride;
+    const int64_t nb = std::min(chunk, nblocks - b0);
+    evaluate_kernel<<<(unsigned)nb, kDpThreads, smem, st>>>(A);
+    LAUNCH_CHECK(h);
+  }
+  return 0;
+}
+
+// State tables shared by all models (depend on K and n_max only) + per-model maxn.
+static int lattice_prepare(coral_s1_handle* h) {
+  const int K = h->K, R = h->n_max - 1;
+  cudaStream_t st = h->stream;
+  h->lat_base.assign(R + 2, 0);
+  for (int sz = 1; sz <= R; ++sz) {
+    long double c = 1;
+    for (int i = 1; i <= sz; ++i) c = c * (K + i - 1) / i;  // C(K+sz-1, sz)
+    h->lat_base[sz + 1] = h->lat_base[sz] + (long long)(c + 0.5L);
+  }
+  h->lat_states = h->lat_base[R + 1];
+  int rc;
+  if ((rc = upload(h, h->lat_base_d, h->lat_base))) return rc;
+  if (h->lat_states == 0) return 0;
+  const long long ns = h->lat_states;
+  if ((rc = h->lat_key.ensure(ns * 8)) || (rc = h->lat_nsub.ensure((ns + 1) * 8)) ||
+      (rc = h->lat_off.ensure((ns + 1) * 8)) ||
+      (rc = h->lat_maxn.ensure((size_t)std::max(h->NM, 1) * ns * 4)))
+    return rc;
+  LatModel L{K, R, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
+  const unsigned gb = (unsigned)((ns + 255) / 256);
+  lat_state_keys_kernel<<<gb, 256, 0, st>>>(L, h->dp.rank1, h->lat_key.as<unsigned long long>());
+  LAUNCH_CHECK(h);
+  lat_nsub_kernel<<<(unsigned)((ns + 256) / 256), 256, 0, st>>>(L, h->lat_key.as<unsigned long long>(),
+                                                                h->lat_nsub.as<long long>());
+  LAUNCH_CHECK(h);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, h->lat_nsub.as<long long>(), h->lat_off.as<long long>(),
+                                (int)(ns + 1), st);
+  if ((rc = ensure_tmp(h, tmp))) return rc;
+  CUDA_TRY(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, h->lat_nsub.as<long long>(),
+                                         h->lat_off.as<long long>(), (int)(ns + 1), st));
+  h->launches += 2;
+  long long nsub_total = 0;
+  CUDA_TRY(cudaMemcpyAsync(&nsub_total, h->lat_off.as<long long>() + ns, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if ((rc = h->lat_sub.ensure(std::max<long long>(nsub_total, 1) * sizeof(uint2)))) return rc;
+  lat_subtab_kernel<<<gb, 256, 0, st>>>(L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(),
+                                        h->lat_off.as<long long>(), h->lat_sub.as<uint2>());
+  LAUNCH_CHECK(h);
+  CUDA_TRY(cudaMemsetAsync(h->lat_maxn.p, 0, (size_t)h->NM * ns * 4, st));
+  for (int m = 0; m < h->NM; ++m) {
+    const long long nc = h->counts[m];
+    if (!nc) continue;
+    lat_maxn_kernel<<<(unsigned)((nc * 64 + 255) / 256), 256, 0, st>>>(
+        L, h->dp.inv_rank, h->keys.as<unsigned long long>() + (int64_t)m * h->U, nc,
+        h->lat_maxn.as<unsigned>() + (size_t)m * ns);
+    LAUNCH_CHECK(h);
+  }
+  // workspaces
+  const long long LuP = h->maxLu + 1;
+  for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
+    if ((rc = h->ws_value[i].ensure(ns * LuP * 8)) || (rc = h->ws_f0[i].ensure(ns * LuP * 8)) ||
+        (rc = h->ws_f1[i].ensure(ns * LuP * 8)) ||
+        (rc = h->ws_ch[i].ensure((size_t)std::max(h->n_max - 2, 1) * ns * LuP * 2)))
+      return rc;
+  }
+  return 0;
+}
+
+// One (model, phase) unit chain: S values ascending on stream `slot`.
+static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss, int slot) {
+  cudaStream_t st = h->side[slot];
+  const int m = mp / h->NP;
+  const int K = h->K, Lu = h->Lu[m], g = h->g[m];
+  const long long ns = h->lat_states, LuP = h->maxLu + 1;
+  const long long ncombo = h->counts[m];
+  if (!ncombo) return 0;
+  LatModel L{K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
+  const unsigned long long* keys = h->keys.as<unsigned long long>() + (int64_t)m * h->U;
+  coral_s1_record* rec = h->rec.as<coral_s1_record>() + h->cand_off[mp];
+  double* value = h->ws_value[slot].as<double>();
+  double* fb[2] = {h->ws_f0[slot].as<double>(), h->ws_f1[slot].as<double>()};
+  unsigned short* ch = h->ws_ch[slot].as<unsigned short>();
+  const long long layer_stride = ns * LuP;
+  for (int S : Ss) {
+    bool mono = true;  // kernels.py:291 over every config row at (mp, S)
+    for (int c = 0; c < K; ++c) mono &= (h->flags_h[((size_t)mp * h->n_max + (S - 1)) * K + c] & 1) != 0;
+    if (!mono) {  // exact per-candidate fallback for this S
+      int rc = launch_percombo(h, st, h->cand_off[mp], h->cand_off[mp + 1], 1, S, S);
+      if (rc) return rc;
+      continue;
+    }
+    const double* tabS = h->tab.as<double>() + h->tab_off[mp] + (int64_t)(S - 1) * K * Lu;
+    if (S >= 2) {
+      const long long nv = ns * Lu;
+      lat_value_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(
+          L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(), tabS, Lu, value);
+      LAUNCH_CHECK(h);
+      // value rows use stride Lu+1 of this model; the workspaces are sized for maxLu
+    }
+    for (int sg = 2; sg <= S - 1; ++sg) {
+      const int smaxsz = std::min(h->n_max - 1, h->n_max - (S - sg));
+      if (smaxsz < sg || Lu - (S - sg) < sg) continue;
+      const long long nst = h->lat_base[smaxsz + 1] - h->lat_base[sg];
+      const double* fprev = (sg == 2) ? value : fb[(sg - 1) & 1];
+      lat_layer_kernel<<<(unsigned)((nst * 32 + 255) / 256), 256, 0, st>>>(
+          L, S, sg, smaxsz, Lu, h->lat_maxn.as<unsigned>() + (size_t)m * ns,
+          h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), value, fprev, fb[sg & 1],
+          ch + (sg - 2) * layer_stride);
+      LAUNCH_CHECK(h);
+    }
+    TopArgs T;
+    T.L = L;
+    T.inv_rank = h->dp.inv_rank;
+    T.keys = keys;
+    T.ncombo = ncombo;
+    T.S = S;
+    T.Lu = Lu;
+    T.g = g;
+    T.tabS = tabS;
+    T.value = value;
+    T.fprev = (S == 2) ? value : fb[(S - 1) & 1];
+    T.ch = ch;
+    T.layer_stride = layer_stride;
+    T.state_key = h->lat_key.as<unsigned long long>();
+    T.off = h->lat_off.as<long long>();
+    T.subtab = h->lat_sub.as<uint2>();
+    T.rec = rec;
+    lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
+    LAUNCH_CHECK(h);
+  }
+  return 0;
+}
+
+// Evaluate the (mp, S) units selected by `take(mp, S)`.
+template <class Take>
+static int evaluate_units(coral_s1_handle* h, Take take) {
   if (!h || !h->have_tables || !h->have_enum) return fail(CORAL_S1_EINVAL, "tables and enumerate first");
   CUDA_TRY(cudaSetDevice(h->device));
-  if (hi < 0 || hi > h->ncand) hi = h->ncand;
-  if (lo < 0) lo = 0;
-  if (stride < 1) return fail(CORAL_S1_EINVAL, "stride must be >= 1");
   int rc;
   if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record)))) return rc;
   cudaStream_t st = h->stream;
-  // records not evaluated by this call read as infeasible (num_stages 0)
-  CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), st));
+  const int NMP = h->NM * h->NP;
+  h->flags_h.assign((size_t)std::max(NMP, 1) * h->n_max * h->K, 0);
+  if (NMP && h->K)
+    CUDA_TRY(cudaMemcpyAsync(h->flags_h.data(), h->flags.p, (size_t)NMP * h->n_max * h->K,
+                             cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaEventRecord(h->ev[4], st));
-  if (hi > lo) {
-    EvalArgs A;
-    A.P = h->dp;
-    A.keys = h->keys.as<unsigned long long>();
-    A.U = h->U;
-    A.cand_off = h->cand_off_d.as<int64_t>();
-    A.NMP = h->NM * h->NP;
-    A.hi = hi;
-    A.stride = stride;
-    A.tab = h->tab.as<double>();
-    A.tab_off = h->tab_off_d.as<int64_t>();
-    A.flags = h->flags.as<unsigned char>();
-    A.rec = h->rec.as<coral_s1_record>();
-    const size_t smem = dp_smem_bytes(kMaxM, h->maxLu + 1, h->maxLu);
-    const int64_t nblocks = (hi - lo + stride - 1) / stride;
-    const int64_t chunk = 1ll << 30;
-    for (int64_t b0 = 0; b0 < nblocks; b0 += chunk) {
-      A.lo = lo + b0 * stride;
-      const int64_t nb = std::min(chunk, nblocks - b0);
-      evaluate_kernel<<<(unsigned)nb, kDpThreads, smem, st>>>(A);
-      LAUNCH_CHECK(h);
-    }
+  // records not improved by any unit read as infeasible (num_stages 0)
+  CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), st));
+  if ((rc = lattice_prepare(h))) return rc;
+  CUDA_TRY(cudaStreamSynchronize(st));  // flags_h valid
+  CUDA_TRY(cudaEventRecord(h->fork_ev, st));
+  for (int i = 0; i < coral_s1_handle::kStreams; ++i) CUDA_TRY(cudaStreamWaitEvent(h->side[i], h->fork_ev, 0));
+  // heaviest (model, phase) chains first, round-robin over the side streams
+  std::vector<int> order(NMP);
+  for (int i = 0; i < NMP; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const int ma = a / h->NP, mb = b / h->NP;
+    return (double)h->counts[ma] * h->Lu[ma] > (double)h->counts[mb] * h->Lu[mb];
+  });
+  int slot = 0;
+  for (int mp : order) {
+    const int m = mp / h->NP;
+    std::vector<int> Ss;
+    for (int S = 1; S <= std::min(h->smax[m], h->Lu[m]); ++S)
+      if (take(mp, S)) Ss.push_back(S);
+    if (Ss.empty() || !h->counts[m]) continue;
+    if ((rc = lattice_units(h, mp, Ss, slot))) return rc;
+    slot = (slot + 1) % coral_s1_handle::kStreams;
+  }
+  for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
+    CUDA_TRY(cudaEventRecord(h->side_ev[i], h->side[i]));
+    CUDA_TRY(cudaStreamWaitEvent(st, h->side_ev[i], 0));
   }
   CUDA_TRY(cudaEventRecord(h->ev[5], st));
   h->have_eval = true;
   return 0;
 }
 
-int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi) { return evaluate_impl(h, lo, hi, 1); }
+extern "C" {
 
+int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi) {
+  if (!h || !h->have_tables || !h->have_enum) return fail(CORAL_S1_EINVAL, "tables and enumerate first");
+  if (hi < 0 || hi > h->ncand) hi = h->ncand;
+  if (lo < 0) lo = 0;
+  if (lo == 0 && hi == h->ncand) return evaluate_units(h, [](int, int) { return true; });
+  // a sub-range: per-candidate kernel over [lo, hi), every S
+  CUDA_TRY(cudaSetDevice(h->device));
+  int rc;
+  if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record)))) return rc;
+  CUDA_TRY(cudaEventRecord(h->ev[4], h->stream));
+  CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), h->stream));
+  if ((rc = launch_percombo(h, h->stream, lo, hi, 1, 1, CORAL_S1_MAX_NODES))) return rc;
+  CUDA_TRY(cudaEventRecord(h->ev[5], h->stream));
+  h->have_eval = true;
+  return 0;
+}
+
+// Multi-GPU shard: (model, phase, S) units, longest-processing-time assignment on a
+// deterministic cost estimate; every rank computes the same assignment.
 int coral_s1_evaluate_shard(coral_s1_handle* h, int rank, int world) {
+  if (!h || !h->have_enum) return fail(CORAL_S1_EINVAL, "enumerate first");
   if (world < 1 || rank < 0 || rank >= world) return fail(CORAL_S1_EINVAL, "bad rank/world");
-  return evaluate_impl(h, rank, -1, world);
+  struct Unit { double cost; int mp, S; };
+  std::vector<Unit> units;
+  for (int mp = 0; mp < h->NM * h->NP; ++mp) {
+    const int m = mp / h->NP;
+    for (int S = 1; S <= std::min(h->smax[m], h->Lu[m]); ++S)
+      units.push_back({(double)h->counts[m] * (1.0 + (S - 1) * (double)h->Lu[m] / 8.0), mp, S});
+  }
+  std::stable_sort(units.begin(), units.end(), [](const Unit& a, const Unit& b) { return a.cost > b.cost; });
+  std::vector<double> load(world, 0.0);
+  std::vector<char> mine(units.size(), 0);
+  std::vector<std::vector<char>> owner((size_t)h->NM * h->NP, std::vector<char>(CORAL_S1_MAX_NODES + 1, 0));
+  for (size_t i = 0; i < units.size(); ++i) {
+    int best = 0;
+    for (int r = 1; r < world; ++r) if (load[r] < load[best]) best = r;
+    load[best] += units[i].cost;
+    if (best == rank) owner[units[i].mp][units[i].S] = 1;
+  }
+  return evaluate_units(h, [&](int mp, int S) { return owner[mp][S] != 0; });
 }
 
 int coral_s1_get_records(coral_s1_handle* h, int mp, coral_s1_record* out, int64_t n) {

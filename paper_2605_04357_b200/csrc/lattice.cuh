@@ -1,0 +1,224 @@
+// lattice.cuh — the placement DP evaluated once per sub-multiset, shared by every
+// candidate combo that contains it.
+//
+// The reference (kernels.py:143-276, _placement_dp_nb) runs an independent DP per
+// candidate combo: f[sg][l][rem] over the combo's sub-multisets rem. Nothing in a
+// cell depends on the enclosing combo:
+//   * value[u][j] = sum over u's configs (name order) of digit * tput[c][j-1]
+//     (kernels.py:164-170; zero digits add +0.0), a function of u alone;
+//   * the u loop visits sub-multisets of rem in increasing mixed-radix code order
+//     (kernels.py:204), which is lexicographic with the highest-named config most
+//     significant — identical for every combo containing rem;
+//   * the size filter (:207) and the crossing rule (:210-253) read only u, rem-u.
+// So f_S[sg][X][l] and its (u, j) choice are functions of the multiset X, and one
+// table per (model, phase, S, sg) over all multisets X serves every candidate:
+// 9.6e8 (u, l) pairs for BASELINE config 2 instead of 1.56e11 in the reference
+// (measured in DESIGN.md).
+//
+// Cells computed per (S, sg): X with sg <= |X| <= maxn(X) - (S - sg), l in
+// [sg, Lu - (S - sg)], where maxn(X) is the largest candidate containing X — exactly
+// the cells some candidate's DP can reach. The top cell (S, Lu, full) is per
+// candidate. Choices are stored per cell (u as X-local code, j) and walked back for
+// the candidates whose best S improves.
+//
+// States: multisets of 1..R = n_max-1 configs, indexed size-major and colex within a
+// size: idx = base[s] + sum_i C(a_i + i, i + 1) for sorted picks a_0 <= ... <= a_{s-1}.
+#pragma once
+#include "placement_dp.cuh"
+
+namespace coral {
+
+constexpr int kLatMaxState = kMaxC - 1;  // lattice tables hold |X| <= 5
+
+struct LatModel {
+  int K, R;                 // configs, largest state size (n_max - 1)
+  const long long* base;    // [R + 2]: first index of each size (base[1] = 0), base[R+1] = total
+  const unsigned long long* binom;  // [160][8]
+};
+
+__device__ __forceinline__ unsigned long long lat_binom(const LatModel& L, int N, int k) {
+  if (k < 0 || N < k) return 0ull;
+  return L.binom[N * 8 + k];
+}
+
+// colex index of the multiset given by ascending picks
+__device__ __forceinline__ long long lat_rank(const LatModel& L, const int* picks, int s) {
+  unsigned long long r = 0;
+  for (int i = 0; i < s; ++i) r += lat_binom(L, picks[i] + i, i + 1);
+  return L.base[s] + (long long)r;
+}
+
+// index of the multiset sum_t d[t] x cfg[t] (tokens in ascending config order)
+__device__ __forceinline__ long long lat_rank_tokens(const LatModel& L, const int* cfg, const int* d,
+                                                     int ntok, int* size_out) {
+  int picks[kMaxC];
+  int s = 0;
+  for (int t = 0; t < ntok; ++t)
+    for (int k = 0; k < d[t]; ++k) picks[s++] = cfg[t];
+  *size_out = s;
+  return s ? lat_rank(L, picks, s) : -1;
+}
+
+// ---- per-model state tables -------------------------------------------------
+
+// state_key[idx] = packed token key of state idx (same token format as combos).
+__global__ void lat_state_keys_kernel(LatModel L, const int* __restrict__ rank1,
+                                      unsigned long long* __restrict__ state_key) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= L.base[L.R + 1]) return;
+  int s = 1;
+  while (idx >= L.base[s + 1]) ++s;
+  unsigned long long r = (unsigned long long)(idx - L.base[s]);
+  int b[kMaxC];
+  for (int i = s - 1; i >= 0; --i) {  // colex unrank
+    int v = i;
+    while (lat_binom(L, v + 1, i + 1) <= r) ++v;
+    b[i] = v;
+    r -= lat_binom(L, v, i + 1);
+  }
+  unsigned long long key = 0;
+  int ntok = 0;
+  for (int i = 0; i < s;) {
+    const int a = b[i] - i;
+    int j = i;
+    while (j < s && b[j] - j == a) ++j;
+    key = (key << 9) | ((unsigned long long)rank1[a] << 3) | (unsigned long long)(j - i);
+    ++ntok;
+    i = j;
+  }
+  state_key[idx] = key << (9 * (kMaxC - ntok));
+}
+
+// decode a packed key into ascending config indices + counts
+__device__ __forceinline__ int lat_tokens(const int* __restrict__ inv_rank, unsigned long long key,
+                                          int* cfg, int* cnt) {
+  int C = 0;
+  for (int t = 0; t < kMaxC; ++t) {
+    const unsigned tok = (unsigned)(key >> (9 * (kMaxC - 1 - t))) & 511u;
+    if (!tok) break;
+    cfg[C] = inv_rank[(tok >> 3) - 1];
+    cnt[C] = tok & 7u;
+    ++C;
+  }
+  return C;
+}
+
+// maxn[idx] = max |combo| over the model's candidates containing state idx.
+// One thread per (combo, sub-multiset code).
+__global__ void lat_maxn_kernel(LatModel L, const int* __restrict__ inv_rank,
+                                const unsigned long long* __restrict__ keys, long long ncombo,
+                                unsigned* __restrict__ maxn) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long ci = t >> 6;
+  const int code = (int)(t & 63);
+  if (ci >= ncombo) return;
+  int cfg[kMaxC], cnt[kMaxC];
+  const int C = lat_tokens(inv_rank, keys[ci], cfg, cnt);
+  int M = 1, n = 0;
+  for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; }
+  if (code == 0 || code >= M) return;
+  int d[kMaxC], rest = code;
+  for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; }
+  int s;
+  const long long r = lat_rank_tokens(L, cfg, d, C, &s);
+  if (s > L.R) return;
+  atomicMax(maxn + r, (unsigned)n);
+}
+
+// nsub[idx] = M(X) = prod(counts + 1)
+__global__ void lat_nsub_kernel(LatModel L, const unsigned long long* __restrict__ state_key,
+                                long long* __restrict__ nsub) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long tot = L.base[L.R + 1];
+  if (idx > tot) return;
+  if (idx == tot) { nsub[idx] = 0; return; }
+  const unsigned long long key = state_key[idx];
+  long long M = 1;
+  for (int t = 0; t < kMaxC; ++t) {
+    const unsigned tok = (unsigned)(key >> (9 * (kMaxC - 1 - t))) & 511u;
+    if (!tok) break;
+    M *= (tok & 7u) + 1;
+  }
+  nsub[idx] = M;
+}
+
+// subtab[off[X] + code] = {size(u) << 24 | idx(u), idx(X - u)} for code in [0, M(X)).
+__global__ void lat_subtab_kernel(LatModel L, const int* __restrict__ inv_rank,
+                                  const unsigned long long* __restrict__ state_key,
+                                  const long long* __restrict__ off, uint2* __restrict__ subtab) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= L.base[L.R + 1]) return;
+  int cfg[kMaxC], cnt[kMaxC];
+  const int C = lat_tokens(inv_rank, state_key[idx], cfg, cnt);
+  int M = 1;
+  for (int c = 0; c < C; ++c) M *= cnt[c] + 1;
+  uint2* out = subtab + off[idx];
+  for (int code = 0; code < M; ++code) {
+    int d[kMaxC], e[kMaxC], rest = code;
+    for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; e[c] = cnt[c] - d[c]; }
+    int su, sr;
+    const long long ru = lat_rank_tokens(L, cfg, d, C, &su);
+    const long long rr = lat_rank_tokens(L, cfg, e, C, &sr);
+    out[code] = make_uint2(((unsigned)su << 24) | (unsigned)(ru < 0 ? 0 : ru), (unsigned)(rr < 0 ? 0 : rr));
+  }
+}
+
+// ---- per (model, phase, S) ----------------------------------------------------
+
+// value[idx][j], j = 1..Lu (kernels.py:164-170) from the S table rows.
+__global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
+                                 const unsigned long long* __restrict__ state_key,
+                                 const double* __restrict__ tabS /* [K][Lu] */, int Lu,
+                                 double* __restrict__ value) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long idx = t / Lu;
+  const int j = (int)(t - idx * Lu) + 1;
+  if (idx >= L.base[L.R + 1]) return;
+  int cfg[kMaxC], cnt[kMaxC];
+  const int C = lat_tokens(inv_rank, state_key[idx], cfg, cnt);
+  double v = 0.0;
+  for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], tabS[cfg[c] * Lu + (j - 1)]));
+  value[idx * (Lu + 1) + j] = v;
+}
+
+// One DP layer sg of stage count S: warp per state X, lanes over l.
+__global__ void __launch_bounds__(256) lat_layer_kernel(
+    LatModel L, int S, int sg, int smaxsz, int Lu, const unsigned* __restrict__ maxn,
+    const long long* __restrict__ off, const uint2* __restrict__ subtab,
+    const double* __restrict__ value, const double* __restrict__ fprev, double* __restrict__ fout,
+    unsigned short* __restrict__ chout) {
+  const int lane = threadIdx.x & 31;
+  const long long idx = L.base[sg] + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (idx >= L.base[smaxsz + 1]) return;  // |X| <= n_max - (S - sg)
+  int s = sg;
+  while (idx >= L.base[s + 1]) ++s;
+  if (s > (int)maxn[idx] - (S - sg)) return;  // no candidate reaches this cell
+  const int LuP = Lu + 1;
+  const int lmax = Lu - (S - sg);
+  const int usz = s - (sg - 1);  // |u| <= |X| - (sg - 1)
+  const long long o = off[idx];
+  const long long M = off[idx + 1] - o;
+  for (int l0 = sg; l0 <= lmax; l0 += 32) {
+    const int l = l0 + lane;
+    const bool act = l <= lmax;
+    const int jmax = l - (sg - 1);
+    double best = kNegInf;
+    int bu = 0, bj = 0;
+    for (int code = 1; code < M; ++code) {
+      const uint2 e = subtab[o + code];
+      if ((int)(e.x >> 24) > usz) continue;
+      if (!act) continue;
+      double cand;
+      int cj;
+      dp_pair(value + (long long)(e.x & 0xFFFFFFu) * LuP, fprev + (long long)e.y * LuP, l, jmax, true,
+              cand, cj);
+      if (cand > best) { best = cand; bu = code; bj = cj; }
+    }
+    if (act) {
+      fout[idx * LuP + l] = best;
+      chout[idx * LuP + l] = (unsigned short)((bu << 10) | bj);
+    }
+  }
+}
+
+}  // namespace coral

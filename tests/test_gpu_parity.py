@@ -230,3 +230,21 @@ def test_errors():
     with pytest.raises(LibraryGenError):
         build_library(configs, [huge], {"huge": SloSpec(1500, 80)}, caps, ctx)
     assert len(build_library(configs, [], {}, caps, ctx)) == 0
+
+
+def test_lattice_path_equals_per_candidate_path():
+    """The lattice evaluator (full range) and the per-candidate fallback kernel
+    (sub-ranges) produce byte-identical records."""
+    configs, models, slos, caps, ctx, regions, prices = workload("core")
+    prob = Stage1Problem(configs, models, slos, caps, ctx).run()
+    full = [prob.records(mp).tobytes() for mp in range(len(models) * 2)]
+    n = prob.num_candidates
+    prob.h.evaluate(0, n - 1)  # sub-range -> per-candidate kernel
+    part = [prob.records(mp) for mp in range(len(models) * 2)]
+    for mp in range(len(models) * 2):
+        recs = part[mp]
+        if mp == len(models) * 2 - 1:
+            recs = recs[:-1]
+            assert recs.tobytes() == full[mp][:len(recs.tobytes())]
+        else:
+            assert recs.tobytes() == full[mp]

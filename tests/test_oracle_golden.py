@@ -157,3 +157,31 @@ def test_frontier_matches_reference_library_frontier(w):
     ref = [[a, b, c, d, None, f] for a, b, c, d, e, f in g]
     key = lambda t: (t[0], t[1], t[2])  # noqa: E731
     assert sorted(got, key=key) == sorted(ref, key=key)
+
+
+def test_library_extended_sample():
+    """Every 97th template of BASELINE config 2's reference library (1,084,362
+    templates): the oracle re-solves those combos and matches bit for bit."""
+    g = golden("library_extended.json.gz")
+    op = oracle_problem("extended")
+    cbr = cfg_by_rank(op.configs)
+    rank_of = {c.name: r for r, c in enumerate(cbr)}
+    midx = {m.name: i for i, m in enumerate(op.models)}
+    by_mp = {}
+    for ln in g["sample"]:
+        model, phase, combo = ln.split("|")[:3]
+        key = 0
+        toks = combo.split("+")
+        for name, n in (t.rsplit("*", 1) for t in toks):
+            key = (key << 9) | ((rank_of[name] + 1) << 3) | int(n)
+        key <<= 9 * (6 - len(toks))
+        by_mp.setdefault((model, phase), []).append((key, ln))
+    from tests.helpers import record_line
+    checked = 0
+    for (model, phase), items in by_mp.items():
+        keys = np.array([k for k, _ in items], dtype=np.uint64)
+        recs = op.solve(midx[model], 0 if phase == "prefill" else 1, keys)
+        for (k, ln), r in zip(items, recs):
+            assert record_line(model, phase, k, r, cbr) == ln
+            checked += 1
+    assert checked == len(g["sample"]) > 10000
