@@ -88,13 +88,14 @@ struct coral_s1_handle {
   int maxLu = 0;
   int64_t U = 0;                 // multiset universe size per model
   std::vector<int64_t> counts;   // combos per model
+  std::vector<int64_t> koff;     // [NM+1] first key of each model (compacted)
   std::vector<int64_t> cand_off; // [NM*NP + 1]
   int64_t ncand = 0;
   int64_t nfront = 0;
   int num_regions = 0;
   DevProblem dp{};
   // device buffers
-  DevBuf prob, tab, flags, budget, keys_raw, keys, seg_off, nvalid, cand_off_d, rec, cub_tmp;
+  DevBuf prob, tab, flags, budget, keys_raw, keys, keys_tmp, koff_d, nvalid, cand_off_d, rec, cub_tmp;
   DevBuf items, items_sorted, sort_a, sort_b, perm_a, perm_b, segk, scanv, flagsel, nsel, front,
       prices, enum_tmp;
   DevBuf op_in, op_out, tab_off_d;
@@ -103,7 +104,7 @@ struct coral_s1_handle {
   long long lat_states = 0;
   std::vector<long long> lat_base;     // [R + 2]
   DevBuf lat_base_d, lat_binom_d, lat_key, lat_nsub, lat_off, lat_sub, lat_maxn, lat_flags_h;
-  DevBuf ws_value[kStreams], ws_f0[kStreams], ws_f1[kStreams], ws_ch[kStreams];
+  DevBuf ws_value[kStreams], ws_f0[kStreams], ws_ch[kStreams];
   cudaStream_t side[kStreams] = {};
   cudaEvent_t side_ev[kStreams] = {};
   cudaEvent_t fork_ev = nullptr;
@@ -209,6 +210,7 @@ __global__ void enumerate_kernel(DevProblem P, int64_t U, unsigned long long* __
         i = j;
       }
       key <<= kKeyTokenBits * (kMaxC - ntok);
+      key |= (unsigned long long)m << (kKeyTokenBits * kMaxC);
     }
   }
   if (r < U) keys[(int64_t)m * U + r] = key;
@@ -216,13 +218,13 @@ __global__ void enumerate_kernel(DevProblem P, int64_t U, unsigned long long* __
   if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(nvalid + m, (unsigned long long)__popc(ballot));
 }
 
-__global__ void seg_offsets_kernel(int NM, int64_t U, const unsigned long long* nvalid,
-                                   int64_t* begin, int64_t* end) {
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m < NM) {
-    begin[m] = (int64_t)m * U;
-    end[m] = (int64_t)m * U + U;
-  }
+struct NotNoCombo {
+  __device__ __forceinline__ bool operator()(unsigned long long k) const { return k != kNoCombo; }
+};
+
+__global__ void strip_model_kernel(unsigned long long* keys, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] &= (1ull << (kKeyTokenBits * kMaxC)) - 1;
 }
 
 __device__ __forceinline__ int decode_key(const DevProblem& P, unsigned long long key,
@@ -286,6 +288,12 @@ __device__ __forceinline__ double record_best(const coral_s1_record& r) {
   return r.num_stages ? r.throughput_tps : kNegInf;
 }
 
+// templates.py:317-324 keeps S if val > best and val > 1e-9 while S ascends; the
+// equivalent order-independent rule also prefers the smaller S on an exact tie.
+__device__ __forceinline__ bool better_S(double val, int S, double best, int bestS) {
+  return val > 1e-9 && (val > best || (val == best && bestS > 0 && S < bestS));
+}
+
 // --------------------------------------------------------------------------------
 // Per-candidate evaluator (exact fallback): one CTA per candidate (model, phase,
 // combo) for S in [S_lo, S_hi], continuing from the candidate's current record.
@@ -295,8 +303,8 @@ __device__ __forceinline__ double record_best(const coral_s1_record& r) {
 // --------------------------------------------------------------------------------
 struct EvalArgs {
   DevProblem P;
-  const unsigned long long* keys;  // sorted per model at m*U
-  int64_t U;
+  const unsigned long long* keys;  // model m's combos at koff[m], str(combo) order
+  const int64_t* koff;
   const int64_t* cand_off;         // [NMP+1]
   int NMP;
   int64_t lo, hi, stride;          // candidates lo, lo+stride, ... < hi
@@ -312,6 +320,7 @@ __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
   __shared__ DpShared sh;
   __shared__ int s_mp, s_cfg[kMaxC];
   __shared__ double s_best;
+  __shared__ int s_bestS;
   __shared__ coral_s1_record s_rec;
   const int64_t ci = A.lo + (int64_t)blockIdx.x * A.stride;
   if (ci >= A.hi) return;
@@ -327,13 +336,14 @@ __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
     const int m = lo / P.NP;
     const int64_t idx = ci - A.cand_off[lo];
     int cfg[kMaxC], cnt[kMaxC];
-    const int C = decode_key(P, A.keys[(int64_t)m * A.U + idx], cfg, cnt);
+    const int C = decode_key(P, A.keys[A.koff[m] + idx], cfg, cnt);
     sh.C = C;
     for (int c = 0; c < C; ++c) { s_cfg[c] = cfg[c]; sh.cnt[c] = cnt[c]; }
     sh.Lu = P.Lu[m];
     sh.LuP = sh.Lu + 1;
     s_rec = A.rec[ci];
     s_best = record_best(s_rec);
+    s_bestS = s_rec.num_stages;
   }
   __syncthreads();
   dp_setup_lattice(sh);
@@ -368,9 +378,11 @@ __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
       dp_run(sh, B, S);
       val = sh.top_val;
     }
-    // templates.py:322: strictly better and > 1e-9 (ties keep the smaller S)
-    if (tid == 0 && val > s_best && val > 1e-9) {
+    // templates.py:322: strictly better and > 1e-9, ties keep the smaller S
+    // (order-independent form, so S values may be evaluated by different kernels)
+    if (tid == 0 && better_S(val, S, s_best, s_bestS)) {
       s_best = val;
+      s_bestS = S;
       if (S == 1) { sh.stage_j[0] = Lu; sh.stage_u[0] = M - 1; }
       else dp_decode(sh, B, S);
       int stage_cnt[kMaxC][kMaxC];
@@ -384,23 +396,21 @@ __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
 }
 
 // --------------------------------------------------------------------------------
-// Lattice top cell: one warp per candidate of one (model, phase) at stage count S.
+// Lattice top cells: one warp per candidate of one (model, phase), every S in smask.
 // f_S[S][Lu][full] = max over u (lanes) of the crossing with f_S[S-1][.][full-u]
-// (or value for S == 2); reduce with the reference tie rule (value desc, u code
-// asc). On a strict improvement (> 1e-9) walk the stored choices back through the
-// lattice layers and write the canonical record.
+// (value_S when S == 2), reduced with the reference tie rule (value desc, u code
+// asc); best S by better_S; the winning S's choices are walked back through its
+// lattice layers into the canonical record.
 // --------------------------------------------------------------------------------
 struct TopArgs {
   LatModel L;
   const int* inv_rank;
   const unsigned long long* keys;   // this model's combos (library order)
   long long ncombo;
-  int S, Lu, g;
-  const double* tabS;               // [K][Lu] at S
-  const double* value;              // [states][Lu+1] at S
-  const double* fprev;              // layer S-1 (value when S == 2)
-  const unsigned short* ch;         // layers 2..S-1, stride layer_stride
-  long long layer_stride;
+  unsigned smask;                   // S values of this chain
+  int K, Lu, g;
+  const double* tab_mp;             // [S][K][Lu]
+  LatWork W;
   const unsigned long long* state_key;
   const long long* off;
   const uint2* subtab;
@@ -408,6 +418,11 @@ struct TopArgs {
 };
 
 __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
+  __shared__ unsigned long long s_binom[160 * 8];
+  for (int i = threadIdx.x; i < 160 * 8; i += blockDim.x) s_binom[i] = A.L.binom[i];
+  __syncthreads();
+  LatModel L = A.L;
+  L.binom = s_binom;
   const int lane = threadIdx.x & 31;
   const long long ci = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= A.ncombo) return;
@@ -415,83 +430,95 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
   const int C = lat_tokens(A.inv_rank, A.keys[ci], cfg, cnt);
   int M = 1, n = 0;
   for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; }
-  const int S = A.S, Lu = A.Lu, LuP = Lu + 1;
-  if (S > n || S > Lu) return;
-  if (S == 1) {  // f[1][L][full] = value[full][L], summed in config order
-    if (lane) return;
-    double v = 0.0;
-    for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], A.tabS[cfg[c] * Lu + (Lu - 1)]));
-    coral_s1_record& r = A.rec[ci];
-    if (v > record_best(r) && v > 1e-9) {
-      int sj[kMaxC] = {Lu};
-      int sc[kMaxC][kMaxC];
-      for (int c = 0; c < C; ++c) sc[0][c] = cnt[c];
-      canonical_record(1, sj, sc, C, cnt, A.g, v, n, &r);
-    }
-    return;
-  }
-  const int jmax = Lu - (S - 1);
-  const int umax = n - (S - 1);
-  double best = kNegInf;
-  int bu = 1 << 20, bj = 0;
-  long long brem = 0;
+  const int Lu = A.Lu, LuP = Lu + 1;
+  const int Smax = min(n, Lu);
+  double tv[kMaxC + 1];
+  int tu[kMaxC + 1], tj[kMaxC + 1];
+#pragma unroll
+  for (int S = 1; S <= kMaxC; ++S) { tv[S] = kNegInf; tu[S] = 1 << 20; tj[S] = 0; }
+  // per lane: its u codes (ascending), every S
   for (int code = lane + 1; code < M; code += 32) {
     int d[kMaxC], e[kMaxC], rest = code;
     for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; e[c] = cnt[c] - d[c]; }
     int su, sr;
-    const long long ru = lat_rank_tokens(A.L, cfg, d, C, &su);
-    if (su > umax) continue;
-    const long long rr = lat_rank_tokens(A.L, cfg, e, C, &sr);
-    double cand;
-    int cj;
-    dp_pair(A.value + ru * LuP, A.fprev + rr * LuP, Lu, jmax, true, cand, cj);
-    if (cand > best) { best = cand; bu = code; bj = cj; brem = rr; }
+    const long long ru = lat_rank_tokens(L, cfg, d, C, &su);
+    const long long rr = lat_rank_tokens(L, cfg, e, C, &sr);
+#pragma unroll
+    for (int S = 2; S <= kMaxC; ++S) {
+      if (S > Smax || !((A.smask >> S) & 1u) || su > n - (S - 1)) continue;
+      double cand;
+      int cj;
+      dp_pair(A.W.val(S) + ru * LuP, A.W.lay(S, S - 1) + rr * LuP, Lu, Lu - (S - 1), true, cand, cj);
+      if (cand > tv[S]) { tv[S] = cand; tu[S] = code; tj[S] = cj; }
+    }
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ob = __shfl_down_sync(0xffffffffu, best, o);
-    const int ou = __shfl_down_sync(0xffffffffu, bu, o);
-    const int oj = __shfl_down_sync(0xffffffffu, bj, o);
-    const long long orr = __shfl_down_sync(0xffffffffu, brem, o);
-    if (ob > best || (ob == best && ou < bu)) { best = ob; bu = ou; bj = oj; brem = orr; }
+#pragma unroll
+  for (int S = 2; S <= kMaxC; ++S) {
+    if (S > Smax || !((A.smask >> S) & 1u)) continue;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_down_sync(0xffffffffu, tv[S], o);
+      const int ou = __shfl_down_sync(0xffffffffu, tu[S], o);
+      const int oj = __shfl_down_sync(0xffffffffu, tj[S], o);
+      if (ob > tv[S] || (ob == tv[S] && ou < tu[S])) { tv[S] = ob; tu[S] = ou; tj[S] = oj; }
+    }
   }
   if (lane) return;
-  coral_s1_record& r = A.rec[ci];
-  if (!(best > record_best(r) && best > 1e-9)) return;
-  // walk back (kernels.py:258-275): stage 0 is the top choice
+  if (A.smask & 2u) {  // S = 1: f[1][L][full] = value[full][L], summed in config order
+    double v = 0.0;
+    const double* tab1 = A.tab_mp;
+    for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], tab1[cfg[c] * Lu + (Lu - 1)]));
+    tv[1] = v;
+  }
+  coral_s1_record r = A.rec[ci];
+  double best = record_best(r);
+  int bestS = r.num_stages, win = 0;
+#pragma unroll
+  for (int S = 1; S <= kMaxC; ++S) {
+    if (S > Smax || !((A.smask >> S) & 1u)) continue;
+    if (better_S(tv[S], S, best, bestS)) { best = tv[S]; bestS = S; win = S; }
+  }
+  if (!win) return;
   int sj[kMaxC], sc[kMaxC][kMaxC];
-  {
-    int rest = bu;
-    for (int c = 0; c < C; ++c) { sc[0][c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; }
-    sj[0] = bj;
+  if (win == 1) {
+    sj[0] = Lu;
+    for (int c = 0; c < C; ++c) sc[0][c] = cnt[c];
+  } else {
+    // walk back (kernels.py:258-275): stage 0 is the top choice
+    int ucode = 0, uj = 0;
+#pragma unroll
+    for (int S = 2; S <= kMaxC; ++S) if (S == win) { ucode = tu[S]; uj = tj[S]; }
+    int e[kMaxC], rest = ucode;
+    for (int c = 0; c < C; ++c) { sc[0][c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; e[c] = cnt[c] - sc[0][c]; }
+    sj[0] = uj;
+    int sr;
+    long long X = lat_rank_tokens(L, cfg, e, C, &sr);
+    int l = Lu - uj;
+    for (int s = 1; s < win; ++s) {
+      const int sg = win - s;
+      int xc[kMaxC], xn[kMaxC];
+      const int XC = lat_tokens(A.inv_rank, A.state_key[X], xc, xn);
+      int uc = -1, j = l;
+      if (sg > 1) {
+        const unsigned short chv = A.W.chl(win, sg)[X * LuP + l];
+        uc = chv >> 10;
+        j = chv & 1023;
+      }
+      int ud[kMaxC];
+      if (uc < 0) { for (int t = 0; t < XC; ++t) ud[t] = xn[t]; }
+      else {
+        int rr = uc;
+        for (int t = 0; t < XC; ++t) { ud[t] = rr % (xn[t] + 1); rr /= xn[t] + 1; }
+      }
+      for (int c = 0; c < C; ++c) {
+        sc[s][c] = 0;
+        for (int t = 0; t < XC; ++t) if (xc[t] == cfg[c]) sc[s][c] = ud[t];
+      }
+      sj[s] = j;
+      if (uc >= 0) X = A.subtab[A.off[X] + uc].y;
+      l -= j;
+    }
   }
-  long long X = brem;
-  int l = Lu - bj;
-  for (int s = 1; s < S; ++s) {
-    const int sg = S - s;
-    int xc[kMaxC], xn[kMaxC];
-    const int XC = lat_tokens(A.inv_rank, A.state_key[X], xc, xn);
-    int ucode, j;
-    if (sg == 1) { ucode = -1; j = l; }
-    else {
-      const unsigned short chv = A.ch[(long long)(sg - 2) * A.layer_stride + X * LuP + l];
-      ucode = chv >> 10;
-      j = chv & 1023;
-    }
-    int ud[kMaxC];
-    if (ucode < 0) { for (int t = 0; t < XC; ++t) ud[t] = xn[t]; }
-    else {
-      int rest = ucode;
-      for (int t = 0; t < XC; ++t) { ud[t] = rest % (xn[t] + 1); rest /= xn[t] + 1; }
-    }
-    for (int c = 0; c < C; ++c) {
-      sc[s][c] = 0;
-      for (int t = 0; t < XC; ++t) if (xc[t] == cfg[c]) sc[s][c] = ud[t];
-    }
-    sj[s] = j;
-    if (ucode >= 0) X = A.subtab[A.off[X] + ucode].y;
-    l -= j;
-  }
-  canonical_record(S, sj, sc, C, cnt, A.g, best, n, &r);
+  canonical_record(win, sj, sc, C, cnt, A.g, best, n, &A.rec[ci]);
 }
 
 // --------------------------------------------------------------------------------
@@ -571,7 +598,7 @@ __global__ void __launch_bounds__(kDpThreads) placement_op_kernel(OpArgs A) {
 struct FrontArgs {
   DevProblem P;
   const unsigned long long* keys;
-  int64_t U;
+  const int64_t* koff;
   const int64_t* cand_off;
   int NMP;
   const coral_s1_record* rec;
@@ -598,7 +625,7 @@ __global__ void frontier_items_kernel(FrontArgs A) {
         if (A.cand_off[mid] <= ci) lo = mid; else hi = mid;
       }
       const int m = lo / A.P.NP;
-      const unsigned long long key = A.keys[(int64_t)m * A.U + (ci - A.cand_off[lo])];
+      const unsigned long long key = A.keys[A.koff[m] + (ci - A.cand_off[lo])];
       int cfg[kMaxC], cnt[kMaxC];
       const int C = decode_key(A.P, key, cfg, cnt);
       double total = 0.0;
@@ -820,7 +847,7 @@ int coral_s1_create(int device, coral_s1_handle** out) {
 int coral_s1_destroy(coral_s1_handle* h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
-  DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->seg_off,
+  DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->keys_tmp, &h->koff_d,
                     &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
                     &h->sort_a, &h->sort_b, &h->perm_a, &h->perm_b, &h->segk, &h->scanv,
                     &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d,
@@ -828,7 +855,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
                     &h->lat_sub, &h->lat_maxn, &h->lat_flags_h};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
-    h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_f1[i].release(); h->ws_ch[i].release();
+    h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release();
     if (h->side[i]) cudaStreamDestroy(h->side[i]);
     if (h->side_ev[i]) cudaEventDestroy(h->side_ev[i]);
   }
@@ -1003,35 +1030,55 @@ int coral_s1_enumerate(coral_s1_handle* h) {
   const int64_t U = h->U;
   const int64_t tot = std::max<int64_t>((int64_t)NM * U, 1);
   int rc;
-  if ((rc = h->keys_raw.ensure(tot * 8)) || (rc = h->keys.ensure(tot * 8)) ||
-      (rc = h->nvalid.ensure(std::max(NM, 1) * 8)) || (rc = h->seg_off.ensure(std::max(NM, 1) * 16)))
+  if ((rc = h->keys_raw.ensure(tot * 8)) || (rc = h->nvalid.ensure(std::max(NM, 1) * 8 + 16)))
     return rc;
   cudaStream_t st = h->stream;
   CUDA_TRY(cudaEventRecord(h->ev[2], st));
   h->counts.assign(NM, 0);
+  h->koff.assign(NM + 1, 0);
   if (NM > 0 && U > 0) {
     CUDA_TRY(cudaMemsetAsync(h->nvalid.p, 0, NM * 8, st));
     dim3 grid((unsigned)((U + 255) / 256), NM);
     enumerate_kernel<<<grid, 256, 0, st>>>(h->dp, U, h->keys_raw.as<unsigned long long>(),
                                            h->nvalid.as<unsigned long long>());
     LAUNCH_CHECK(h);
-    int64_t* beg = h->seg_off.as<int64_t>();
-    int64_t* end = beg + NM;
-    seg_offsets_kernel<<<(NM + 127) / 128, 128, 0, st>>>(NM, U, h->nvalid.as<unsigned long long>(), beg, end);
-    LAUNCH_CHECK(h);
-    size_t tmp = 0;
-    cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp, h->keys_raw.as<unsigned long long>(),
-                                            h->keys.as<unsigned long long>(), (int)(NM * U), NM, beg,
-                                            end, 0, 64, st);
-    if ((rc = ensure_tmp(h, tmp))) return rc;
-    CUDA_TRY(cub::DeviceSegmentedRadixSort::SortKeys(h->cub_tmp.p, tmp, h->keys_raw.as<unsigned long long>(),
-                                                     h->keys.as<unsigned long long>(), (int)(NM * U), NM,
-                                                     beg, end, 0, 64, st));
-    h->launches += 4;
     std::vector<unsigned long long> nv(NM);
     CUDA_TRY(cudaMemcpyAsync(nv.data(), h->nvalid.p, NM * 8, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    for (int m = 0; m < NM; ++m) h->counts[m] = (int64_t)nv[m];
+    for (int m = 0; m < NM; ++m) {
+      h->counts[m] = (int64_t)nv[m];
+      h->koff[m + 1] = h->koff[m] + h->counts[m];
+    }
+    const int64_t nk = h->koff[NM];
+    if ((rc = h->keys.ensure(std::max<int64_t>(nk, 1) * 8)) ||
+        (rc = h->keys_tmp.ensure(std::max<int64_t>(nk, 1) * 8)))
+      return rc;
+    if (nk > 0) {
+    // compact the window survivors (keys carry the model index above bit 54) ...
+    size_t tmp = 0;
+    NotNoCombo pred;
+    cub::DeviceSelect::If(nullptr, tmp, h->keys_raw.as<unsigned long long>(),
+                          h->keys_tmp.as<unsigned long long>(), h->nvalid.as<long long>() + NM,
+                          (int)(NM * U), pred, st);
+    if ((rc = ensure_tmp(h, tmp))) return rc;
+    CUDA_TRY(cub::DeviceSelect::If(h->cub_tmp.p, tmp, h->keys_raw.as<unsigned long long>(),
+                                   h->keys_tmp.as<unsigned long long>(), h->nvalid.as<long long>() + NM,
+                                   (int)(NM * U), pred, st));
+    // ... then one radix sort: model-major, str(combo) order within a model
+    int mbits = 0;
+    while ((1 << mbits) < NM) ++mbits;
+    tmp = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tmp, h->keys_tmp.as<unsigned long long>(),
+                                   h->keys.as<unsigned long long>(), (int)nk, 0,
+                                   kKeyTokenBits * kMaxC + mbits, st);
+    if ((rc = ensure_tmp(h, tmp))) return rc;
+    CUDA_TRY(cub::DeviceRadixSort::SortKeys(h->cub_tmp.p, tmp, h->keys_tmp.as<unsigned long long>(),
+                                            h->keys.as<unsigned long long>(), (int)nk, 0,
+                                            kKeyTokenBits * kMaxC + mbits, st));
+    strip_model_kernel<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(h->keys.as<unsigned long long>(), nk);
+    h->launches += 6;
+    LAUNCH_CHECK(h);
+    }
   }
   CUDA_TRY(cudaEventRecord(h->ev[3], st));
   // candidate list: mp-major, library order within each (model, phase)
@@ -1039,7 +1086,7 @@ int coral_s1_enumerate(coral_s1_handle* h) {
   h->cand_off.assign(NMP + 1, 0);
   for (int mp = 0; mp < NMP; ++mp) h->cand_off[mp + 1] = h->cand_off[mp] + h->counts[mp / h->NP];
   h->ncand = h->cand_off[NMP];
-  if ((rc = upload(h, h->cand_off_d, h->cand_off))) return rc;
+  if ((rc = upload(h, h->cand_off_d, h->cand_off)) || (rc = upload(h, h->koff_d, h->koff))) return rc;
   h->have_enum = true;
   h->have_eval = false;
   return 0;
@@ -1058,7 +1105,7 @@ int coral_s1_get_combos(coral_s1_handle* h, int model, int enumeration_order, ui
   const int64_t cnt = h->counts[model];
   if (n < cnt) return fail(CORAL_S1_EINVAL, "output too small");
   if (cnt)
-    CUDA_TRY(cudaMemcpyAsync(keys, h->keys.as<unsigned long long>() + (int64_t)model * h->U, cnt * 8,
+    CUDA_TRY(cudaMemcpyAsync(keys, h->keys.as<unsigned long long>() + h->koff[model], cnt * 8,
                              cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   if (enumeration_order) {
@@ -1090,7 +1137,7 @@ static int launch_percombo(coral_s1_handle* h, cudaStream_t st, int64_t lo, int6
   EvalArgs A;
   A.P = h->dp;
   A.keys = h->keys.as<unsigned long long>();
-  A.U = h->U;
+  A.koff = h->koff_d.as<int64_t>();
   A.cand_off = h->cand_off_d.as<int64_t>();
   A.NMP = h->NM * h->NP;
   A.hi = hi;
@@ -1158,83 +1205,84 @@ static int lattice_prepare(coral_s1_handle* h) {
     const long long nc = h->counts[m];
     if (!nc) continue;
     lat_maxn_kernel<<<(unsigned)((nc * 64 + 255) / 256), 256, 0, st>>>(
-        L, h->dp.inv_rank, h->keys.as<unsigned long long>() + (int64_t)m * h->U, nc,
+        L, h->dp.inv_rank, h->keys.as<unsigned long long>() + h->koff[m], nc,
         h->lat_maxn.as<unsigned>() + (size_t)m * ns);
     LAUNCH_CHECK(h);
   }
   // workspaces
   const long long LuP = h->maxLu + 1;
+  const long long nS = std::max(h->n_max - 1, 1);                         // S = 2..n_max
+  const long long nch = std::max((h->n_max - 2) * (h->n_max - 1) / 2, 1);  // (S, sg) choice layers
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
-    if ((rc = h->ws_value[i].ensure(ns * LuP * 8)) || (rc = h->ws_f0[i].ensure(ns * LuP * 8)) ||
-        (rc = h->ws_f1[i].ensure(ns * LuP * 8)) ||
-        (rc = h->ws_ch[i].ensure((size_t)std::max(h->n_max - 2, 1) * ns * LuP * 2)))
+    if ((rc = h->ws_value[i].ensure(nS * ns * LuP * 8)) || (rc = h->ws_f0[i].ensure(2 * nS * ns * LuP * 8)) ||
+        (rc = h->ws_ch[i].ensure(nch * ns * LuP * 2)))
       return rc;
   }
   return 0;
 }
 
-// One (model, phase) unit chain: S values ascending on stream `slot`.
+// One (model, phase) chain on stream `slot`: lattice for every monotone S of the
+// chain, the exact per-candidate kernel for the others.
 static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss, int slot) {
   cudaStream_t st = h->side[slot];
   const int m = mp / h->NP;
-  const int K = h->K, Lu = h->Lu[m], g = h->g[m];
+  const int K = h->K, Lu = h->Lu[m];
   const long long ns = h->lat_states, LuP = h->maxLu + 1;
   const long long ncombo = h->counts[m];
   if (!ncombo) return 0;
   LatModel L{K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
-  const unsigned long long* keys = h->keys.as<unsigned long long>() + (int64_t)m * h->U;
-  coral_s1_record* rec = h->rec.as<coral_s1_record>() + h->cand_off[mp];
-  double* value = h->ws_value[slot].as<double>();
-  double* fb[2] = {h->ws_f0[slot].as<double>(), h->ws_f1[slot].as<double>()};
-  unsigned short* ch = h->ws_ch[slot].as<unsigned short>();
-  const long long layer_stride = ns * LuP;
+  unsigned smask = 0;
+  int Smax = 0;
   for (int S : Ss) {
     bool mono = true;  // kernels.py:291 over every config row at (mp, S)
     for (int c = 0; c < K; ++c) mono &= (h->flags_h[((size_t)mp * h->n_max + (S - 1)) * K + c] & 1) != 0;
-    if (!mono) {  // exact per-candidate fallback for this S
+    if (!mono) {  // exact per-candidate kernel for this S
       int rc = launch_percombo(h, st, h->cand_off[mp], h->cand_off[mp + 1], 1, S, S);
       if (rc) return rc;
       continue;
     }
-    const double* tabS = h->tab.as<double>() + h->tab_off[mp] + (int64_t)(S - 1) * K * Lu;
-    if (S >= 2) {
-      const long long nv = ns * Lu;
-      lat_value_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(
-          L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(), tabS, Lu, value);
-      LAUNCH_CHECK(h);
-      // value rows use stride Lu+1 of this model; the workspaces are sized for maxLu
-    }
-    for (int sg = 2; sg <= S - 1; ++sg) {
-      const int smaxsz = std::min(h->n_max - 1, h->n_max - (S - sg));
-      if (smaxsz < sg || Lu - (S - sg) < sg) continue;
-      const long long nst = h->lat_base[smaxsz + 1] - h->lat_base[sg];
-      const double* fprev = (sg == 2) ? value : fb[(sg - 1) & 1];
-      lat_layer_kernel<<<(unsigned)((nst * 32 + 255) / 256), 256, 0, st>>>(
-          L, S, sg, smaxsz, Lu, h->lat_maxn.as<unsigned>() + (size_t)m * ns,
-          h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), value, fprev, fb[sg & 1],
-          ch + (sg - 2) * layer_stride);
-      LAUNCH_CHECK(h);
-    }
-    TopArgs T;
-    T.L = L;
-    T.inv_rank = h->dp.inv_rank;
-    T.keys = keys;
-    T.ncombo = ncombo;
-    T.S = S;
-    T.Lu = Lu;
-    T.g = g;
-    T.tabS = tabS;
-    T.value = value;
-    T.fprev = (S == 2) ? value : fb[(S - 1) & 1];
-    T.ch = ch;
-    T.layer_stride = layer_stride;
-    T.state_key = h->lat_key.as<unsigned long long>();
-    T.off = h->lat_off.as<long long>();
-    T.subtab = h->lat_sub.as<uint2>();
-    T.rec = rec;
-    lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
+    smask |= 1u << S;
+    Smax = std::max(Smax, S);
+  }
+  if (!smask) return 0;
+  LatWork W;
+  W.value = h->ws_value[slot].as<double>();
+  W.f = h->ws_f0[slot].as<double>();
+  W.ch = h->ws_ch[slot].as<unsigned short>();
+  W.stride = ns * (Lu + 1);
+  (void)LuP;
+  const double* tab_mp = h->tab.as<double>() + h->tab_off[mp];
+  if (Smax >= 2 && ns > 0) {
+    const long long nv = ns * Lu;
+    lat_value_kernel<<<dim3((unsigned)((nv + 255) / 256), Smax - 1), 256, 0, st>>>(
+        L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(), tab_mp, K, Lu, 2, smask, W);
     LAUNCH_CHECK(h);
   }
+  for (int sg = 2; sg <= Smax - 1; ++sg) {
+    const long long nst = h->lat_base[h->n_max - 1 + 1] - h->lat_base[sg];
+    if (nst <= 0) continue;
+    lat_layer_kernel<<<dim3((unsigned)((nst * 32 + 255) / 256), Smax - sg), 256, 0, st>>>(
+        L, sg, sg + 1, smask, h->n_max, Lu, h->lat_maxn.as<unsigned>() + (size_t)m * ns,
+        h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), W);
+    LAUNCH_CHECK(h);
+  }
+  TopArgs T;
+  T.L = L;
+  T.inv_rank = h->dp.inv_rank;
+  T.keys = h->keys.as<unsigned long long>() + h->koff[m];
+  T.ncombo = ncombo;
+  T.smask = smask;
+  T.K = K;
+  T.Lu = Lu;
+  T.g = h->g[m];
+  T.tab_mp = tab_mp;
+  T.W = W;
+  T.state_key = h->lat_key.as<unsigned long long>();
+  T.off = h->lat_off.as<long long>();
+  T.subtab = h->lat_sub.as<uint2>();
+  T.rec = h->rec.as<coral_s1_record>() + h->cand_off[mp];
+  lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
+  LAUNCH_CHECK(h);
   return 0;
 }
 
@@ -1360,7 +1408,7 @@ int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices,
     FrontArgs A;
     A.P = h->dp;
     A.keys = h->keys.as<unsigned long long>();
-    A.U = h->U;
+    A.koff = h->koff_d.as<int64_t>();
     A.cand_off = h->cand_off_d.as<int64_t>();
     A.NMP = h->NM * h->NP;
     A.rec = h->rec.as<coral_s1_record>();

@@ -122,7 +122,7 @@ __global__ void lat_maxn_kernel(LatModel L, const int* __restrict__ inv_rank,
   int s;
   const long long r = lat_rank_tokens(L, cfg, d, C, &s);
   if (s > L.R) return;
-  atomicMax(maxn + r, (unsigned)n);
+  if (maxn[r] < (unsigned)n) atomicMax(maxn + r, (unsigned)n);  // popular states saturate fast
 }
 
 // nsub[idx] = M(X) = prod(counts + 1)
@@ -163,33 +163,54 @@ __global__ void lat_subtab_kernel(LatModel L, const int* __restrict__ inv_rank,
   }
 }
 
-// ---- per (model, phase, S) ----------------------------------------------------
+// ---- per (model, phase): every S at once ----------------------------------------
 
-// value[idx][j], j = 1..Lu (kernels.py:164-170) from the S table rows.
+// Workspace of one (model, phase) chain: per S = 2..n_max a value table and two
+// ping-pong f layers, plus one choice layer per (S, sg), sg = 2..S-1.
+struct LatWork {
+  double* value;          // [S-2][states][LuP]
+  double* f;              // [S-2][2][states][LuP]
+  unsigned short* ch;     // [tri(S) + sg-2][states][LuP]
+  long long stride;       // states * LuP
+  __device__ __forceinline__ double* val(int S) const { return value + (long long)(S - 2) * stride; }
+  __device__ __forceinline__ double* lay(int S, int sg) const {
+    return sg == 1 ? val(S) : f + ((long long)(S - 2) * 2 + (sg & 1)) * stride;
+  }
+  __device__ __forceinline__ unsigned short* chl(int S, int sg) const {
+    return ch + ((long long)((S - 3) * (S - 2) / 2) + (sg - 2)) * stride;
+  }
+};
+
+// value_S[idx][j], j = 1..Lu (kernels.py:164-170) for S in [S_lo, S_lo + gridDim.y).
 __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
                                  const unsigned long long* __restrict__ state_key,
-                                 const double* __restrict__ tabS /* [K][Lu] */, int Lu,
-                                 double* __restrict__ value) {
+                                 const double* __restrict__ tab_mp /* [S][K][Lu] */, int K, int Lu,
+                                 int S_lo, unsigned smask, LatWork W) {
+  const int S = S_lo + blockIdx.y;
+  if (!((smask >> S) & 1u)) return;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long idx = t / Lu;
   const int j = (int)(t - idx * Lu) + 1;
   if (idx >= L.base[L.R + 1]) return;
+  const double* tabS = tab_mp + (long long)(S - 1) * K * Lu;
   int cfg[kMaxC], cnt[kMaxC];
   const int C = lat_tokens(inv_rank, state_key[idx], cfg, cnt);
   double v = 0.0;
   for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], tabS[cfg[c] * Lu + (j - 1)]));
-  value[idx * (Lu + 1) + j] = v;
+  W.val(S)[idx * (Lu + 1) + j] = v;
 }
 
-// One DP layer sg of stage count S: warp per state X, lanes over l.
+// DP layer sg for every S in [S_lo, S_lo + gridDim.y) with S > sg: warp per state X,
+// lanes over l. Cells: sg <= |X| <= maxn(X) - (S - sg), sg <= l <= Lu - (S - sg).
 __global__ void __launch_bounds__(256) lat_layer_kernel(
-    LatModel L, int S, int sg, int smaxsz, int Lu, const unsigned* __restrict__ maxn,
-    const long long* __restrict__ off, const uint2* __restrict__ subtab,
-    const double* __restrict__ value, const double* __restrict__ fprev, double* __restrict__ fout,
-    unsigned short* __restrict__ chout) {
+    LatModel L, int sg, int S_lo, unsigned smask, int n_max, int Lu, const unsigned* __restrict__ maxn,
+    const long long* __restrict__ off, const uint2* __restrict__ subtab, LatWork W) {
+  const int S = S_lo + blockIdx.y;
+  if (!((smask >> S) & 1u) || S <= sg) return;
   const int lane = threadIdx.x & 31;
+  const int smaxsz = min(L.R, n_max - (S - sg));
   const long long idx = L.base[sg] + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  if (idx >= L.base[smaxsz + 1]) return;  // |X| <= n_max - (S - sg)
+  if (smaxsz < sg || idx >= L.base[smaxsz + 1]) return;
   int s = sg;
   while (idx >= L.base[s + 1]) ++s;
   if (s > (int)maxn[idx] - (S - sg)) return;  // no candidate reaches this cell
@@ -198,6 +219,10 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
   const int usz = s - (sg - 1);  // |u| <= |X| - (sg - 1)
   const long long o = off[idx];
   const long long M = off[idx + 1] - o;
+  const double* __restrict__ value = W.val(S);
+  const double* __restrict__ fprev = W.lay(S, sg - 1);
+  double* __restrict__ fout = W.lay(S, sg);
+  unsigned short* __restrict__ chout = W.chl(S, sg);
   for (int l0 = sg; l0 <= lmax; l0 += 32) {
     const int l = l0 + lane;
     const bool act = l <= lmax;
