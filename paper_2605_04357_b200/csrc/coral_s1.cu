@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -101,6 +102,8 @@ struct coral_s1_handle {
   DevBuf op_in, op_out, tab_off_d;
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
   static constexpr int kStreams = 4;
+  int nstreams = kStreams;  // side streams in use (CORAL_S1_STREAMS)
+  bool top_per_S = false;   // one top-cell launch per S (CORAL_S1_TOP_PER_S)
   long long lat_states = 0;
   std::vector<long long> lat_base;     // [R + 2]
   DevBuf lat_base_d, lat_binom_d, lat_key, lat_nsub, lat_off, lat_sub, lat_maxn, lat_flags_h;
@@ -432,82 +435,81 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
   for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; }
   const int Lu = A.Lu, LuP = Lu + 1;
   const int Smax = min(n, Lu);
-  double tv[kMaxC + 1];
-  int tu[kMaxC + 1], tj[kMaxC + 1];
+  // this lane's u codes (lane+1, lane+33): size, rank(u), rank(full-u), computed once
+  int su[2];
+  long long ru[2], rr[2];
 #pragma unroll
-  for (int S = 1; S <= kMaxC; ++S) { tv[S] = kNegInf; tu[S] = 1 << 20; tj[S] = 0; }
-  // per lane: its u codes (ascending), every S
-  for (int code = lane + 1; code < M; code += 32) {
-    int d[kMaxC], e[kMaxC], rest = code;
-    for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; e[c] = cnt[c] - d[c]; }
-    int su, sr;
-    const long long ru = lat_rank_tokens(L, cfg, d, C, &su);
-    const long long rr = lat_rank_tokens(L, cfg, e, C, &sr);
-#pragma unroll
-    for (int S = 2; S <= kMaxC; ++S) {
-      if (S > Smax || !((A.smask >> S) & 1u) || su > n - (S - 1)) continue;
+  for (int k = 0; k < 2; ++k) {
+    const int code = lane + 1 + 32 * k;
+    su[k] = 1 << 20;
+    ru[k] = rr[k] = 0;
+    if (code < M) {
+      int d[kMaxC], e[kMaxC], rest = code;
+      for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; e[c] = cnt[c] - d[c]; }
+      int sr;
+      ru[k] = lat_rank_tokens(L, cfg, d, C, &su[k]);
+      rr[k] = lat_rank_tokens(L, cfg, e, C, &sr);
+    }
+  }
+  // S ascending; strict improvement (templates.py:322) -> smaller S on ties
+  double tbest = kNegInf;
+  int twin = 0, tcode = 0, tj = 0;
+  if ((A.smask & 2u) && Smax >= 1) {  // S = 1: f[1][L][full] = value[full][L]
+    double v = 0.0;
+    for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], A.tab_mp[cfg[c] * Lu + (Lu - 1)]));
+    if (v > 1e-9) { tbest = v; twin = 1; }
+  }
+  for (int S = 2; S <= Smax; ++S) {
+    if (!((A.smask >> S) & 1u)) continue;
+    const double* val = A.W.val(S);
+    const double* lay = A.W.lay(S, S - 1);
+    double best = kNegInf;
+    int bu = 1 << 20, bj = 0;
+    for (int k = 0; k < 2; ++k) {
+      if (su[k] > n - (S - 1)) continue;
       double cand;
       int cj;
-      dp_pair(A.W.val(S) + ru * LuP, A.W.lay(S, S - 1) + rr * LuP, Lu, Lu - (S - 1), true, cand, cj);
-      if (cand > tv[S]) { tv[S] = cand; tu[S] = code; tj[S] = cj; }
+      dp_pair(val + ru[k] * LuP, lay + rr[k] * LuP, Lu, Lu - (S - 1), true, cand, cj);
+      if (cand > best) { best = cand; bu = lane + 1 + 32 * k; bj = cj; }
     }
-  }
-#pragma unroll
-  for (int S = 2; S <= kMaxC; ++S) {
-    if (S > Smax || !((A.smask >> S) & 1u)) continue;
     for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_down_sync(0xffffffffu, tv[S], o);
-      const int ou = __shfl_down_sync(0xffffffffu, tu[S], o);
-      const int oj = __shfl_down_sync(0xffffffffu, tj[S], o);
-      if (ob > tv[S] || (ob == tv[S] && ou < tu[S])) { tv[S] = ob; tu[S] = ou; tj[S] = oj; }
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int ou = __shfl_xor_sync(0xffffffffu, bu, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ob > best || (ob == best && ou < bu)) { best = ob; bu = ou; bj = oj; }
     }
+    if (best > tbest && best > 1e-9) { tbest = best; twin = S; tcode = bu; tj = bj; }
   }
-  if (lane) return;
-  if (A.smask & 2u) {  // S = 1: f[1][L][full] = value[full][L], summed in config order
-    double v = 0.0;
-    const double* tab1 = A.tab_mp;
-    for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], tab1[cfg[c] * Lu + (Lu - 1)]));
-    tv[1] = v;
-  }
+  if (lane || !twin) return;
   coral_s1_record r = A.rec[ci];
-  double best = record_best(r);
-  int bestS = r.num_stages, win = 0;
-#pragma unroll
-  for (int S = 1; S <= kMaxC; ++S) {
-    if (S > Smax || !((A.smask >> S) & 1u)) continue;
-    if (better_S(tv[S], S, best, bestS)) { best = tv[S]; bestS = S; win = S; }
-  }
-  if (!win) return;
+  if (!better_S(tbest, twin, record_best(r), r.num_stages)) return;
   int sj[kMaxC], sc[kMaxC][kMaxC];
-  if (win == 1) {
+  if (twin == 1) {
     sj[0] = Lu;
     for (int c = 0; c < C; ++c) sc[0][c] = cnt[c];
   } else {
     // walk back (kernels.py:258-275): stage 0 is the top choice
-    int ucode = 0, uj = 0;
-#pragma unroll
-    for (int S = 2; S <= kMaxC; ++S) if (S == win) { ucode = tu[S]; uj = tj[S]; }
-    int e[kMaxC], rest = ucode;
+    int e[kMaxC], rest = tcode;
     for (int c = 0; c < C; ++c) { sc[0][c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; e[c] = cnt[c] - sc[0][c]; }
-    sj[0] = uj;
+    sj[0] = tj;
     int sr;
     long long X = lat_rank_tokens(L, cfg, e, C, &sr);
-    int l = Lu - uj;
-    for (int s = 1; s < win; ++s) {
-      const int sg = win - s;
+    int l = Lu - tj;
+    for (int s = 1; s < twin; ++s) {
+      const int sg = twin - s;
       int xc[kMaxC], xn[kMaxC];
       const int XC = lat_tokens(A.inv_rank, A.state_key[X], xc, xn);
       int uc = -1, j = l;
       if (sg > 1) {
-        const unsigned short chv = A.W.chl(win, sg)[X * LuP + l];
+        const unsigned short chv = A.W.chl(twin, sg)[X * LuP + l];
         uc = chv >> 10;
         j = chv & 1023;
       }
       int ud[kMaxC];
       if (uc < 0) { for (int t = 0; t < XC; ++t) ud[t] = xn[t]; }
       else {
-        int rr = uc;
-        for (int t = 0; t < XC; ++t) { ud[t] = rr % (xn[t] + 1); rr /= xn[t] + 1; }
+        int q = uc;
+        for (int t = 0; t < XC; ++t) { ud[t] = q % (xn[t] + 1); q /= xn[t] + 1; }
       }
       for (int c = 0; c < C; ++c) {
         sc[s][c] = 0;
@@ -518,7 +520,7 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
       l -= j;
     }
   }
-  canonical_record(win, sj, sc, C, cnt, A.g, best, n, &A.rec[ci]);
+  canonical_record(twin, sj, sc, C, cnt, A.g, tbest, n, &A.rec[ci]);
 }
 
 // --------------------------------------------------------------------------------
@@ -833,6 +835,8 @@ int coral_s1_create(int device, coral_s1_handle** out) {
     cudaEventCreateWithFlags(&h->side_ev[i], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
+  if (const char* e = getenv("CORAL_S1_STREAMS")) h->nstreams = std::max(1, std::min(atoi(e), coral_s1_handle::kStreams));
+  if (const char* e = getenv("CORAL_S1_TOP_PER_S")) h->top_per_S = atoi(e) != 0;
   if (h->lat_binom_d.ensure(sizeof(tab)) == 0)
     cudaMemcpy(h->lat_binom_d.p, tab, sizeof(tab), cudaMemcpyHostToDevice);
   const size_t smem_max = dp_smem_bytes(kMaxM, CORAL_S1_MAX_LAYER_UNITS + 1, CORAL_S1_MAX_LAYER_UNITS);
@@ -1281,8 +1285,17 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   T.off = h->lat_off.as<long long>();
   T.subtab = h->lat_sub.as<uint2>();
   T.rec = h->rec.as<coral_s1_record>() + h->cand_off[mp];
-  lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
-  LAUNCH_CHECK(h);
+  if (h->top_per_S) {  // one launch per S: working set value_S + f_S[S-1] stays in L2
+    for (int S = 1; S <= Smax; ++S) {
+      if (!((smask >> S) & 1u)) continue;
+      T.smask = 1u << S;
+      lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
+      LAUNCH_CHECK(h);
+    }
+  } else {
+    lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
+    LAUNCH_CHECK(h);
+  }
   return 0;
 }
 
@@ -1321,7 +1334,7 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
       if (take(mp, S)) Ss.push_back(S);
     if (Ss.empty() || !h->counts[m]) continue;
     if ((rc = lattice_units(h, mp, Ss, slot))) return rc;
-    slot = (slot + 1) % coral_s1_handle::kStreams;
+    slot = (slot + 1) % h->nstreams;
   }
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     CUDA_TRY(cudaEventRecord(h->side_ev[i], h->side[i]));
