@@ -191,6 +191,7 @@ def main():
     from paper_2605_04357_b200 import _native, build_frontier, catalog
     from paper_2605_04357_b200.frontier import _merge_across_ranks, _price_matrix
     from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem
+    from paper_2605_04357_b200.shard import assign_units
 
     w = catalog.WORKLOADS[args.workload]()
     caps, ctx = LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf, granularity=w.granularity)
@@ -203,9 +204,10 @@ def main():
         h.tables()
         h.enumerate()
         if world > 1:
-            h.evaluate_shard(rank, world)
-            n_local = h.frontier(pmat)
             prob.counts = h.num_combos()
+            _, lsteps, smax = h.table_layout()
+            h.evaluate_units(assign_units(prob.counts, lsteps, smax, 2, world)[rank])
+            n_local = h.frontier(pmat)
             return _merge_across_ranks(prob, n_local, tdist)
         h.evaluate(0, -1)
         return h.frontier(pmat)

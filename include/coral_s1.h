@@ -154,9 +154,10 @@ int coral_s1_get_combos(coral_s1_handle* h, int model, int enumeration_order,
  * [lo, hi) of the global (model, phase, combo) list (mp-major, library order);
  * hi < 0 means all. Placement DP = _placement_dp_nb (kernels.py:143-276). */
 int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi);
-/* multi-GPU shard: candidates rank, rank+world, rank+2*world, ... (interleaving
- * balances the ~100x per-candidate cost spread across ranks) */
-int coral_s1_evaluate_shard(coral_s1_handle* h, int rank, int world);
+/* multi-GPU units: smask[mp] bit S set = evaluate stage count S of (model, phase)
+ * mp; records hold each candidate's best over the given S values (ties -> fewer
+ * stages), so disjoint masks on different ranks merge exactly. */
+int coral_s1_evaluate_units(coral_s1_handle* h, const uint32_t* smask);
 int coral_s1_num_candidates(const coral_s1_handle* h, int64_t* n);
 /* records of one (model, phase slot), library order; n = its combo count */
 int coral_s1_get_records(coral_s1_handle* h, int mp, coral_s1_record* out, int64_t n);

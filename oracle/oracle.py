@@ -48,7 +48,8 @@ def lib():
         L.or_placement_search.argtypes = [C.POINTER(C.c_int64), C.c_int, f64p, C.c_int, C.c_int,
                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.or_solve_many.restype = None
-        L.or_solve_many.argtypes = [vp, C.c_int, f64p, C.POINTER(C.c_uint64), i64, i64, i64, vp, C.c_int]
+        L.or_solve_many.argtypes = [vp, C.c_int, f64p, C.POINTER(C.c_uint64), i64, i64, i64, vp, C.c_int,
+                                    C.c_uint32]
         L.or_frontier.restype = i64
         L.or_frontier.argtypes = [vp, C.POINTER(C.c_uint64), vp, i64, C.c_int, f64p,
                                   C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
@@ -111,7 +112,7 @@ class OracleProblem:
         lib().or_enumerate(self.ref, m, keys.ctypes.data_as(C.POINTER(C.c_uint64)), n)
         return keys[:n]
 
-    def solve(self, m, phase_code, keys, first=0, stride=1, tables=None, threads=0):
+    def solve(self, m, phase_code, keys, first=0, stride=1, tables=None, threads=0, smask=0):
         from paper_2605_04357_b200._native import RECORD_DTYPE
         if tables is None:
             tables = self.tables(m, phase_code)
@@ -120,7 +121,7 @@ class OracleProblem:
         recs = np.zeros(max(len(keys), 1), dtype=RECORD_DTYPE)
         lib().or_solve_many(self.ref, m, tables.ctypes.data_as(C.POINTER(C.c_double)),
                             keys.ctypes.data_as(C.POINTER(C.c_uint64)), len(keys), first, stride,
-                            recs.ctypes.data_as(C.c_void_p), threads)
+                            recs.ctypes.data_as(C.c_void_p), threads, smask)
         return recs[:len(keys)]
 
     def frontier(self, keys, recs, prices):

@@ -93,7 +93,7 @@ def load():
             "coral_s1_num_combos": (C.c_int, [vp, _i64p]),
             "coral_s1_get_combos": (C.c_int, [vp, C.c_int, C.c_int, _u64p, C.c_int64]),
             "coral_s1_evaluate": (C.c_int, [vp, C.c_int64, C.c_int64]),
-            "coral_s1_evaluate_shard": (C.c_int, [vp, C.c_int, C.c_int]),
+            "coral_s1_evaluate_units": (C.c_int, [vp, C.POINTER(C.c_uint32)]),
             "coral_s1_num_candidates": (C.c_int, [vp, _i64p]),
             "coral_s1_get_records": (C.c_int, [vp, C.c_int, vp, C.c_int64]),
             "coral_s1_frontier": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
@@ -242,8 +242,9 @@ class Handle:
     def evaluate(self, lo: int = 0, hi: int = -1):
         _check(self._lib.coral_s1_evaluate(self._h, lo, hi))
 
-    def evaluate_shard(self, rank: int, world: int):
-        _check(self._lib.coral_s1_evaluate_shard(self._h, rank, world))
+    def evaluate_units(self, smask):
+        m = np.ascontiguousarray(smask, dtype=np.uint32)
+        _check(self._lib.coral_s1_evaluate_units(self._h, m.ctypes.data_as(C.POINTER(C.c_uint32))))
 
     def num_candidates(self) -> int:
         n = C.c_int64()

@@ -1364,29 +1364,14 @@ int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi) {
   return 0;
 }
 
-// Multi-GPU shard: (model, phase, S) units, longest-processing-time assignment on a
-// deterministic cost estimate; every rank computes the same assignment.
-int coral_s1_evaluate_shard(coral_s1_handle* h, int rank, int world) {
+// Evaluate the (model, phase, S) units given as one S bit-mask per mp (bit S set =
+// evaluate stage count S). Multi-GPU ranks pass disjoint masks (paper_2605_04357_b200/
+// shard.py assigns them); records then hold each candidate's best over its S subset.
+int coral_s1_evaluate_units(coral_s1_handle* h, const uint32_t* smask) {
   if (!h || !h->have_enum) return fail(CORAL_S1_EINVAL, "enumerate first");
-  if (world < 1 || rank < 0 || rank >= world) return fail(CORAL_S1_EINVAL, "bad rank/world");
-  struct Unit { double cost; int mp, S; };
-  std::vector<Unit> units;
-  for (int mp = 0; mp < h->NM * h->NP; ++mp) {
-    const int m = mp / h->NP;
-    for (int S = 1; S <= std::min(h->smax[m], h->Lu[m]); ++S)
-      units.push_back({(double)h->counts[m] * (1.0 + (S - 1) * (double)h->Lu[m] / 8.0), mp, S});
-  }
-  std::stable_sort(units.begin(), units.end(), [](const Unit& a, const Unit& b) { return a.cost > b.cost; });
-  std::vector<double> load(world, 0.0);
-  std::vector<char> mine(units.size(), 0);
-  std::vector<std::vector<char>> owner((size_t)h->NM * h->NP, std::vector<char>(CORAL_S1_MAX_NODES + 1, 0));
-  for (size_t i = 0; i < units.size(); ++i) {
-    int best = 0;
-    for (int r = 1; r < world; ++r) if (load[r] < load[best]) best = r;
-    load[best] += units[i].cost;
-    if (best == rank) owner[units[i].mp][units[i].S] = 1;
-  }
-  return evaluate_units(h, [&](int mp, int S) { return owner[mp][S] != 0; });
+  if (!smask) return fail(CORAL_S1_EINVAL, "null mask");
+  std::vector<uint32_t> mk(smask, smask + (size_t)h->NM * h->NP);
+  return evaluate_units(h, [&](int mp, int S) { return ((mk[mp] >> S) & 1u) != 0; });
 }
 
 int coral_s1_get_records(coral_s1_handle* h, int mp, coral_s1_record* out, int64_t n) {

@@ -23,7 +23,8 @@ import numpy as np
 
 from . import _native
 from .library import GenContext, Stage1Problem, TemplateLibrary, decode_key, library_meta
-from .specs import PHASES, NodeComboKey
+from .shard import assign_units
+from .specs import PHASES, NodeComboKey, Placement, ServingTemplate
 
 
 @dataclass
@@ -130,7 +131,9 @@ def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,
         prob.cand_off = np.zeros(len(prob.models) * NP + 1, dtype=np.int64)
         for mp in range(len(prob.models) * NP):
             prob.cand_off[mp + 1] = prob.cand_off[mp] + prob.counts[mp // NP]
-        prob.h.evaluate_shard(tdist.get_rank(), tdist.get_world_size())
+        _, lsteps, smax = prob.h.table_layout()
+        masks = assign_units(prob.counts, lsteps, smax, NP, tdist.get_world_size())
+        prob.h.evaluate_units(masks[tdist.get_rank()])
         n_local = prob.h.frontier(pmat)
         n = _merge_across_ranks(prob, n_local, tdist)
     else:
@@ -147,17 +150,37 @@ def materialise(prob: Stage1Problem, items: np.ndarray, region_names, meta) -> T
     cbr = prob.cfg_by_rank
     cache = {}
     segments = {}
-    for it in items:
-        mp = int(it["mp"])
-        key = int(it["combo_key"])
+    mps = items["mp"].tolist()
+    keys = items["combo_key"].tolist()
+    regs = items["region"].tolist()
+    prices = items["price_usd_h"].tolist()
+    rec = items["rec"]
+    tps = rec["throughput_tps"].tolist()
+    nst = rec["num_stages"].tolist()
+    nn = rec["num_nodes"].tolist()
+    lps = rec["layers_per_stage"].tolist()
+    son = rec["stage_of_node"].tolist()
+    models, phases, slos = prob.models, prob.phases, prob.slos
+    for i in range(len(mps)):
+        mp, key = mps[i], keys[i]
         t = cache.get((mp, key))
         if t is None:
             combo = object.__new__(NodeComboKey)
             combo.__dict__["items"] = tuple((cbr[r], n) for r, n in decode_key(key))
-            t = prob.make_template(prob.models[mp // NP], prob.phases[mp % NP], combo, it["rec"])
+            model = models[mp // NP]
+            S = nst[i]
+            pl = object.__new__(Placement)
+            pl.__dict__.update(num_stages=S, layers_per_stage=tuple(lps[i][:S]),
+                               stage_of_node=tuple(son[i][:nn[i]]))
+            t = object.__new__(ServingTemplate)
+            t.__dict__.update(model=model.name, phase=phases[mp % NP], slo=slos[model.name],
+                              combo=combo, placement=pl, throughput_tps=tps[i])
             cache[(mp, key)] = t
-        seg = (t.model, t.phase, region_names[int(it["region"])])
-        segments.setdefault(seg, []).append(FrontierEntry(t, float(it["price_usd_h"])))
+        seg = (t.model, t.phase, region_names[regs[i]])
+        entries = segments.get(seg)
+        if entries is None:
+            entries = segments[seg] = []
+        entries.append(FrontierEntry(t, prices[i]))
     return TemplateFrontier(segments=segments, meta=meta,
                             num_candidates=int(prob.cand_off[-1]) if prob.cand_off is not None else 0)
 

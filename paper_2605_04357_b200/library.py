@@ -189,12 +189,19 @@ class Stage1Problem:
 
     # -- host materialisation -------------------------------------------------------
     def combo_objects(self, keys: np.ndarray) -> list:
+        """Packed keys -> NodeComboKey objects (token decode vectorised in numpy)."""
+        keys = np.asarray(keys, dtype=np.uint64)
+        shifts = np.array([9 * (_native.MAX_NODES - 1 - t) for t in range(_native.MAX_NODES)],
+                          dtype=np.uint64)
+        toks = ((keys[:, None] >> shifts[None, :]) & np.uint64(511)).astype(np.int64)
+        ranks = ((toks >> 3) - 1).tolist()
+        cnts = (toks & 7).tolist()
         cbr = self.cfg_by_rank
+        new = object.__new__
         out = []
-        for k in keys.tolist():
-            items = tuple((cbr[r], n) for r, n in decode_key(k))
-            obj = object.__new__(NodeComboKey)
-            obj.__dict__["items"] = items
+        for rk, ct in zip(ranks, cnts):
+            obj = new(NodeComboKey)
+            obj.__dict__["items"] = tuple((cbr[r], c) for r, c in zip(rk, ct) if c)
             out.append(obj)
         return out
 
@@ -213,23 +220,21 @@ class Stage1Problem:
     def library_entries(self):
         """All feasible templates in TemplateLibrary order (templates.py:340)."""
         NP = len(self.phases)
-        entries = []
-        missing = []
-        order = sorted(range(len(self.models) * NP),
-                       key=lambda mp: (self.models[mp // NP].name, self.phases[mp % NP]))
-        combos_cache = {}
-        for mp in range(len(self.models) * NP):
-            m = mp // NP
-            recs = self.records(mp)
-            if not np.any(recs["num_stages"] > 0):
-                missing.append((self.models[m].name, self.phases[mp % NP]))
+        nmp = len(self.models) * NP
+        recs_by_mp = [self.records(mp) for mp in range(nmp)]
+        missing = [(self.models[mp // NP].name, self.phases[mp % NP]) for mp in range(nmp)
+                   if not np.any(recs_by_mp[mp]["num_stages"] > 0)]
         if missing:
             raise LibraryGenError(f"no feasible template for: {sorted(missing)}")
+        order = sorted(range(nmp), key=lambda mp: (self.models[mp // NP].name, self.phases[mp % NP]))
+        combos_cache = {}
+        entries = []
+        new = object.__new__
         for mp in order:
             m, ph = mp // NP, self.phases[mp % NP]
             model = self.models[m]
             g = self.ctx.layer_granularity(model)
-            recs = self.records(mp)
+            recs = recs_by_mp[mp]
             feas = np.nonzero(recs["num_stages"] > 0)[0]
             if len(feas) and model.num_layers % g:
                 raise DomainError(f"stage layers sum to {(model.num_layers // g) * g}, "
@@ -237,8 +242,22 @@ class Stage1Problem:
             if m not in combos_cache:
                 combos_cache[m] = self.combo_objects(self.keys(m))
             combos = combos_cache[m]
-            for i in feas.tolist():
-                entries.append(self.make_template(model, ph, combos[i], recs[i]))
+            sub = recs[feas]
+            tps = sub["throughput_tps"].tolist()
+            nst = sub["num_stages"].tolist()
+            nn = sub["num_nodes"].tolist()
+            lps = sub["layers_per_stage"].tolist()
+            son = sub["stage_of_node"].tolist()
+            slo, name = self.slos[model.name], model.name
+            for k, i in enumerate(feas.tolist()):
+                S = nst[k]
+                pl = new(Placement)
+                pl.__dict__.update(num_stages=S, layers_per_stage=tuple(lps[k][:S]),
+                                   stage_of_node=tuple(son[k][:nn[k]]))
+                t = new(ServingTemplate)
+                t.__dict__.update(model=name, phase=ph, slo=slo, combo=combos[i], placement=pl,
+                                  throughput_tps=tps[k])
+                entries.append(t)
         return entries
 
 

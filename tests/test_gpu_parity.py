@@ -195,7 +195,7 @@ def test_random_scenarios_match_oracle(seed):
 
 
 def test_sharded_evaluation_and_merge_equal_single_gpu():
-    """Interleaved candidate shards + per-shard frontier + merge == full frontier
+    """(model, phase, S) unit shards + per-shard frontier + merge == full frontier
     (the multi-GPU protocol, emulated on one device)."""
     from paper_2605_04357_b200 import _native
     configs, models, slos, caps, ctx, regions, prices = workload("core")
@@ -205,10 +205,13 @@ def test_sharded_evaluation_and_merge_equal_single_gpu():
     n_full = prob.h.frontier(pm)
     full = prob.h.get_frontier(n_full)
     import torch
+    from paper_2605_04357_b200.shard import assign_units
     parts = []
     W = 3
+    _, lsteps, smax = prob.h.table_layout()
+    masks = assign_units(prob.counts, lsteps, smax, 2, W)
     for r in range(W):
-        prob.h.evaluate_shard(r, W)
+        prob.h.evaluate_units(masks[r])
         n = prob.h.frontier(pm)
         parts.append(prob.h.get_frontier(n))
     union = np.concatenate(parts)
