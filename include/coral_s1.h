@@ -192,6 +192,10 @@ int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t*
 int coral_s1_stage_ms(const coral_s1_handle* h, double* tables_ms, double* enumerate_ms,
                       double* evaluate_ms, double* frontier_ms);
 
+/* device time of the last evaluate's lattice kernels of one kind (0 top cells,
+ * 1 layers, 2 value tables): summed CUDA-event time of each launch on its stream */
+int coral_s1_kernel_stats(const coral_s1_handle* h, int kind, double* total_ms, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

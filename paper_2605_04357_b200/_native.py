@@ -103,6 +103,7 @@ def load():
             "coral_s1_placement_search": (C.c_int, [vp, C.c_int64, _i32p, _i64p, _i32p, _i64p,
                                                     _f64p, C.c_int64, _i32p, _f64p, _i64p, _i64p]),
             "coral_s1_stage_ms": (C.c_int, [vp, _f64p, _f64p, _f64p, _f64p]),
+            "coral_s1_kernel_stats": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -296,6 +297,12 @@ class Handle:
             _ptr(tput_off, C.c_int64), _ptr(tp, C.c_double), tput.size, _ptr(S, C.c_int32),
             _ptr(best, C.c_double), _ptr(sj, C.c_int64), _ptr(sc, C.c_int64)))
         return best, sj, sc
+
+    def kernel_stats(self, kind: int):
+        """(total ms, launches) of the last evaluate's lattice kernels: 0 top, 1 layer, 2 value."""
+        t, n = C.c_double(), C.c_int64()
+        _check(self._lib.coral_s1_kernel_stats(self._h, kind, C.byref(t), C.byref(n)))
+        return t.value, n.value
 
     def stage_ms(self) -> dict:
         vals = [C.c_double() for _ in range(4)]

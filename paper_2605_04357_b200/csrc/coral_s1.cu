@@ -112,6 +112,11 @@ struct coral_s1_handle {
   cudaEvent_t side_ev[kStreams] = {};
   cudaEvent_t fork_ev = nullptr;
   std::vector<unsigned char> flags_h;
+  // per-launch timing of the lattice kernels (coral_s1_kernel_stats)
+  static constexpr int kTimedMax = 512;
+  cudaEvent_t tev[kTimedMax][2] = {};
+  int tkind[kTimedMax] = {};
+  int ntimed = 0;
   cudaEvent_t ev[8] = {};
   float ms[4] = {0, 0, 0, 0};
 };
@@ -835,6 +840,10 @@ int coral_s1_create(int device, coral_s1_handle** out) {
     cudaEventCreateWithFlags(&h->side_ev[i], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
+  for (int i = 0; i < coral_s1_handle::kTimedMax; ++i) {
+    cudaEventCreate(&h->tev[i][0]);
+    cudaEventCreate(&h->tev[i][1]);
+  }
   if (const char* e = getenv("CORAL_S1_STREAMS")) h->nstreams = std::max(1, std::min(atoi(e), coral_s1_handle::kStreams));
   if (const char* e = getenv("CORAL_S1_TOP_PER_S")) h->top_per_S = atoi(e) != 0;
   if (h->lat_binom_d.ensure(sizeof(tab)) == 0)
@@ -864,6 +873,10 @@ int coral_s1_destroy(coral_s1_handle* h) {
     if (h->side_ev[i]) cudaEventDestroy(h->side_ev[i]);
   }
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
+  for (int i = 0; i < coral_s1_handle::kTimedMax; ++i) {
+    if (h->tev[i][0]) cudaEventDestroy(h->tev[i][0]);
+    if (h->tev[i][1]) cudaEventDestroy(h->tev[i][1]);
+  }
   for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
   delete h;
   return 0;
@@ -1164,6 +1177,19 @@ static int launch_percombo(coral_s1_handle* h, cudaStream_t st, int64_t lo, int6
   return 0;
 }
 
+// Bracket one launch on stream st with a timing-event pair of kind `kind`
+// (0 = lat_top_kernel, 1 = lat_layer_kernel, 2 = lat_value_kernel).
+static int timed_begin(coral_s1_handle* h, cudaStream_t st, int kind) {
+  if (h->ntimed >= coral_s1_handle::kTimedMax) return -1;
+  const int i = h->ntimed++;
+  h->tkind[i] = kind;
+  cudaEventRecord(h->tev[i][0], st);
+  return i;
+}
+static void timed_end(coral_s1_handle* h, cudaStream_t st, int i) {
+  if (i >= 0) cudaEventRecord(h->tev[i][1], st);
+}
+
 // State tables shared by all models (depend on K and n_max only) + per-model maxn.
 static int lattice_prepare(coral_s1_handle* h) {
   const int K = h->K, R = h->n_max - 1;
@@ -1258,16 +1284,20 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   const double* tab_mp = h->tab.as<double>() + h->tab_off[mp];
   if (Smax >= 2 && ns > 0) {
     const long long nv = ns * Lu;
+    const int ti = timed_begin(h, st, 2);
     lat_value_kernel<<<dim3((unsigned)((nv + 255) / 256), Smax - 1), 256, 0, st>>>(
         L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(), tab_mp, K, Lu, 2, smask, W);
+    timed_end(h, st, ti);
     LAUNCH_CHECK(h);
   }
   for (int sg = 2; sg <= Smax - 1; ++sg) {
     const long long nst = h->lat_base[h->n_max - 1 + 1] - h->lat_base[sg];
     if (nst <= 0) continue;
+    const int ti = timed_begin(h, st, 1);
     lat_layer_kernel<<<dim3((unsigned)((nst * 32 + 255) / 256), Smax - sg), 256, 0, st>>>(
         L, sg, sg + 1, smask, h->n_max, Lu, h->lat_maxn.as<unsigned>() + (size_t)m * ns,
         h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), W);
+    timed_end(h, st, ti);
     LAUNCH_CHECK(h);
   }
   TopArgs T;
@@ -1293,7 +1323,9 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
       LAUNCH_CHECK(h);
     }
   } else {
+    const int ti = timed_begin(h, st, 0);
     lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
+    timed_end(h, st, ti);
     LAUNCH_CHECK(h);
   }
   return 0;
@@ -1313,6 +1345,7 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
     CUDA_TRY(cudaMemcpyAsync(h->flags_h.data(), h->flags.p, (size_t)NMP * h->n_max * h->K,
                              cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaEventRecord(h->ev[4], st));
+  h->ntimed = 0;
   // records not improved by any unit read as infeasible (num_stages 0)
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), st));
   if ((rc = lattice_prepare(h))) return rc;
@@ -1528,6 +1561,23 @@ int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t*
   CUDA_TRY(cudaMemcpyAsync(stage_j, out + ob_sj, ncases * kMaxC * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(stage_counts, out + ob_sc, ncases * kMaxC * kMaxC * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int coral_s1_kernel_stats(const coral_s1_handle* h, int kind, double* total_ms, int64_t* launches) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  double tot = 0;
+  int64_t n = 0;
+  for (int i = 0; i < h->ntimed; ++i) {
+    if (h->tkind[i] != kind) continue;
+    float t = 0;
+    CUDA_TRY(cudaEventSynchronize(h->tev[i][1]));
+    CUDA_TRY(cudaEventElapsedTime(&t, h->tev[i][0], h->tev[i][1]));
+    tot += t;
+    ++n;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = n;
   return 0;
 }
 
