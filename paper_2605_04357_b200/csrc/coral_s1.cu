@@ -99,7 +99,7 @@ struct coral_s1_handle {
   DevBuf prob, tab, flags, budget, keys_raw, keys, keys_tmp, koff_d, nvalid, cand_off_d, rec, cub_tmp;
   DevBuf items, items_sorted, sort_a, sort_b, perm_a, perm_b, segk, scanv, flagsel, nsel, front,
       prices, enum_tmp;
-  DevBuf op_in, op_out, tab_off_d;
+  DevBuf op_in, op_out, tab_off_d, win;
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
   static constexpr int kStreams = 4;
   int nstreams = kStreams;  // side streams in use (CORAL_S1_STREAMS)
@@ -423,6 +423,7 @@ struct TopArgs {
   const long long* off;
   const uint2* subtab;
   coral_s1_record* rec;             // this (model, phase)'s records
+  int4* win;                        // per candidate: best value (lo, hi), S, u code << 10 | j
 };
 
 __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
@@ -485,31 +486,49 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
     }
     if (best > tbest && best > 1e-9) { tbest = best; twin = S; tcode = bu; tj = bj; }
   }
-  if (lane || !twin) return;
+  if (lane) return;
+  A.win[ci] = make_int4(__double2loint(tbest), __double2hiint(tbest), twin, (tcode << 10) | tj);
+}
+
+// Walk-back of each candidate's winning S (kernels.py:258-275) into its canonical
+// record (templates.py:209-228), one thread per candidate so that the dependent
+// table lookups of 32 candidates overlap. Applies better_S against the record.
+__global__ void __launch_bounds__(256) lat_decode_kernel(TopArgs A) {
+  const long long ci = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci >= A.ncombo) return;
+  const int4 w = A.win[ci];
+  const int twin = w.z;
+  if (!twin) return;
+  const double tbest = __hiloint2double(w.y, w.x);
   coral_s1_record r = A.rec[ci];
   if (!better_S(tbest, twin, record_best(r), r.num_stages)) return;
+  int cfg[kMaxC], cnt[kMaxC];
+  const int C = lat_tokens(A.inv_rank, A.keys[ci], cfg, cnt);
+  int n = 0;
+  for (int c = 0; c < C; ++c) n += cnt[c];
+  const int Lu = A.Lu, LuP = Lu + 1;
   int sj[kMaxC], sc[kMaxC][kMaxC];
   if (twin == 1) {
     sj[0] = Lu;
     for (int c = 0; c < C; ++c) sc[0][c] = cnt[c];
   } else {
-    // walk back (kernels.py:258-275): stage 0 is the top choice
+    const int tcode = w.w >> 10, tj = w.w & 1023;
     int e[kMaxC], rest = tcode;
     for (int c = 0; c < C; ++c) { sc[0][c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; e[c] = cnt[c] - sc[0][c]; }
     sj[0] = tj;
     int sr;
-    long long X = lat_rank_tokens(L, cfg, e, C, &sr);
+    long long X = lat_rank_tokens(A.L, cfg, e, C, &sr);
     int l = Lu - tj;
     for (int s = 1; s < twin; ++s) {
       const int sg = twin - s;
+      // independent loads first: state tokens, choice, sub-table offset
+      const unsigned long long xkey = A.state_key[X];
+      const unsigned short chv = sg > 1 ? A.W.chl(twin, sg)[X * LuP + l] : 0;
+      const long long xo = A.off[X];
       int xc[kMaxC], xn[kMaxC];
-      const int XC = lat_tokens(A.inv_rank, A.state_key[X], xc, xn);
+      const int XC = lat_tokens(A.inv_rank, xkey, xc, xn);
       int uc = -1, j = l;
-      if (sg > 1) {
-        const unsigned short chv = A.W.chl(twin, sg)[X * LuP + l];
-        uc = chv >> 10;
-        j = chv & 1023;
-      }
+      if (sg > 1) { uc = chv >> 10; j = chv & 1023; }
       int ud[kMaxC];
       if (uc < 0) { for (int t = 0; t < XC; ++t) ud[t] = xn[t]; }
       else {
@@ -521,7 +540,7 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
         for (int t = 0; t < XC; ++t) if (xc[t] == cfg[c]) sc[s][c] = ud[t];
       }
       sj[s] = j;
-      if (uc >= 0) X = A.subtab[A.off[X] + uc].y;
+      if (uc >= 0) X = A.subtab[xo + uc].y;
       l -= j;
     }
   }
@@ -863,7 +882,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
   DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->keys_tmp, &h->koff_d,
                     &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
                     &h->sort_a, &h->sort_b, &h->perm_a, &h->perm_b, &h->segk, &h->scanv,
-                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d,
+                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d, &h->win,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
                     &h->lat_sub, &h->lat_maxn, &h->lat_flags_h};
   for (DevBuf* b : bufs) b->release();
@@ -1315,17 +1334,24 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   T.off = h->lat_off.as<long long>();
   T.subtab = h->lat_sub.as<uint2>();
   T.rec = h->rec.as<coral_s1_record>() + h->cand_off[mp];
+  T.win = h->win.as<int4>() + h->cand_off[mp];
   if (h->top_per_S) {  // one launch per S: working set value_S + f_S[S-1] stays in L2
     for (int S = 1; S <= Smax; ++S) {
       if (!((smask >> S) & 1u)) continue;
       T.smask = 1u << S;
       lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
       LAUNCH_CHECK(h);
+      lat_decode_kernel<<<(unsigned)((ncombo + 255) / 256), 256, 0, st>>>(T);
+      LAUNCH_CHECK(h);
     }
   } else {
     const int ti = timed_begin(h, st, 0);
     lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
     timed_end(h, st, ti);
+    LAUNCH_CHECK(h);
+    const int td = timed_begin(h, st, 3);
+    lat_decode_kernel<<<(unsigned)((ncombo + 255) / 256), 256, 0, st>>>(T);
+    timed_end(h, st, td);
     LAUNCH_CHECK(h);
   }
   return 0;
@@ -1337,7 +1363,9 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   if (!h || !h->have_tables || !h->have_enum) return fail(CORAL_S1_EINVAL, "tables and enumerate first");
   CUDA_TRY(cudaSetDevice(h->device));
   int rc;
-  if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record)))) return rc;
+  if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record))) ||
+      (rc = h->win.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(int4))))
+    return rc;
   cudaStream_t st = h->stream;
   const int NMP = h->NM * h->NP;
   h->flags_h.assign((size_t)std::max(NMP, 1) * h->n_max * h->K, 0);
