@@ -416,6 +416,7 @@ struct TopArgs {
   const unsigned long long* keys;   // this model's combos (library order)
   long long ncombo;
   unsigned smask;                   // S values of this chain
+  unsigned xmask;                   // S values whose rows are exactly monotone
   int K, Lu, g;
   const double* tab_mp;             // [S][K][Lu]
   LatWork W;
@@ -471,8 +472,10 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
     const double* lay = A.W.lay(S, S - 1);
     double best = kNegInf;
     int bu = 1 << 20, bj = 0;
+    // S == 2 reads value rows on both sides: symmetric, search the lower half only
+    const int chalf = (S == 2 && ((A.xmask >> 2) & 1u)) ? (M - 1) / 2 : M;
     for (int k = 0; k < 2; ++k) {
-      if (su[k] > n - (S - 1)) continue;
+      if (su[k] > n - (S - 1) || lane + 1 + 32 * k > chalf) continue;
       double cand;
       int cj;
       dp_pair(val + ru[k] * LuP, lay + rr[k] * LuP, Lu, Lu - (S - 1), true, cand, cj);
@@ -1280,7 +1283,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   const long long ncombo = h->counts[m];
   if (!ncombo) return 0;
   LatModel L{K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
-  unsigned smask = 0;
+  unsigned smask = 0, xmask = 0;
   int Smax = 0;
   for (int S : Ss) {
     bool mono = true;  // kernels.py:291 over every config row at (mp, S)
@@ -1292,6 +1295,9 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
     }
     smask |= 1u << S;
     Smax = std::max(Smax, S);
+    bool exact = true;  // bit 1 of the row flags: all diffs <= 0
+    for (int c = 0; c < K; ++c) exact &= (h->flags_h[((size_t)mp * h->n_max + (S - 1)) * K + c] & 2) != 0;
+    if (exact) xmask |= 1u << S;
   }
   if (!smask) return 0;
   LatWork W;
@@ -1314,7 +1320,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
     if (nst <= 0) continue;
     const int ti = timed_begin(h, st, 1);
     lat_layer_kernel<<<dim3((unsigned)((nst * 32 + 255) / 256), Smax - sg), 256, 0, st>>>(
-        L, sg, sg + 1, smask, h->n_max, Lu, h->lat_maxn.as<unsigned>() + (size_t)m * ns,
+        L, sg, sg + 1, smask, xmask, h->n_max, Lu, h->lat_maxn.as<unsigned>() + (size_t)m * ns,
         h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), W);
     timed_end(h, st, ti);
     LAUNCH_CHECK(h);
@@ -1325,6 +1331,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   T.keys = h->keys.as<unsigned long long>() + h->koff[m];
   T.ncombo = ncombo;
   T.smask = smask;
+  T.xmask = xmask;
   T.K = K;
   T.Lu = Lu;
   T.g = h->g[m];

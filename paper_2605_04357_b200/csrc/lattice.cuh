@@ -203,8 +203,9 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
 // DP layer sg for every S in [S_lo, S_lo + gridDim.y) with S > sg: warp per state X,
 // lanes over l. Cells: sg <= |X| <= maxn(X) - (S - sg), sg <= l <= Lu - (S - sg).
 __global__ void __launch_bounds__(256) lat_layer_kernel(
-    LatModel L, int sg, int S_lo, unsigned smask, int n_max, int Lu, const unsigned* __restrict__ maxn,
-    const long long* __restrict__ off, const uint2* __restrict__ subtab, LatWork W) {
+    LatModel L, int sg, int S_lo, unsigned smask, unsigned xmask, int n_max, int Lu,
+    const unsigned* __restrict__ maxn, const long long* __restrict__ off,
+    const uint2* __restrict__ subtab, LatWork W) {
   const int S = S_lo + blockIdx.y;
   if (!((smask >> S) & 1u) || S <= sg) return;
   const int lane = threadIdx.x & 31;
@@ -219,6 +220,10 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
   const int usz = s - (sg - 1);  // |u| <= |X| - (sg - 1)
   const long long o = off[idx];
   const long long M = off[idx + 1] - o;
+  // Layer 2 reads value rows on both sides: with exactly monotone rows the crossing
+  // is the true max, so cand(u) == cand(X-u) (j <-> l-j); the smallest maximising
+  // code lies in the lower half (code(X-u) = M-1-code(u)) and only it is searched.
+  const long long cmax = (sg == 2 && ((xmask >> S) & 1u)) ? (M - 1) / 2 + 1 : M;
   const double* __restrict__ value = W.val(S);
   const double* __restrict__ fprev = W.lay(S, sg - 1);
   double* __restrict__ fout = W.lay(S, sg);
@@ -229,7 +234,7 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
     const int jmax = l - (sg - 1);
     double best = kNegInf;
     int bu = 0, bj = 0;
-    for (int code = 1; code < M; ++code) {
+    for (int code = 1; code < cmax; ++code) {
       const uint2 e = subtab[o + code];
       if ((int)(e.x >> 24) > usz) continue;
       if (!act) continue;
