@@ -99,7 +99,7 @@ struct coral_s1_handle {
   DevBuf prob, tab, flags, budget, keys_raw, keys, keys_tmp, koff_d, nvalid, cand_off_d, rec, cub_tmp;
   DevBuf items, items_sorted, sort_a, sort_b, perm_a, perm_b, segk, scanv, flagsel, nsel, front,
       prices, enum_tmp;
-  DevBuf op_in, op_out, tab_off_d, win;
+  DevBuf op_in, op_out, tab_off_d, win, fbucket;
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
   static constexpr int kStreams = 4;
   int nstreams = kStreams;  // side streams in use (CORAL_S1_STREAMS)
@@ -638,50 +638,108 @@ struct FrontArgs {
   unsigned long long* nitems;
 };
 
-// allocation.py:91-98 _template_price, per (candidate, region)
-__global__ void frontier_items_kernel(FrontArgs A) {
+// allocation.py:91-98 _template_price of candidate ci in region r; false when the
+// candidate has no template or a config is not offered (price None).
+__device__ __forceinline__ bool frontier_item(const FrontArgs& A, int64_t ci, int r,
+                                              coral_s1_frontier_item* it) {
+  if (ci >= A.ncand) return false;
+  const coral_s1_record rc = A.rec[ci];
+  if (rc.num_stages == 0) return false;
+  int lo = 0, hi = A.NMP;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (A.cand_off[mid] <= ci) lo = mid; else hi = mid;
+  }
+  const int m = lo / A.P.NP;
+  const unsigned long long key = A.keys[A.koff[m] + (ci - A.cand_off[lo])];
+  int cfg[kMaxC], cnt[kMaxC];
+  const int C = decode_key(A.P, key, cfg, cnt);
+  double total = 0.0;
+  for (int c = 0; c < C; ++c) {
+    const double p = A.prices[(int64_t)r * A.P.K + cfg[c]];
+    if (isnan(p)) return false;
+    total = rn_add(total, rn_mul((double)cnt[c], p));
+  }
+  it->price_usd_h = total;
+  it->throughput_tps = rc.throughput_tps;
+  it->combo_key = key;
+  it->mp = lo;
+  it->region = r;
+  it->rec = rc;
+  return true;
+}
+
+__device__ __forceinline__ unsigned long long dbits(double x) {
+  return (unsigned long long)__double_as_longlong(x);  // monotone for x >= 0
+}
+
+// Exact prefilter, pass 1: the price range (bit patterns) over all items.
+__global__ void frontier_range_kernel(FrontArgs A, unsigned long long* __restrict__ range) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t ci = t / A.R;
-  const int r = (int)(t - ci * A.R);
-  bool keep = false;
   coral_s1_frontier_item it;
-  if (ci < A.ncand) {
-    const coral_s1_record rc = A.rec[ci];
-    if (rc.num_stages > 0) {
-      int lo = 0, hi = A.NMP;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (A.cand_off[mid] <= ci) lo = mid; else hi = mid;
-      }
-      const int m = lo / A.P.NP;
-      const unsigned long long key = A.keys[A.koff[m] + (ci - A.cand_off[lo])];
-      int cfg[kMaxC], cnt[kMaxC];
-      const int C = decode_key(A.P, key, cfg, cnt);
-      double total = 0.0;
-      bool priced = true;
-      for (int c = 0; c < C; ++c) {
-        const double p = A.prices[(int64_t)r * A.P.K + cfg[c]];
-        if (isnan(p)) { priced = false; break; }
-        total = rn_add(total, rn_mul((double)cnt[c], p));
-      }
-      if (priced) {
-        keep = true;
-        it.price_usd_h = total;
-        it.throughput_tps = rc.throughput_tps;
-        it.combo_key = key;
-        it.mp = lo;
-        it.region = r;
-        it.rec = rc;
-      }
-    }
+  const bool ok = frontier_item(A, t / A.R, (int)(t % A.R), &it);
+  unsigned long long lo = ok ? dbits(it.price_usd_h) : ~0ull, hi = ok ? dbits(it.price_usd_h) : 0ull;
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0 && hi) {
+    atomicMin(range, lo);
+    atomicMax(range + 1, hi);
+  }
+}
+
+// pass 2: per (segment, price bucket) the max throughput (bit pattern, T > 0)
+__global__ void frontier_bucket_kernel(FrontArgs A, int shift, unsigned long long base, int nb,
+                                       unsigned long long* __restrict__ bmax) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  coral_s1_frontier_item it;
+  if (!frontier_item(A, t / A.R, (int)(t % A.R), &it)) return;
+  const int b = (int)((dbits(it.price_usd_h) >> shift) - base);
+  unsigned long long* slot = bmax + ((int64_t)it.mp * A.R + it.region) * nb + b;
+  const unsigned long long tb = dbits(it.throughput_tps);
+  if (*slot < tb) atomicMax(slot, tb);
+}
+
+// pass 3: exclusive prefix max over the buckets of each segment (block per segment)
+__global__ void frontier_prefix_kernel(int nb, unsigned long long* __restrict__ bmax) {
+  typedef cub::BlockScan<unsigned long long, 256> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  unsigned long long* row = bmax + (int64_t)blockIdx.x * nb;
+  const int per = (nb + 255) / 256;
+  const int b0 = threadIdx.x * per;
+  unsigned long long local = 0;
+  for (int b = b0; b < min(b0 + per, nb); ++b) local = max(local, row[b]);
+  unsigned long long excl;
+  Scan(tmp).ExclusiveScan(local, excl, 0ull, cub::Max());
+  __syncthreads();
+  unsigned long long run = excl;
+  for (int b = b0; b < min(b0 + per, nb); ++b) {
+    const unsigned long long v = row[b];
+    row[b] = run;  // max over strictly cheaper buckets
+    run = max(run, v);
+  }
+}
+
+// pass 4: write the items that can still be on the frontier: T must exceed every
+// throughput of a strictly cheaper bucket, else a cheaper candidate dominates it
+// (SURVEY.md 8c keep rule: T > running max of the earlier items).
+__global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long base, int nb,
+                                      const unsigned long long* __restrict__ pmax) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  coral_s1_frontier_item it;
+  bool keep = frontier_item(A, t / A.R, (int)(t % A.R), &it);
+  if (keep && nb > 0) {
+    const int b = (int)((dbits(it.price_usd_h) >> shift) - base);
+    keep = dbits(it.throughput_tps) > pmax[((int64_t)it.mp * A.R + it.region) * nb + b];
   }
   const unsigned ballot = __ballot_sync(0xffffffffu, keep);
   if (!ballot) return;
   const int lane = threadIdx.x & 31;
-  unsigned long long base = 0;
-  if (lane == __ffs(ballot) - 1) base = atomicAdd(A.nitems, (unsigned long long)__popc(ballot));
-  base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
-  if (keep) A.items[base + __popc(ballot & ((1u << lane) - 1u))] = it;
+  unsigned long long pos = 0;
+  if (lane == __ffs(ballot) - 1) pos = atomicAdd(A.nitems, (unsigned long long)__popc(ballot));
+  pos = __shfl_sync(0xffffffffu, pos, __ffs(ballot) - 1);
+  if (keep) A.items[pos + __popc(ballot & ((1u << lane) - 1u))] = it;
 }
 
 // sort-key extraction for the 4 stable LSD passes
@@ -744,7 +802,7 @@ int frontier_from_items(coral_s1_handle* h, int64_t n, int R) {
       (rc = h->perm_a.ensure(n * 4)) || (rc = h->perm_b.ensure(n * 4)) ||
       (rc = h->items_sorted.ensure(n * sizeof(coral_s1_frontier_item))) ||
       (rc = h->segk.ensure(n * 8)) || (rc = h->scanv.ensure(n * 8)) ||
-      (rc = h->flagsel.ensure(n)) || (rc = h->nsel.ensure(16)))
+      (rc = h->flagsel.ensure(n)) || (rc = h->nsel.ensure(32)))
     return rc;
   const int TB = 256;
   const unsigned gb = (unsigned)((n + TB - 1) / TB);
@@ -885,7 +943,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
   DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->keys_tmp, &h->koff_d,
                     &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
                     &h->sort_a, &h->sort_b, &h->perm_a, &h->perm_b, &h->segk, &h->scanv,
-                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d, &h->win,
+                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
                     &h->lat_sub, &h->lat_maxn, &h->lat_flags_h};
   for (DevBuf* b : bufs) b->release();
@@ -1466,7 +1524,7 @@ int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices,
   std::vector<double> pv(prices, prices + (size_t)num_regions * h->K);
   if ((rc = upload(h, h->prices, pv)) ||
       (rc = h->items.ensure(std::max<int64_t>(nmax, 1) * sizeof(coral_s1_frontier_item))) ||
-      (rc = h->nsel.ensure(16)))
+      (rc = h->nsel.ensure(32)))
     return rc;
   int64_t n = 0;
   if (nmax > 0) {
@@ -1483,7 +1541,30 @@ int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices,
     A.R = num_regions;
     A.items = h->items.as<coral_s1_frontier_item>();
     A.nitems = h->nsel.as<unsigned long long>();
-    frontier_items_kernel<<<(unsigned)((nmax + 255) / 256), 256, 0, st>>>(A);
+    // exact prefilter: range -> per (segment, price bucket) max T -> prefix max
+    const unsigned gb = (unsigned)((nmax + 255) / 256);
+    unsigned long long init[2] = {~0ull, 0ull}, range[2];
+    CUDA_TRY(cudaMemcpyAsync(h->nsel.as<unsigned long long>() + 1, init, 16, cudaMemcpyHostToDevice, st));
+    frontier_range_kernel<<<gb, 256, 0, st>>>(A, h->nsel.as<unsigned long long>() + 1);
+    LAUNCH_CHECK(h);
+    CUDA_TRY(cudaMemcpyAsync(range, h->nsel.as<unsigned long long>() + 1, 16, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int shift = 0, nb = 0;
+    unsigned long long base = 0;
+    const int64_t nseg = (int64_t)h->NM * h->NP * num_regions;
+    if (range[1] >= range[0] && range[1]) {
+      shift = 40;  // 11 exponent + 12 mantissa bits; coarser until <= 4096 buckets
+      while (((range[1] >> shift) - (range[0] >> shift)) + 1 > 4096) ++shift;
+      base = range[0] >> shift;
+      nb = (int)(((range[1] >> shift) - base) + 1);
+      if ((rc = h->fbucket.ensure(std::max<int64_t>(nseg * nb, 1) * 8))) return rc;
+      CUDA_TRY(cudaMemsetAsync(h->fbucket.p, 0, nseg * nb * 8, st));
+      frontier_bucket_kernel<<<gb, 256, 0, st>>>(A, shift, base, nb, h->fbucket.as<unsigned long long>());
+      LAUNCH_CHECK(h);
+      frontier_prefix_kernel<<<(unsigned)nseg, 256, 0, st>>>(nb, h->fbucket.as<unsigned long long>());
+      LAUNCH_CHECK(h);
+    }
+    frontier_items_kernel<<<gb, 256, 0, st>>>(A, shift, base, nb, h->fbucket.as<unsigned long long>());
     LAUNCH_CHECK(h);
     unsigned long long ni = 0;
     CUDA_TRY(cudaMemcpyAsync(&ni, h->nsel.p, 8, cudaMemcpyDeviceToHost, st));
