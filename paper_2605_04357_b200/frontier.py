@@ -22,19 +22,30 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
-from .library import GenContext, Stage1Problem, TemplateLibrary, decode_key, library_meta
+from .library import GenContext, Stage1Problem, TemplateLibrary, library_meta
 from .shard import assign_units
-from .specs import PHASES, NodeComboKey, Placement, ServingTemplate
+from .specs import PHASES, Placement, ServingTemplate
 
 
-@dataclass
 class FrontierEntry:
-    template: object      # ServingTemplate
-    price_usd_h: float    # one instance in this region
+    """One survivor: the template and its one-instance price in the segment's region."""
+
+    __slots__ = ("template", "price_usd_h")
+
+    def __init__(self, template, price_usd_h: float):
+        self.template = template
+        self.price_usd_h = price_usd_h
 
     @property
     def throughput_tps(self) -> float:
         return self.template.throughput_tps
+
+    def __eq__(self, other):
+        return (isinstance(other, FrontierEntry) and self.template == other.template
+                and self.price_usd_h == other.price_usd_h)
+
+    def __repr__(self):
+        return f"FrontierEntry({self.template.template_id!r}, {self.price_usd_h!r})"
 
 
 @dataclass
@@ -147,11 +158,12 @@ def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,
 def materialise(prob: Stage1Problem, items: np.ndarray, region_names, meta) -> TemplateFrontier:
     """Survivor records -> ServingTemplate objects (one object per (mp, combo))."""
     NP = len(prob.phases)
-    cbr = prob.cfg_by_rank
     cache = {}
     segments = {}
     mps = items["mp"].tolist()
-    keys = items["combo_key"].tolist()
+    keys = items["combo_key"]
+    combos = prob.combo_objects(keys) if len(items) else []
+    keys = keys.tolist()
     regs = items["region"].tolist()
     prices = items["price_usd_h"].tolist()
     rec = items["rec"]
@@ -161,20 +173,19 @@ def materialise(prob: Stage1Problem, items: np.ndarray, region_names, meta) -> T
     lps = rec["layers_per_stage"].tolist()
     son = rec["stage_of_node"].tolist()
     models, phases, slos = prob.models, prob.phases, prob.slos
+    new = object.__new__
     for i in range(len(mps)):
         mp, key = mps[i], keys[i]
         t = cache.get((mp, key))
         if t is None:
-            combo = object.__new__(NodeComboKey)
-            combo.__dict__["items"] = tuple((cbr[r], n) for r, n in decode_key(key))
             model = models[mp // NP]
             S = nst[i]
-            pl = object.__new__(Placement)
+            pl = new(Placement)
             pl.__dict__.update(num_stages=S, layers_per_stage=tuple(lps[i][:S]),
                                stage_of_node=tuple(son[i][:nn[i]]))
-            t = object.__new__(ServingTemplate)
+            t = new(ServingTemplate)
             t.__dict__.update(model=model.name, phase=phases[mp % NP], slo=slos[model.name],
-                              combo=combo, placement=pl, throughput_tps=tps[i])
+                              combo=combos[i], placement=pl, throughput_tps=tps[i])
             cache[(mp, key)] = t
         seg = (t.model, t.phase, region_names[regs[i]])
         entries = segments.get(seg)

@@ -242,6 +242,8 @@ def main():
     ext_pkl = argv[argv.index("--extended-pkl") + 1] if "--extended-pkl" in argv else None
     if "--only-extended" in argv:
         return extended(ext_pkl)
+    if "--c3-pkl" in argv:
+        return big_library("c3", argv[argv.index("--c3-pkl") + 1])
     dump("kernels.json.gz", kernel_cases())
     dump("perf_grid.json.gz", perf_grid())
     dump("profile.json.gz", profile_case())
@@ -258,6 +260,15 @@ def main():
         dump(f"frontier_{w}.json.gz", frontier_oracle(recs, prices, [r.name for r in regions]))
     if ext_pkl:
         extended(ext_pkl)
+
+
+def big_library(name, pkl):
+    with open(pkl, "rb") as fh:
+        data = pickle.load(fh)
+    recs = data["records"]
+    configs, models, slos, caps, ctx, regions, prices = scenario_inputs(name)
+    dump(f"library_{name}.json.gz", library_fixture(name, recs, False, data["wall_s"]))
+    dump(f"frontier_{name}.json.gz", frontier_oracle(recs, prices, [r.name for r in regions]))
 
 
 def extended(ext_pkl):

@@ -93,14 +93,16 @@ def test_build_library_golden_bit_exact(w):
     assert {f"{k[0]}|{k[1]}": v for k, v in lib.counts_by_model_phase().items()} == g["counts"]
 
 
-def test_build_library_extended_golden():
-    """Full BASELINE config 2: 1,084,362 templates, every record bit-identical
+@pytest.mark.parametrize("w", ["extended", "c3"])
+def test_build_library_big_golden(w):
+    """Full BASELINE config 2 (1,084,362 templates) and config 3 (llama3-70b at
+    granularity 1, Lu = 80: 344,548 templates): every record bit-identical
     (sha256 over canonical lines incl. repr(throughput))."""
     try:
-        g = golden("library_extended.json.gz")
+        g = golden(f"library_{w}.json.gz")
     except FileNotFoundError:
-        pytest.skip("extended golden not generated")
-    configs, models, slos, caps, ctx, regions, prices = workload("extended")
+        pytest.skip(f"{w} golden not generated")
+    configs, models, slos, caps, ctx, regions, prices = workload(w)
     prob = Stage1Problem(configs, models, slos, caps, ctx).run()
     cbr = prob.cfg_by_rank
     NP = 2
@@ -136,7 +138,7 @@ def test_profile_override_library():
     assert [template_line(t) for t in lib.entries] == g["library"]["records"]
 
 
-@pytest.mark.parametrize("w", ["c1", "core", "extended"])
+@pytest.mark.parametrize("w", ["c1", "core", "extended", "c3"])
 def test_frontier_golden(w):
     try:
         g = golden(f"frontier_{w}.json.gz")
