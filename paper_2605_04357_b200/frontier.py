@@ -17,6 +17,7 @@ ranks and the per-rank frontiers are merged after ONE NCCL all-gather.
 
 from __future__ import annotations
 
+from collections import namedtuple
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -27,25 +28,14 @@ from .shard import assign_units
 from .specs import PHASES, Placement, ServingTemplate
 
 
-class FrontierEntry:
-    """One survivor: the template and its one-instance price in the segment's region."""
+class FrontierEntry(namedtuple("FrontierEntry", ("template", "price_usd_h"))):
+    """One survivor: the template and its one-instance price (USD/h) in the segment's region."""
 
-    __slots__ = ("template", "price_usd_h")
-
-    def __init__(self, template, price_usd_h: float):
-        self.template = template
-        self.price_usd_h = price_usd_h
+    __slots__ = ()
 
     @property
     def throughput_tps(self) -> float:
         return self.template.throughput_tps
-
-    def __eq__(self, other):
-        return (isinstance(other, FrontierEntry) and self.template == other.template
-                and self.price_usd_h == other.price_usd_h)
-
-    def __repr__(self):
-        return f"FrontierEntry({self.template.template_id!r}, {self.price_usd_h!r})"
 
 
 @dataclass
@@ -161,9 +151,13 @@ def materialise(prob: Stage1Problem, items: np.ndarray, region_names, meta) -> T
     cache = {}
     segments = {}
     mps = items["mp"].tolist()
-    keys = items["combo_key"]
-    combos = prob.combo_objects(keys) if len(items) else []
-    keys = keys.tolist()
+    keys = items["combo_key"].tolist()
+    first = {}
+    for i, mk in enumerate(zip(mps, keys)):
+        first.setdefault(mk, i)
+    uniq = list(first.values())
+    objs = prob.combo_objects(items["combo_key"][uniq]) if uniq else []
+    combo_of = dict(zip(first.keys(), objs))
     regs = items["region"].tolist()
     prices = items["price_usd_h"].tolist()
     rec = items["rec"]
@@ -185,7 +179,7 @@ def materialise(prob: Stage1Problem, items: np.ndarray, region_names, meta) -> T
                                stage_of_node=tuple(son[i][:nn[i]]))
             t = new(ServingTemplate)
             t.__dict__.update(model=model.name, phase=phases[mp % NP], slo=slos[model.name],
-                              combo=combos[i], placement=pl, throughput_tps=tps[i])
+                              combo=combo_of[(mp, key)], placement=pl, throughput_tps=tps[i])
             cache[(mp, key)] = t
         seg = (t.model, t.phase, region_names[regs[i]])
         entries = segments.get(seg)
