@@ -276,6 +276,12 @@ def main():
     total_ms = float(t.item())
     value = ncand * args.steps / (total_ms / 1e3)
     stages = h.stage_ms()
+    rank_eval = [stages["evaluate"]]
+    if world > 1:  # per-rank evaluate time of the last step (load balance of the unit split)
+        ev = torch.tensor([stages["evaluate"]], dtype=torch.float64, device="cuda")
+        allv = torch.empty(world, dtype=torch.float64, device="cuda")
+        tdist.all_gather_into_tensor(allv, ev)
+        rank_eval = allv.tolist()
 
     # e2e: the public API, host spec objects in -> frontier ServingTemplates out
     e2e_times = []
@@ -327,6 +333,7 @@ def main():
                    "l2": "256 MB buffer written between timed steps",
                    "stage1_solve_s": total_ms / args.steps / 1e3},
         "stage_ms": stages,
+        "rank_evaluate_ms": rank_eval,
         "e2e": {"value": ncand / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "stage1_solve_s": e2e_s},
         "gpu_launches": int(launches),

@@ -112,6 +112,10 @@ struct coral_s1_handle {
   cudaEvent_t side_ev[kStreams] = {};
   cudaEvent_t fork_ev = nullptr;
   std::vector<unsigned char> flags_h;
+  std::vector<char> model_used;
+  std::vector<double> memb_h, wbytes_h;  // config memory bytes, model weight bytes
+  double rho = 0;
+  DevBuf lat_sums, lat_soff;
   // per-launch timing of the lattice kernels (coral_s1_kernel_stats)
   static constexpr int kTimedMax = 512;
   cudaEvent_t tev[kTimedMax][2] = {};
@@ -945,7 +949,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
                     &h->sort_a, &h->sort_b, &h->perm_a, &h->perm_b, &h->segk, &h->scanv,
                     &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
-                    &h->lat_sub, &h->lat_maxn, &h->lat_flags_h};
+                    &h->lat_sub, &h->lat_maxn, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release();
@@ -1061,6 +1065,10 @@ int coral_s1_set_problem(coral_s1_handle* h, const coral_s1_problem* p) {
   d.pm = (const int*)(b + o_pm); d.pp = (const int*)(b + o_pp); d.pc = (const int*)(b + o_pc);
   d.pj = (const int*)(b + o_pj); d.pb = (const int*)(b + o_pb); d.pt = (const double*)(b + o_pt);
   h->U = universe_size(K, p->n_max);
+  h->memb_h = memb;
+  h->rho = p->rho;
+  h->wbytes_h.assign(NM, 0.0);
+  for (int m = 0; m < NM; ++m) h->wbytes_h[m] = (p->mdl_params_total_b[m] * 1e9) * p->mdl_bytes_per_param[m];
   h->have_problem = true;
   h->have_tables = h->have_enum = h->have_eval = false;
   h->nfront = 0;
@@ -1303,21 +1311,47 @@ static int lattice_prepare(coral_s1_handle* h) {
   CUDA_TRY(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, h->lat_nsub.as<long long>(),
                                          h->lat_off.as<long long>(), (int)(ns + 1), st));
   h->launches += 2;
-  long long nsub_total = 0;
-  CUDA_TRY(cudaMemcpyAsync(&nsub_total, h->lat_off.as<long long>() + ns, 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  if ((rc = h->lat_sub.ensure(std::max<long long>(nsub_total, 1) * sizeof(uint2)))) return rc;
+  // upper bound (every state has at most 2^R sub-multiset codes): no host round trip
+  if ((rc = h->lat_sub.ensure(std::max<long long>(ns << R, 1) * sizeof(uint2)))) return rc;
   lat_subtab_kernel<<<gb, 256, 0, st>>>(L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(),
                                         h->lat_off.as<long long>(), h->lat_sub.as<uint2>());
   LAUNCH_CHECK(h);
-  CUDA_TRY(cudaMemsetAsync(h->lat_maxn.p, 0, (size_t)h->NM * ns * 4, st));
-  for (int m = 0; m < h->NM; ++m) {
-    const long long nc = h->counts[m];
-    if (!nc) continue;
-    lat_maxn_kernel<<<(unsigned)((nc * 64 + 255) / 256), 256, 0, st>>>(
-        L, h->dp.inv_rank, h->keys.as<unsigned long long>() + h->koff[m], nc,
-        h->lat_maxn.as<unsigned>() + (size_t)m * ns);
-    LAUNCH_CHECK(h);
+  // maxn per model in closed form from the achievable memory sums of k configs
+  {
+    std::vector<double> mem(h->memb_h);
+    std::sort(mem.begin(), mem.end());
+    mem.erase(std::unique(mem.begin(), mem.end()), mem.end());
+    double cap = 0;  // sums at or above the largest window top never matter
+    for (int m = 0; m < h->NM; ++m)
+      if (h->model_used[m]) cap = std::max(cap, h->rho * h->wbytes_h[m]);
+    cap *= 1.0 + 1e-6;
+    const int kmax = h->n_max - 1;  // a state holds >= 1 config
+    std::vector<std::vector<double>> sums(kmax + 1);
+    sums[0].push_back(0.0);
+    for (int k = 1; k <= kmax; ++k) {
+      for (double prev : sums[k - 1])
+        for (double v : mem)
+          if (prev + v < cap) sums[k].push_back(prev + v);
+      std::sort(sums[k].begin(), sums[k].end());
+      sums[k].erase(std::unique(sums[k].begin(), sums[k].end()), sums[k].end());
+    }
+    std::vector<double> flat;
+    std::vector<int> soff(kmax + 2, 0);
+    for (int k = 0; k <= kmax; ++k) {
+      soff[k] = (int)flat.size();
+      flat.insert(flat.end(), sums[k].begin(), sums[k].end());
+    }
+    soff[kmax + 1] = (int)flat.size();
+    if ((rc = upload(h, h->lat_sums, flat)) || (rc = upload(h, h->lat_soff, soff))) return rc;
+    for (int m = 0; m < h->NM; ++m) {
+      if (!h->counts[m] || !h->model_used[m]) continue;
+      const double lo = h->wbytes_h[m], hi = h->rho * lo;
+      lat_maxn_closed_kernel<<<gb, 256, 0, st>>>(L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(),
+                                                 h->dp.mem_bytes, h->lat_sums.as<double>(),
+                                                 h->lat_soff.as<int>(), lo, hi, 1e-9 * hi, h->n_max,
+                                                 h->lat_maxn.as<unsigned>() + (size_t)m * ns);
+      LAUNCH_CHECK(h);
+    }
   }
   // workspaces
   const long long LuP = h->maxLu + 1;
@@ -1441,6 +1475,10 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   h->ntimed = 0;
   // records not improved by any unit read as infeasible (num_stages 0)
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), st));
+  h->model_used.assign(h->NM, 0);  // lattice tables only for the models this call evaluates
+  for (int mp = 0; mp < NMP; ++mp)
+    for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
+      if (take(mp, S)) h->model_used[mp / h->NP] = 1;
   if ((rc = lattice_prepare(h))) return rc;
   CUDA_TRY(cudaStreamSynchronize(st));  // flags_h valid
   CUDA_TRY(cudaEventRecord(h->fork_ev, st));

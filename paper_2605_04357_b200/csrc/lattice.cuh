@@ -104,25 +104,54 @@ __device__ __forceinline__ int lat_tokens(const int* __restrict__ inv_rank, unsi
 }
 
 // maxn[idx] = max |combo| over the model's candidates containing state idx.
-// One thread per (combo, sub-multiset code).
+// One thread per candidate, looping over its sub-multiset codes.
 __global__ void lat_maxn_kernel(LatModel L, const int* __restrict__ inv_rank,
                                 const unsigned long long* __restrict__ keys, long long ncombo,
                                 unsigned* __restrict__ maxn) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long ci = t >> 6;
-  const int code = (int)(t & 63);
+  const long long ci = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (ci >= ncombo) return;
   int cfg[kMaxC], cnt[kMaxC];
   const int C = lat_tokens(inv_rank, keys[ci], cfg, cnt);
   int M = 1, n = 0;
   for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; }
-  if (code == 0 || code >= M) return;
-  int d[kMaxC], rest = code;
-  for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; }
-  int s;
-  const long long r = lat_rank_tokens(L, cfg, d, C, &s);
-  if (s > L.R) return;
-  if (maxn[r] < (unsigned)n) atomicMax(maxn + r, (unsigned)n);  // popular states saturate fast
+  int d[kMaxC] = {0, 0, 0, 0, 0, 0};
+  for (int code = 1; code < M; ++code) {
+    for (int c = 0; c < C; ++c) {  // odometer increment = next mixed-radix code
+      if (++d[c] <= cnt[c]) break;
+      d[c] = 0;
+    }
+    int s;
+    const long long r = lat_rank_tokens(L, cfg, d, C, &s);
+    if (s > L.R) continue;
+    if (maxn[r] < (unsigned)n) atomicMax(maxn + r, (unsigned)n);  // popular states saturate fast
+  }
+}
+
+// Closed form of maxn (a superset of the exact one, so it can only add cells):
+// maxn(X) = |X| + max k such that some k configs E make lo <= mem(X)+mem(E) < hi
+// (templates.py:107-111 window), with a relative slack eps; sums[soff[k]..soff[k+1])
+// are the sorted achievable memories of k-config multisets. 0 if none.
+__global__ void lat_maxn_closed_kernel(LatModel L, const int* __restrict__ inv_rank,
+                                       const unsigned long long* __restrict__ state_key,
+                                       const double* __restrict__ mem_bytes,
+                                       const double* __restrict__ sums, const int* __restrict__ soff,
+                                       double lo, double hi, double eps, int n_max,
+                                       unsigned* __restrict__ maxn) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= L.base[L.R + 1]) return;
+  int cfg[kMaxC], cnt[kMaxC];
+  const int C = lat_tokens(inv_rank, state_key[idx], cfg, cnt);
+  double m = 0.0;
+  int s = 0;
+  for (int c = 0; c < C; ++c) { s += cnt[c]; for (int k = 0; k < cnt[c]; ++k) m += mem_bytes[cfg[c]]; }
+  unsigned best = 0;
+  for (int k = min(n_max - s, n_max - 1); k >= 0 && !best; --k) {
+    const double a = lo - m - eps, b = hi - m + eps;  // need some sum in [a, b)
+    int l = soff[k], r = soff[k + 1];                  // first sum >= a
+    while (l < r) { const int mid = (l + r) >> 1; if (sums[mid] < a) l = mid + 1; else r = mid; }
+    if (l < soff[k + 1] && sums[l] < b) best = (unsigned)(s + k);
+  }
+  maxn[idx] = best;
 }
 
 // nsub[idx] = M(X) = prod(counts + 1)

@@ -1,32 +1,52 @@
 """Multi-GPU work split for stage 1.
 
-Units are (model, phase, S) triples: each has its own lattice chain, and a candidate's
-best over S is combined with an order-independent rule, so any rank may own any
-subset of S values of a (model, phase). Units are assigned longest-processing-time
-first on a deterministic cost estimate; every rank computes the same assignment.
+Units are (model, phase, S) triples: each S has its own lattice layers and top
+cells, and a candidate's best over S is combined with an order-independent rule
+(ties -> fewer stages), so any rank may own any subset of S values of a (model,
+phase). A rank that owns at least one S of a (model, phase) also pays that chain's
+fixed part (its top-cell setup per candidate, memory-window table, decode, launches),
+so the greedy below charges the fixed part once per (rank, chain) and keeps the S
+values of a chain together unless splitting balances better.
+
+Cost model (milliseconds on one B200, calibrated with tools/calibrate_units.py on
+BASELINE config 2, profiles/r01_calibration.txt):
+  fixed(chain)  = 0.12 + 3.2e-6 * candidates
+  unit(chain,S) = 6.6e-8 * candidates * layer_units * W[S]
 """
 
 from __future__ import annotations
 
+W = {1: 0.02, 2: 0.2, 3: 0.75, 4: 1.0, 5: 0.77, 6: 0.53}
+
+
+def chain_fixed(ncombo: int) -> float:
+    return 0.12 + 3.2e-6 * ncombo
+
 
 def unit_cost(ncombo: int, lsteps: int, S: int) -> float:
-    """Relative cost of one (model, phase, S) unit: the top cells of every candidate
-    plus S - 1 lattice layers over ~lsteps layer counts."""
-    return ncombo * (1.0 + (S - 1) * lsteps / 8.0)
+    return 6.6e-8 * ncombo * lsteps * W.get(S, 0.5) + 0.005
 
 
 def assign_units(counts, lsteps, smax, num_phases: int, world: int) -> list:
     """-> per rank, a list of S bit-masks indexed by mp = model * num_phases + phase."""
     units = []
     for m, (nc, lu, sm) in enumerate(zip(counts, lsteps, smax)):
+        if not nc:
+            continue
         for p in range(num_phases):
-            for S in range(1, min(sm, lu) + 1):
+            for S in range(1, min(int(sm), int(lu)) + 1):
                 units.append((unit_cost(int(nc), int(lu), S), m * num_phases + p, S))
     units.sort(key=lambda u: -u[0])  # stable: ties keep (mp, S) order
     load = [0.0] * world
-    masks = [[0] * (len(counts) * num_phases) for _ in range(world)]
+    nmp = len(counts) * num_phases
+    masks = [[0] * nmp for _ in range(world)]
     for cost, mp, S in units:
-        r = min(range(world), key=lambda i: load[i])
-        load[r] += cost
+        fixed = chain_fixed(int(counts[mp // num_phases]))
+
+        def after(r):
+            return load[r] + cost + (0.0 if masks[r][mp] else fixed)
+
+        r = min(range(world), key=lambda i: (after(i), i))
+        load[r] = after(r)
         masks[r][mp] |= 1 << S
     return masks

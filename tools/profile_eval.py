@@ -21,11 +21,23 @@ def main():
     prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho),
                          GenContext(perf=w.perf, granularity=w.granularity))
     _, pm = _price_matrix(prob.configs, w.prices, w.regions)
+    shard = None
+    if "--rank" in sys.argv:  # emulate one rank of a multi-GPU solve on this device
+        from paper_2605_04357_b200.shard import assign_units
+        shard = (int(sys.argv[sys.argv.index("--rank") + 1]), int(sys.argv[sys.argv.index("--world") + 1]))
     for _ in range(solves):
-        prob.run()
+        if shard is None:
+            prob.run()
+        else:
+            prob.h.tables()
+            prob.h.enumerate()
+            prob.counts = prob.h.num_combos()
+            _, lsteps, smax = prob.h.table_layout()
+            prob.cand_off = [0]
+            prob.h.evaluate_units(assign_units(prob.counts, lsteps, smax, 2, shard[1])[shard[0]])
         n = prob.h.frontier(pm)
     torch.cuda.synchronize()
-    print(name, prob.num_candidates, "candidates;", n, "survivors;", prob.h.stage_ms())
+    print(name, prob.h.num_candidates(), "candidates;", n, "survivors;", prob.h.stage_ms())
 
 
 if __name__ == "__main__":
