@@ -433,7 +433,12 @@ struct TopArgs {
 
 __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
   __shared__ unsigned long long s_binom[160 * 8];
+  __shared__ unsigned char s_div[8][64];  // x / r for the mixed-radix digits (no IDIV)
   for (int i = threadIdx.x; i < 160 * 8; i += blockDim.x) s_binom[i] = A.L.binom[i];
+  for (int i = threadIdx.x; i < 8 * 64; i += blockDim.x) {
+    const int r = i >> 6, x = i & 63;
+    s_div[r][x] = (unsigned char)(r ? x / r : 0);
+  }
   __syncthreads();
   LatModel L = A.L;
   L.binom = s_binom;
@@ -456,7 +461,12 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
     ru[k] = rr[k] = 0;
     if (code < M) {
       int d[kMaxC], e[kMaxC], rest = code;
-      for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; e[c] = cnt[c] - d[c]; }
+      for (int c = 0; c < C; ++c) {
+        const int q = s_div[cnt[c] + 1][rest];
+        d[c] = rest - q * (cnt[c] + 1);
+        rest = q;
+        e[c] = cnt[c] - d[c];
+      }
       int sr;
       ru[k] = lat_rank_tokens(L, cfg, d, C, &su[k]);
       rr[k] = lat_rank_tokens(L, cfg, e, C, &sr);
