@@ -407,6 +407,27 @@ __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
   if (tid == 0) A.rec[ci] = s_rec;
 }
 
+// Warp-wide (value desc, code asc) selection of the reference tie rule with the
+// hardware reductions: candidate values are >= 0 (or kNegInf for an empty lane, which
+// never wins), and non-negative doubles order like their bit patterns, so the max is
+// the lexicographic max of (hi word, lo word); ties go to the smallest code. All
+// lanes receive the winner's (value, code, j).
+__device__ __forceinline__ void warp_argmax_code(double& v, int& code, int& j) {
+  const bool ok = v >= 0.0;
+  const unsigned long long b = ok ? (unsigned long long)__double_as_longlong(v) : 0ull;
+  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const bool top = hi == mhi && lo == mlo;
+  const unsigned c = __reduce_min_sync(0xffffffffu, top ? (unsigned)code : 0xffffffffu);
+  const unsigned who = __ballot_sync(0xffffffffu, top && (unsigned)code == c);
+  const int src = __ffs(who) - 1;
+  const double wv = __shfl_sync(0xffffffffu, v, src);
+  j = __shfl_sync(0xffffffffu, j, src);
+  code = (int)c;
+  v = wv;
+}
+
 // --------------------------------------------------------------------------------
 // Lattice top cells: one warp per candidate of one (model, phase), every S in smask.
 // f_S[S][Lu][full] = max over u (lanes) of the crossing with f_S[S-1][.][full-u]
@@ -495,12 +516,7 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
       dp_pair(val + ru[k] * LuP, lay + rr[k] * LuP, Lu, Lu - (S - 1), true, cand, cj);
       if (cand > best) { best = cand; bu = lane + 1 + 32 * k; bj = cj; }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int ou = __shfl_xor_sync(0xffffffffu, bu, o);
-      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-      if (ob > best || (ob == best && ou < bu)) { best = ob; bu = ou; bj = oj; }
-    }
+    warp_argmax_code(best, bu, bj);
     if (best > tbest && best > 1e-9) { tbest = best; twin = S; tcode = bu; tj = bj; }
   }
   if (lane) return;
