@@ -192,6 +192,19 @@ int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t*
 int coral_s1_stage_ms(const coral_s1_handle* h, double* tables_ms, double* enumerate_ms,
                       double* evaluate_ms, double* frontier_ms);
 
+/* ---- persistence: TemplateLibrary.save (templates.py:364-377)
+ * streamed from device records. header = json.dumps(meta, sort_keys=True); mp_order
+ * lists (model, phase) slots in library order; model_json[m] = json.dumps(name),
+ * phase_json[p] = json.dumps(phase), slo_json[m] = json.dumps([prefill_ms, decode_ms]),
+ * cfg_json[c] = json.dumps(config name) (config index order). Byte-identical to the
+ * reference's file for the same templates. */
+int coral_s1_write_library(coral_s1_handle* h, const char* path, const char* header, int n_mp,
+                           const int32_t* mp_order, const char* const* model_json,
+                           const char* const* phase_json, const char* const* slo_json,
+                           const char* const* cfg_json, int64_t* n_written);
+/* CPython repr(float) of v into out (cap >= 40); host-only helper, no device needed */
+int coral_s1_format_double(double v, char* out, int cap);
+
 /* device time of the last evaluate's lattice kernels of one kind (0 top cells,
  * 1 layers, 2 value tables): summed CUDA-event time of each launch on its stream */
 int coral_s1_kernel_stats(const coral_s1_handle* h, int kind, double* total_ms, int64_t* launches);

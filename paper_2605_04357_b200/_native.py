@@ -104,6 +104,10 @@ def load():
                                                     _f64p, C.c_int64, _i32p, _f64p, _i64p, _i64p]),
             "coral_s1_stage_ms": (C.c_int, [vp, _f64p, _f64p, _f64p, _f64p]),
             "coral_s1_kernel_stats": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
+            "coral_s1_write_library": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_int, _i32p,
+                                                 C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
+                                                 C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), _i64p]),
+            "coral_s1_format_double": (C.c_int, [C.c_double, C.c_char_p, C.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -121,6 +125,13 @@ def exported_symbols() -> list:
     with open(hdr) as fh:
         text = fh.read()
     return sorted(set(re.findall(r"\b(coral_s1_[a-z_0-9]+)\s*\(", text)))
+
+
+def format_double(v: float) -> str:
+    """CPython repr(float) computed by the native writer's formatter (host only)."""
+    buf = C.create_string_buffer(64)
+    _check(load().coral_s1_format_double(float(v), buf, 64))
+    return buf.value.decode()
 
 
 class NativeError(RuntimeError):
@@ -303,6 +314,20 @@ class Handle:
         t, n = C.c_double(), C.c_int64()
         _check(self._lib.coral_s1_kernel_stats(self._h, kind, C.byref(t), C.byref(n)))
         return t.value, n.value
+
+    def write_library(self, path: str, header: str, mp_order, model_json, phase_json, slo_json,
+                      cfg_json) -> int:
+        def strs(xs):
+            arr = (C.c_char_p * max(len(xs), 1))()
+            for i, x in enumerate(xs):
+                arr[i] = x.encode()
+            return arr
+        order = np.ascontiguousarray(mp_order, dtype=np.int32)
+        n = C.c_int64()
+        _check(self._lib.coral_s1_write_library(
+            self._h, path.encode(), header.encode(), len(order), _ptr(order, C.c_int32),
+            strs(model_json), strs(phase_json), strs(slo_json), strs(cfg_json), C.byref(n)))
+        return n.value
 
     def stage_ms(self) -> dict:
         vals = [C.c_double() for _ in range(4)]

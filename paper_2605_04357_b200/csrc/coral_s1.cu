@@ -19,6 +19,7 @@
 
 #include "../../include/coral_s1.h"
 #include "lattice.cuh"
+#include "pyrepr.h"
 #include "placement_dp.cuh"
 #include "roofline.cuh"
 
@@ -114,6 +115,7 @@ struct coral_s1_handle {
   std::vector<unsigned char> flags_h;
   std::vector<char> model_used;
   std::vector<double> memb_h, wbytes_h;  // config memory bytes, model weight bytes
+  std::vector<int> inv_rank_h;           // str rank -> config index
   double rho = 0;
   DevBuf lat_sums, lat_soff;
   // per-launch timing of the lattice kernels (coral_s1_kernel_stats)
@@ -1092,6 +1094,7 @@ int coral_s1_set_problem(coral_s1_handle* h, const coral_s1_problem* p) {
   d.pj = (const int*)(b + o_pj); d.pb = (const int*)(b + o_pb); d.pt = (const double*)(b + o_pt);
   h->U = universe_size(K, p->n_max);
   h->memb_h = memb;
+  h->inv_rank_h.assign(inv.begin(), inv.begin() + std::max(K, 1));
   h->rho = p->rho;
   h->wbytes_h.assign(NM, 0.0);
   for (int m = 0; m < NM; ++m) h->wbytes_h[m] = (p->mdl_params_total_b[m] * 1e9) * p->mdl_bytes_per_param[m];
@@ -1742,6 +1745,93 @@ int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t*
   CUDA_TRY(cudaMemcpyAsync(stage_counts, out + ob_sc, ncases * kMaxC * kMaxC * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return 0;
+}
+
+int coral_s1_format_double(double v, char* out, int cap) {
+  if (!out || cap < 40) return fail(CORAL_S1_EINVAL, "buffer too small");
+  py_repr_double(v, out);
+  return 0;
+}
+
+// Stream the evaluated library as the reference's JSONL (templates.py:364-377):
+// header line, then one json.dumps(record, sort_keys=True) line per feasible
+// template, (model, phase) in mp_order, combos in str order. JSON string fragments
+// (json.dumps of names, SLO lists) come from the caller so escaping and number
+// types match Python exactly.
+int coral_s1_write_library(coral_s1_handle* h, const char* path, const char* header, int n_mp,
+                           const int32_t* mp_order, const char* const* model_json,
+                           const char* const* phase_json, const char* const* slo_json,
+                           const char* const* cfg_json, int64_t* n_written) {
+  if (!h || !h->have_eval) return fail(CORAL_S1_EINVAL, "evaluate first");
+  if (!path || !header) return fail(CORAL_S1_EINVAL, "null path/header");
+  CUDA_TRY(cudaSetDevice(h->device));
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(CORAL_S1_EINVAL, std::string("cannot open ") + path);
+  std::vector<char> out;
+  out.reserve(1 << 24);
+  auto put = [&](const char* s, size_t n) { out.insert(out.end(), s, s + n); };
+  auto puts_ = [&](const char* s) { put(s, strlen(s)); };
+  auto flush = [&]() {
+    if (!out.empty()) fwrite(out.data(), 1, out.size(), f);
+    out.clear();
+  };
+  puts_(header);
+  put("\n", 1);
+  int64_t written = 0;
+  std::vector<coral_s1_record> rec;
+  std::vector<unsigned long long> keys;
+  int keys_model = -1;
+  char num[64];
+  for (int i = 0; i < n_mp; ++i) {
+    const int mp = mp_order[i];
+    if (mp < 0 || mp >= h->NM * h->NP) { fclose(f); return fail(CORAL_S1_EINVAL, "bad mp in order"); }
+    const int m = mp / h->NP, ph = mp % h->NP;
+    const int64_t cnt = h->counts[m];
+    if (m != keys_model) {
+      keys.resize(cnt);
+      if (cnt)
+        CUDA_TRY(cudaMemcpyAsync(keys.data(), h->keys.as<unsigned long long>() + h->koff[m], cnt * 8,
+                                 cudaMemcpyDeviceToHost, h->stream));
+      keys_model = m;
+    }
+    rec.resize(cnt);
+    if (cnt)
+      CUDA_TRY(cudaMemcpyAsync(rec.data(), h->rec.as<coral_s1_record>() + h->cand_off[mp],
+                               cnt * sizeof(coral_s1_record), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    for (int64_t c = 0; c < cnt; ++c) {
+      const coral_s1_record& r = rec[c];
+      if (!r.num_stages) continue;
+      puts_("{\"combo\": [");
+      for (int t = 0; t < kMaxC; ++t) {
+        const unsigned tok = (unsigned)(keys[c] >> (kKeyTokenBits * (kMaxC - 1 - t))) & 511u;
+        if (!tok) break;
+        if (t) puts_(", ");
+        puts_("[");
+        puts_(cfg_json[h->inv_rank_h[(tok >> 3) - 1]]);
+        put(num, sprintf(num, ", %u]", tok & 7u));
+      }
+      puts_("], \"layers_per_stage\": [");
+      for (int s2 = 0; s2 < r.num_stages; ++s2) put(num, sprintf(num, s2 ? ", %u" : "%u", r.layers_per_stage[s2]));
+      puts_("], \"model\": ");
+      puts_(model_json[m]);
+      put(num, sprintf(num, ", \"num_stages\": %u, \"phase\": ", r.num_stages));
+      puts_(phase_json[ph]);
+      puts_(", \"slo\": ");
+      puts_(slo_json[m]);
+      puts_(", \"stage_of_node\": [");
+      for (int k = 0; k < r.num_nodes; ++k) put(num, sprintf(num, k ? ", %u" : "%u", r.stage_of_node[k]));
+      puts_("], \"throughput_tps\": ");
+      put(num, py_repr_double(r.throughput_tps, num));
+      puts_("}\n");
+      ++written;
+      if (out.size() > (1u << 24)) flush();
+    }
+  }
+  flush();
+  const bool ok = fclose(f) == 0;
+  if (n_written) *n_written = written;
+  return ok ? 0 : fail(CORAL_S1_EINVAL, "write failed");
 }
 
 int coral_s1_kernel_stats(const coral_s1_handle* h, int kind, double* total_ms, int64_t* launches) {

@@ -384,12 +384,14 @@ class TemplateLibrary:
 # ---------------------------------------------------------------------------------
 
 def build_library(configs, models, slos, caps, ctx=None, workers: int = 1,
-                  method: str = "search", phases=PHASES) -> TemplateLibrary:
+                  method: str = "search", phases=PHASES, lazy: bool = False):
     """Generate the full template library on the GPU (templates.py:417-505).
 
     `workers` is accepted for signature compatibility and ignored (the device is the
     parallelism). `method` must be "search": the reference's ILP path
     (templates.py:455-456) is a test oracle, not part of the stage-1 hot path.
+    `lazy=True` returns a LazyTemplateLibrary (same interface, objects built on
+    access, native byte-identical save).
     """
     del workers
     ctx = ctx or GenContext()
@@ -403,6 +405,8 @@ def build_library(configs, models, slos, caps, ctx=None, workers: int = 1,
         return TemplateLibrary(entries=[], meta=meta)
     prob = Stage1Problem(configs, models, slos, caps, ctx, phases)
     prob.run()
+    if lazy:  # array-backed: objects on access, native save
+        return LazyTemplateLibrary(prob, meta)
     return TemplateLibrary(entries=prob.library_entries(), meta=meta, _presorted=True)
 
 
@@ -449,3 +453,114 @@ def stage_budget_s(model, slo, phase, S, ctx) -> float:
     cfg = NodeConfig(GpuSpec("probe", 1.0, 1.0, 1.0, 1.0), 1)
     h = _tables_for([cfg], model, slo, phase, S, ctx)
     return float(h.get_budgets()[0, S - 1])
+
+
+class LazyTemplateLibrary:
+    """Array-backed TemplateLibrary over one device solve.
+
+    Same interface as TemplateLibrary (templates.py:329-401): entries, meta,
+    templates_for, get, model_phases, counts_by_model_phase, __len__, save. Template
+    objects are built per (model, phase) on first access; save() streams the records
+    straight from device memory through the native writer, byte-identical to the
+    reference's TemplateLibrary.save.
+    """
+
+    def __init__(self, prob: "Stage1Problem", meta: dict):
+        self._prob = prob
+        self.meta = meta
+        NP = len(prob.phases)
+        self._mp_of = {(m.name, ph): mi * NP + pi for mi, m in enumerate(prob.models)
+                       for pi, ph in enumerate(prob.phases)}
+        self._recs = {mp: prob.records(mp) for mp in self._mp_of.values()}
+        self._feas = {mp: np.nonzero(r["num_stages"] > 0)[0] for mp, r in self._recs.items()}
+        missing = [k for k, mp in self._mp_of.items() if len(self._feas[mp]) == 0]
+        if missing:
+            raise LibraryGenError(f"no feasible template for: {sorted(missing)}")
+        for (mname, ph), mp in self._mp_of.items():
+            model = prob.models[mp // NP]
+            g = prob.ctx.layer_granularity(model)
+            if model.num_layers % g:
+                raise DomainError(f"stage layers sum to {(model.num_layers // g) * g}, "
+                                  f"model has {model.num_layers}")
+        self._keys = {}
+        self._combos = {}
+        self._segments = {}
+        self._entries = None
+        self._rank_of = {c.name: r for r, c in enumerate(prob.cfg_by_rank)}
+
+    def _model_keys(self, m):
+        if m not in self._keys:
+            self._keys[m] = self._prob.keys(m)
+        return self._keys[m]
+
+    def model_phases(self) -> list:
+        return sorted(self._mp_of)
+
+    def counts_by_model_phase(self) -> dict:
+        return {k: int(len(self._feas[self._mp_of[k]])) for k in self.model_phases()}
+
+    def __len__(self) -> int:
+        return int(sum(len(f) for f in self._feas.values()))
+
+    def templates_for(self, model: str, phase: str) -> list:
+        key = (model, phase)
+        if key not in self._mp_of:
+            return []
+        if key not in self._segments:
+            mp = self._mp_of[key]
+            NP = len(self._prob.phases)
+            m = mp // NP
+            if m not in self._combos:
+                self._combos[m] = self._prob.combo_objects(self._model_keys(m))
+            combos = self._combos[m]
+            recs, feas = self._recs[mp], self._feas[mp]
+            mdl = self._prob.models[m]
+            self._segments[key] = [self._prob.make_template(mdl, phase, combos[i], recs[i])
+                                   for i in feas.tolist()]
+        return self._segments[key]
+
+    @property
+    def entries(self) -> list:
+        if self._entries is None:
+            self._entries = [t for k in self.model_phases() for t in self.templates_for(*k)]
+        return self._entries
+
+    def get(self, template_id: str) -> ServingTemplate:
+        model, phase, combo = template_id.split("|", 2)
+        mp = self._mp_of.get((model, phase))
+        if mp is None:
+            raise KeyError(template_id)
+        key = 0
+        toks = combo.split("+")
+        try:
+            for tok in toks:
+                name, n = tok.rsplit("*", 1)
+                key = (key << 9) | ((self._rank_of[name] + 1) << 3) | int(n)
+        except (KeyError, ValueError):
+            raise KeyError(template_id) from None
+        key <<= 9 * (_native.MAX_NODES - len(toks))
+        NP = len(self._prob.phases)
+        keys = self._model_keys(mp // NP)
+        i = int(np.searchsorted(keys, np.uint64(key)))
+        if i >= len(keys) or int(keys[i]) != key or self._recs[mp]["num_stages"][i] == 0:
+            raise KeyError(template_id)
+        m = mp // NP
+        combo_obj = self._prob.combo_objects(keys[i:i + 1])[0]
+        return self._prob.make_template(self._prob.models[m], phase, combo_obj, self._recs[mp][i])
+
+    def reindex(self) -> None:
+        pass
+
+    def save(self, path: str) -> int:
+        """Native JSONL writer; returns the number of templates written."""
+        prob = self._prob
+        NP = len(prob.phases)
+        order = [self._mp_of[k] for k in self.model_phases()]
+        header = json.dumps(self.meta, sort_keys=True)
+        model_json = [json.dumps(m.name) for m in prob.models]
+        phase_json = [json.dumps(p) for p in prob.phases]
+        slo_json = [json.dumps([prob.slos[m.name].prefill_ms, prob.slos[m.name].decode_ms])
+                    for m in prob.models]
+        cfg_json = [json.dumps(c.name) for c in prob.configs]
+        del NP
+        return prob.h.write_library(path, header, order, model_json, phase_json, slo_json, cfg_json)

@@ -281,5 +281,45 @@ def extended(ext_pkl):
         dump("frontier_extended.json.gz", frontier_oracle(recs, prices, [r.name for r in regions]))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--save-digests" not in sys.argv:
     main()
+
+
+def saved_file_digest(name, records_or_lib):
+    """sha256 of the reference's own TemplateLibrary.save (templates.py:364-377) output."""
+    import tempfile
+    from hetserve.domain import NodeComboKey, Placement, ServingTemplate
+    from hetserve.templates import TemplateLibrary, _library_meta
+    configs, models, slos, caps, ctx, regions, prices = scenario_inputs(name)
+    if isinstance(records_or_lib, TemplateLibrary):
+        lib = records_or_lib
+    else:
+        cfg = {c.name: c for c in configs}
+        entries = []
+        for (model, phase, combo, S, layers, son, T) in records_or_lib:
+            items = tuple((cfg[tok.rsplit("*", 1)[0]], int(tok.rsplit("*", 1)[1])) for tok in combo.split("+"))
+            entries.append(ServingTemplate(model, phase, slos[model], NodeComboKey(items),
+                                           Placement(S, tuple(layers), tuple(son)), T))
+        lib = TemplateLibrary(entries=entries,
+                              meta=_library_meta(sorted(configs, key=lambda c: c.name), models, slos, caps, ctx))
+    with tempfile.NamedTemporaryFile(suffix=".jsonl") as fh:
+        lib.save(fh.name)
+        data = open(fh.name, "rb").read()
+    return {"sha256": hashlib.sha256(data).hexdigest(), "bytes": len(data),
+            "header": data.split(b"\n", 1)[0].decode()}
+
+
+def save_digests(pkls):
+    out = {}
+    for name in ("c1", "core"):
+        configs, models, slos, caps, ctx, regions, prices = scenario_inputs(name)
+        out[name] = saved_file_digest(name, build_library(configs, models, slos, caps, ctx,
+                                                          workers=os.cpu_count()))
+    for name, pkl in pkls.items():
+        with open(pkl, "rb") as fh:
+            out[name] = saved_file_digest(name, pickle.load(fh)["records"])
+    dump("saved_libraries.json.gz", out)
+
+
+if __name__ == "__main__" and "--save-digests" in sys.argv:
+    save_digests({"extended": "/tmp/ref_extended.pkl", "c3": "/tmp/ref_c3.pkl"})

@@ -253,3 +253,32 @@ def test_lattice_path_equals_per_candidate_path():
             assert recs.tobytes() == full[mp][:len(recs.tobytes())]
         else:
             assert recs.tobytes() == full[mp]
+
+
+@pytest.mark.parametrize("w", ["c1", "core", "extended", "c3"])
+def test_lazy_library_native_save_byte_identical(w, tmp_path):
+    """the array-backed library streams a JSONL file
+    byte-identical to the reference's TemplateLibrary.save (285.7 MB for config 2)."""
+    import hashlib
+    import time
+    ref = golden("saved_libraries.json.gz")[w]
+    configs, models, slos, caps, ctx, regions, prices = workload(w)
+    lib = build_library(configs, models, slos, caps, ctx, lazy=True)
+    path = str(tmp_path / "lib.jsonl")
+    t0 = time.perf_counter()
+    n = lib.save(path)
+    dt = time.perf_counter() - t0
+    data = open(path, "rb").read()
+    assert n == len(lib)
+    assert len(data) == ref["bytes"]
+    assert hashlib.sha256(data).hexdigest() == ref["sha256"]
+    print(f"{w}: {n} templates, {len(data)} bytes saved in {dt:.3f}s")
+    if w in ("c1", "core"):
+        eager = build_library(configs, models, slos, caps, ctx)
+        assert [template_line(t) for t in lib.entries] == [template_line(t) for t in eager.entries]
+        assert lib.counts_by_model_phase() == eager.counts_by_model_phase()
+        for t in eager.entries[::37]:
+            assert template_line(lib.get(t.template_id)) == template_line(t)
+        mp = lib.model_phases()[0]
+        assert [template_line(t) for t in lib.templates_for(*mp)] == \
+               [template_line(t) for t in eager.templates_for(*mp)]
