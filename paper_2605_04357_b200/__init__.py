@@ -6,7 +6,7 @@ throughput-vs-cost frontier that feeds the unchanged stage-2 MILP. All computati
 runs in libcoral_s1.so (hand-written sm_100a CUDA behind a C ABI, include/coral_s1.h).
 """
 
-from .frontier import FrontierEntry, TemplateFrontier, build_frontier
+from .frontier import FrontierEntry, FrontierSession, TemplateFrontier, build_frontier
 from .kernels import NEG_INF, placement_search, placement_search_batch
 from .library import (GenContext, LibraryCaps, LibraryGenError, Stage1Problem, TemplateLibrary,
                       build_library, enumerate_combos, stage_budget_s, throughput_table)

@@ -182,5 +182,18 @@ def c5_workload(seed: int = 0, n_models: int = 50) -> Stage1Workload:
                           prices=make_prices(configs, regs))
 
 
+def c4_epoch_prices(w: Stage1Workload, epoch: int) -> dict:
+    """BASELINE config 4 price path: per (region, config) the base
+    price times exp(0.1 z), z ~ N(0, 1) from default_rng(1000 + epoch), drawn in
+    (region, config) name order."""
+    rng = np.random.default_rng(1000 + epoch)
+    out = {}
+    for r in sorted(w.regions, key=lambda r: r.name):
+        for c in sorted(w.configs, key=lambda c: c.name):
+            base = w.prices[(r.name, c.name)]
+            out[(r.name, c.name)] = base * math.exp(0.1 * rng.standard_normal())
+    return out
+
+
 WORKLOADS = {"c1": c1_workload, "core": core_workload, "extended": extended_workload,
              "c2": extended_workload, "c3": c3_workload, "c5": c5_workload}

@@ -190,4 +190,23 @@ def materialise(prob: Stage1Problem, items: np.ndarray, region_names, meta) -> T
                             num_candidates=int(prob.cand_off[-1]) if prob.cand_off is not None else 0)
 
 
-__all__ = ["FrontierEntry", "TemplateFrontier", "build_frontier", "materialise"]
+class FrontierSession:
+    """Stage 1 solved once, frontiers re-priced many times (BASELINE config 4).
+
+    Stage-1 records are price-invariant (T-hat and the DP never read prices), so an
+    epoch whose prices or regions change only re-runs the device pricing + skyline
+    over the cached records ("incremental re-solve").
+    """
+
+    def __init__(self, configs, models, slos, caps, ctx=None, phases=PHASES):
+        self.ctx = ctx or GenContext()
+        self.prob = Stage1Problem(configs, models, slos, caps, self.ctx, phases).run()
+        self.meta = library_meta(self.prob.configs, models, slos, caps, self.ctx)
+
+    def frontier(self, prices, regions=None) -> TemplateFrontier:
+        region_names, pmat = _price_matrix(self.prob.configs, prices, regions)
+        n = self.prob.h.frontier(pmat)
+        return materialise(self.prob, self.prob.h.get_frontier(n), region_names, self.meta)
+
+
+__all__ = ["FrontierEntry", "FrontierSession", "TemplateFrontier", "build_frontier", "materialise"]

@@ -282,3 +282,35 @@ def test_lazy_library_native_save_byte_identical(w, tmp_path):
         mp = lib.model_phases()[0]
         assert [template_line(t) for t in lib.templates_for(*mp)] == \
                [template_line(t) for t in eager.templates_for(*mp)]
+
+
+def test_c4_incremental_reprice_equals_full_resolve():
+    """BASELINE config 4: per-epoch prices; the cached-records re-pricing path gives
+    exactly the frontier of a full stage-1 re-solve, and the oracle's."""
+    from paper_2605_04357_b200 import FrontierSession, catalog
+    from tests.helpers import price_matrix
+    w = catalog.extended_workload()
+    caps, ctx = LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf)
+    sess = FrontierSession(w.configs, w.models, w.slos, caps, ctx)
+    for epoch in (1, 2):
+        prices = catalog.c4_epoch_prices(w, epoch)
+        inc = sess.frontier(prices, regions=w.regions)
+        full = build_frontier(w.configs, w.models, w.slos, caps, prices, regions=w.regions, ctx=ctx)
+        def rows(f):
+            return sorted((k, str(e.template.combo), e.price_usd_h, e.throughput_tps)
+                          for k, v in f.segments.items() for e in v)
+        assert rows(inc) == rows(full)
+        assert len(inc) > 1000
+    # oracle check of the last epoch on two models
+    op = oracle_problem("extended")
+    pm = price_matrix(op.configs, prices, w.regions)
+    cbr = cfg_by_rank(op.configs)
+    for mi in (1, 2):
+        keys = op.enumerate(mi)
+        for pi, ph in enumerate(("prefill", "decode")):
+            recs = op.solve(mi, pi, keys)
+            reg, idx = op.frontier(keys, recs, pm)
+            want = sorted((w.regions[r].name, key_str(keys[i], cbr)) for r, i in zip(reg, idx))
+            got = sorted((k[2], str(e.template.combo)) for k, v in inc.segments.items()
+                         if k[0] == w.models[mi].name and k[1] == ph for e in v)
+            assert got == want
