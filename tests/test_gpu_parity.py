@@ -314,3 +314,32 @@ def test_c4_incremental_reprice_equals_full_resolve():
             got = sorted((k[2], str(e.template.combo)) for k, v in inc.segments.items()
                          if k[0] == w.models[mi].name and k[1] == ph for e in v)
             assert got == want
+
+
+def test_c5_synthetic_scale_sampled_parity():
+    """BASELINE config 5 (50 synthetic models x 40 configs, ~4.7e8 candidates): a
+    stride sample of every (model, phase) re-solved by the oracle, bit-identical."""
+    from paper_2605_04357_b200 import catalog
+    w = catalog.c5_workload()
+    caps, ctx = LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf)
+    prob = Stage1Problem(w.configs, w.models, w.slos, caps, ctx).run()
+    assert prob.num_candidates > 1e8
+    op = oracle_problem((w.configs, w.models, w.slos, caps, ctx))
+    cbr = prob.cfg_by_rank
+    checked = 0
+    for mi in range(0, len(w.models), 7):
+        keys = prob.keys(mi)
+        if not len(keys):
+            continue
+        stride = max(1, len(keys) // 60)
+        sample = keys[::stride]
+        for pi, ph in enumerate(("prefill", "decode")):
+            recs = prob.records(mi * 2 + pi)[::stride]
+            ref = op.solve(mi, pi, sample)
+            for k, a, b in zip(sample, recs, ref):
+                assert (a["num_stages"] == 0) == (b["num_stages"] == 0)
+                if a["num_stages"]:
+                    assert record_line(w.models[mi].name, ph, k, a, cbr) == \
+                           record_line(w.models[mi].name, ph, k, b, cbr)
+                checked += 1
+    assert checked > 500
