@@ -202,6 +202,13 @@ int coral_s1_write_library(coral_s1_handle* h, const char* path, const char* hea
                            const int32_t* mp_order, const char* const* model_json,
                            const char* const* phase_json, const char* const* slo_json,
                            const char* const* cfg_json, int64_t* n_written);
+/* ---- caps sweep (cli.py:233-272 cmd_sweep): for caps entries
+ * (n_max[k], rho[k]) inside the solved caps, the template count and the best
+ * tokens/s per USD-h (price = min over regions, prices[r*K + c], NaN = not offered)
+ * over phases in phase_mask (bit = phase slot), from ONE evaluated solve. */
+int coral_s1_sweep(coral_s1_handle* h, int ncaps, const int32_t* n_max, const double* rho,
+                   int num_regions, const double* prices, uint32_t phase_mask, int64_t* counts,
+                   double* best);
 /* CPython repr(float) of v into out (cap >= 40); host-only helper, no device needed */
 int coral_s1_format_double(double v, char* out, int cap);
 

@@ -108,6 +108,8 @@ def load():
                                                  C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
                                                  C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), _i64p]),
             "coral_s1_format_double": (C.c_int, [C.c_double, C.c_char_p, C.c_int]),
+            "coral_s1_sweep": (C.c_int, [vp, C.c_int, _i32p, _f64p, C.c_int, _f64p, C.c_uint32, _i64p,
+                                         _f64p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -328,6 +330,17 @@ class Handle:
             self._h, path.encode(), header.encode(), len(order), _ptr(order, C.c_int32),
             strs(model_json), strs(phase_json), strs(slo_json), strs(cfg_json), C.byref(n)))
         return n.value
+
+    def sweep(self, n_max, rho, prices, phase_mask: int):
+        n_max = np.ascontiguousarray(n_max, dtype=np.int32)
+        rho = np.ascontiguousarray(rho, dtype=np.float64)
+        prices = np.ascontiguousarray(prices, dtype=np.float64)
+        counts = np.zeros(max(len(n_max), 1), dtype=np.int64)
+        best = np.zeros(max(len(n_max), 1))
+        _check(self._lib.coral_s1_sweep(self._h, len(n_max), _ptr(n_max, C.c_int32), _ptr(rho, C.c_double),
+                                        prices.shape[0], _ptr(prices, C.c_double), phase_mask,
+                                        _ptr(counts, C.c_int64), _ptr(best, C.c_double)))
+        return counts[:len(n_max)], best[:len(n_max)]
 
     def stage_ms(self) -> dict:
         vals = [C.c_double() for _ in range(4)]

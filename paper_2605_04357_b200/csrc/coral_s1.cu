@@ -774,6 +774,56 @@ __global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long
   if (keep) A.items[pos + __popc(ballot & ((1u << lane) - 1u))] = it;
 }
 
+// cmd_sweep statistics (cli.py:233-272) for several LibraryCaps at once from one
+// solve at the widest caps: DP records do not depend on the caps, only the
+// enumeration window does (templates.py:107-111). Per candidate: window test per caps
+// entry, price = min over regions of the combo-order sum (regions with an unpriced
+// config skipped), efficiency T / price; per entry count + max efficiency.
+__global__ void sweep_kernel(FrontArgs A, int ncaps, const int* __restrict__ cap_n,
+                             const double* __restrict__ cap_rho, unsigned phase_mask,
+                             unsigned long long* __restrict__ counts,
+                             unsigned long long* __restrict__ best_bits) {
+  const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci >= A.ncand) return;
+  const coral_s1_record rc = A.rec[ci];
+  if (rc.num_stages == 0) return;
+  int lo = 0, hi = A.NMP;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (A.cand_off[mid] <= ci) lo = mid; else hi = mid;
+  }
+  if (!((phase_mask >> (lo % A.P.NP)) & 1u)) return;
+  const int m = lo / A.P.NP;
+  const unsigned long long key = A.keys[A.koff[m] + (ci - A.cand_off[lo])];
+  int cfg[kMaxC], cnt[kMaxC];
+  const int C = decode_key(A.P, key, cfg, cnt);
+  double mem = 0.0;
+  int n = 0;
+  for (int c = 0; c < C; ++c) {
+    n += cnt[c];
+    for (int k = 0; k < cnt[c]; ++k) mem = rn_add(mem, A.P.mem_bytes[cfg[c]]);
+  }
+  double price = __longlong_as_double(0x7ff0000000000000ll);
+  for (int r = 0; r < A.R; ++r) {
+    double total = 0.0;
+    bool ok = true;
+    for (int c = 0; c < C; ++c) {
+      const double p = A.prices[(int64_t)r * A.P.K + cfg[c]];
+      if (isnan(p)) { ok = false; break; }
+      total = rn_add(total, rn_mul((double)cnt[c], p));
+    }
+    if (ok && total < price) price = total;
+  }
+  const bool priced = isfinite(price);
+  const double eff = priced ? rn_div(rc.throughput_tps, price) : 0.0;
+  const double w = rn_mul(rn_mul(A.P.ptb[m], 1e9), A.P.bpp[m]);
+  for (int k = 0; k < ncaps; ++k) {
+    if (n > cap_n[k] || !(w <= mem && mem < rn_mul(cap_rho[k], w))) continue;
+    atomicAdd(counts + k, 1ull);
+    if (priced) atomicMax(best_bits + k, (unsigned long long)__double_as_longlong(eff));
+  }
+}
+
 // sort-key extraction for the 4 stable LSD passes
 __global__ void sortkey_kernel(const coral_s1_frontier_item* __restrict__ items,
                                const unsigned* __restrict__ perm, int64_t n, int field, int R,
@@ -1744,6 +1794,58 @@ int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t*
   CUDA_TRY(cudaMemcpyAsync(stage_j, out + ob_sj, ncases * kMaxC * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(stage_counts, out + ob_sc, ncases * kMaxC * kMaxC * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int coral_s1_sweep(coral_s1_handle* h, int ncaps, const int32_t* n_max, const double* rho,
+                   int num_regions, const double* prices, uint32_t phase_mask, int64_t* counts,
+                   double* best) {
+  if (!h || !h->have_eval) return fail(CORAL_S1_EINVAL, "evaluate first");
+  if (ncaps < 0 || num_regions < 0) return fail(CORAL_S1_EINVAL, "bad sizes");
+  for (int k = 0; k < ncaps; ++k)
+    if (n_max[k] > h->n_max) return fail(CORAL_S1_EINVAL, "sweep caps must lie inside the solved caps");
+  CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  int rc;
+  std::vector<double> pv(prices, prices + (size_t)num_regions * h->K);
+  std::vector<int> nv(n_max, n_max + ncaps);
+  std::vector<double> rv(rho, rho + ncaps);
+  DevBuf capn, caprho, out;
+  if ((rc = upload(h, h->prices, pv)) || (rc = upload(h, capn, nv)) || (rc = upload(h, caprho, rv)) ||
+      (rc = out.ensure(std::max(ncaps, 1) * 16)))
+    return rc;
+  CUDA_TRY(cudaMemsetAsync(out.p, 0, std::max(ncaps, 1) * 16, st));
+  FrontArgs A;
+  A.P = h->dp;
+  A.keys = h->keys.as<unsigned long long>();
+  A.koff = h->koff_d.as<int64_t>();
+  A.cand_off = h->cand_off_d.as<int64_t>();
+  A.NMP = h->NM * h->NP;
+  A.rec = h->rec.as<coral_s1_record>();
+  A.ncand = h->ncand;
+  A.prices = h->prices.as<double>();
+  A.R = num_regions;
+  A.items = nullptr;
+  A.nitems = nullptr;
+  if (h->ncand > 0 && ncaps > 0) {
+    unsigned long long* o = out.as<unsigned long long>();
+    sweep_kernel<<<(unsigned)((h->ncand + 255) / 256), 256, 0, st>>>(A, ncaps, capn.as<int>(), caprho.as<double>(),
+                                                                    phase_mask, o, o + ncaps);
+    LAUNCH_CHECK(h);
+  }
+  std::vector<unsigned long long> hv(2 * std::max(ncaps, 1));
+  CUDA_TRY(cudaMemcpyAsync(hv.data(), out.p, hv.size() * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int k = 0; k < ncaps; ++k) {
+    counts[k] = (int64_t)hv[k];
+    unsigned long long b = hv[ncaps + k];
+    double d;
+    memcpy(&d, &b, 8);
+    best[k] = d;
+  }
+  capn.release();
+  caprho.release();
+  out.release();
   return 0;
 }
 

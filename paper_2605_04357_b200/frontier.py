@@ -210,3 +210,28 @@ class FrontierSession:
 
 
 __all__ = ["FrontierEntry", "FrontierSession", "TemplateFrontier", "build_frontier", "materialise"]
+
+
+def sweep(configs, models, slos, caps_list, prices, regions=None, ctx=None, phases=PHASES):
+    """cmd_sweep (cli.py:233-272) for a list of LibraryCaps from ONE device solve.
+
+    Stage-1 records do not depend on the caps (only the enumeration window does), so
+    the problem is solved once at the widest caps and every entry is a device-side
+    filter. Rows mirror the reference CSV:
+    (n_max, rho, templates, gen_seconds, best_tokens_per_usd_h); gen_seconds is the
+    shared solve + sweep wall time. Caps must stay within the GPU envelope (n_max <= 6).
+    """
+    import time
+
+    from .library import LibraryCaps
+    t0 = time.monotonic()
+    widest = LibraryCaps(max(c.n_max for c in caps_list), max(c.rho for c in caps_list))
+    prob = Stage1Problem(configs, models, slos, widest, ctx or GenContext(), phases).run()
+    _, pmat = _price_matrix(prob.configs, prices, regions)
+    counts, best = prob.h.sweep([c.n_max for c in caps_list], [c.rho for c in caps_list], pmat,
+                                (1 << len(prob.phases)) - 1)
+    wall = time.monotonic() - t0
+    return [(c.n_max, c.rho, int(n), wall, float(b)) for c, n, b in zip(caps_list, counts, best)]
+
+
+__all__.append("sweep")

@@ -281,7 +281,7 @@ def extended(ext_pkl):
         dump("frontier_extended.json.gz", frontier_oracle(recs, prices, [r.name for r in regions]))
 
 
-if __name__ == "__main__" and "--save-digests" not in sys.argv:
+if __name__ == "__main__" and "--save-digests" not in sys.argv and "--sweep" not in sys.argv:
     main()
 
 
@@ -323,3 +323,40 @@ def save_digests(pkls):
 
 if __name__ == "__main__" and "--save-digests" in sys.argv:
     save_digests({"extended": "/tmp/ref_extended.pkl", "c3": "/tmp/ref_c3.pkl"})
+
+
+def sweep_rows():
+    """Reference cmd_sweep semantics (cli.py:248-260): build_library per caps, best
+    tokens/s per USD-h with price = min over regions; core scenario and the c09
+    model (test_acceptance.py:320-348) on a single price list."""
+    out = {}
+    points = [(4, 8.0), (5, 10.0), (6, 12.0)]
+    configs, models, slos, caps, ctx, regions, prices = scenario_inputs("core")
+    rows = []
+    for n_max, rho in points:
+        lib = build_library(configs, models, slos, LibraryCaps(n_max, rho), ctx, workers=os.cpu_count())
+        best = 0.0
+        for t in lib.entries:
+            price = min(sum(n * prices[(r.name, cfg.name)] for cfg, n in t.combo.items) for r in regions)
+            best = max(best, t.throughput_tps / price)
+        rows.append([n_max, rho, len(lib), best])
+    out["core"] = rows
+    model = ModelSpec("m120b", num_layers=36, params_total_b=116.8, params_active_b=5.1,
+                      hidden_size=2880, kv_bytes_per_token_per_layer=2048, is_moe=True,
+                      is_hybrid_attn=True)
+    cfgs = [NodeConfig(RC.GPU_CATALOG["H100"], 2, 64.0), NodeConfig(RC.GPU_CATALOG["L40S"], 1, 64.0)]
+    rows = []
+    for n_max, rho in points:
+        lib = build_library(cfgs, [model], {"m120b": SloSpec(1000, 40)}, LibraryCaps(n_max, rho),
+                            GenContext(), phases=(PREFILL,))
+        best = 0.0
+        for t in lib.entries:
+            price = sum(n * c.gpu.rel_cost * c.gpu_count for c, n in t.combo.items)
+            best = max(best, t.throughput_tps / price)
+        rows.append([n_max, rho, len(lib), best])
+    out["c09"] = rows
+    dump("sweep.json.gz", out)
+
+
+if __name__ == "__main__" and "--sweep" in sys.argv:
+    sweep_rows()

@@ -343,3 +343,26 @@ def test_c5_synthetic_scale_sampled_parity():
                            record_line(w.models[mi].name, ph, k, b, cbr)
                 checked += 1
     assert checked > 500
+
+
+def test_sweep_matches_reference_cmd_sweep():
+    """cmd_sweep (cli.py:233-272) from one solve: template counts and best tokens/s per
+    USD-h equal the reference's per-caps rebuilds (core scenario and the c09 model)."""
+    from paper_2605_04357_b200 import catalog
+    from paper_2605_04357_b200.frontier import sweep
+    from paper_2605_04357_b200.specs import ModelSpec, NodeConfig, SloSpec
+    g = golden("sweep.json.gz")
+    caps_list = [LibraryCaps(n, r) for n, r, _, _ in g["core"]]
+    configs, models, slos, caps, ctx, regions, prices = workload("core")
+    rows = sweep(configs, models, slos, caps_list, prices, regions=regions, ctx=ctx)
+    assert [(n, r, c, b) for n, r, c, _, b in rows] == [tuple(x) for x in g["core"]]
+    model = ModelSpec("m120b", num_layers=36, params_total_b=116.8, params_active_b=5.1,
+                      hidden_size=2880, kv_bytes_per_token_per_layer=2048, is_moe=True,
+                      is_hybrid_attn=True)
+    cfgs = [NodeConfig(catalog.GPU_CATALOG["H100"], 2, 64.0), NodeConfig(catalog.GPU_CATALOG["L40S"], 1, 64.0)]
+    p = {("r", c.name): c.gpu.rel_cost * c.gpu_count for c in cfgs}
+    rows = sweep(cfgs, [model], {"m120b": SloSpec(1000, 40)}, [LibraryCaps(n, r) for n, r, _, _ in g["c09"]],
+                 p, regions=["r"], ctx=GenContext(), phases=("prefill",))
+    assert [(n, r, c, b) for n, r, c, _, b in rows] == [tuple(x) for x in g["c09"]]
+    effs = [b for *_, b in rows]
+    assert effs == sorted(effs)  # c09: best goodput/USD non-decreasing in the caps
