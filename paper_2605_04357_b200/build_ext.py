@@ -30,7 +30,29 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
+MAT_SRC = os.path.join(HERE, "csrc", "materialize.c")
+
+
+def build_materialize(force: bool = False, verbose: bool = False) -> str:
+    """CPython extension that turns device frontier items into template objects."""
+    import sysconfig
+    out = os.path.join(HERE, "_lib", "_materialize" + sysconfig.get_config_var("EXT_SUFFIX"))
+    hdr = os.path.join(os.path.dirname(HERE), "include", "coral_s1.h")
+    if not force and os.path.exists(out) and all(os.path.getmtime(d) <= os.path.getmtime(out)
+                                                 for d in (MAT_SRC, hdr)):
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = ["gcc", "-O2", "-shared", "-fPIC", "-std=c11", "-I" + sysconfig.get_paths()["include"],
+           "-o", out + ".tmp", MAT_SRC]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_materialize(force, verbose)
     if not force and not stale():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)

@@ -25,7 +25,7 @@ import numpy as np
 from . import _native
 from .library import GenContext, Stage1Problem, TemplateLibrary, library_meta
 from .shard import assign_units
-from .specs import PHASES, Placement, ServingTemplate
+from .specs import PHASES, NodeComboKey, Placement, ServingTemplate
 
 
 class FrontierEntry(namedtuple("FrontierEntry", ("template", "price_usd_h"))):
@@ -146,7 +146,24 @@ def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,
 
 
 def materialise(prob: Stage1Problem, items: np.ndarray, region_names, meta) -> TemplateFrontier:
-    """Survivor records -> ServingTemplate objects (one object per (mp, combo))."""
+    """Survivor records -> ServingTemplate objects (one per (mp, combo)), built by the
+    CPython extension _lib/_materialize (csrc/materialize.c)."""
+    from ._lib import _materialize
+    segments = _materialise_native(_materialize, prob, items, region_names)
+    return TemplateFrontier(segments=segments, meta=meta,
+                            num_candidates=int(prob.cand_off[-1]) if prob.cand_off is not None else 0)
+
+
+def _materialise_native(mod, prob, items, region_names):
+    items = np.ascontiguousarray(items)
+    return mod.materialise(items.view(np.uint8).tobytes() if len(items) else b"", list(prob.cfg_by_rank),
+                           [m.name for m in prob.models], tuple(prob.phases),
+                           [prob.slos[m.name] for m in prob.models], list(region_names),
+                           len(prob.phases), ServingTemplate, Placement, NodeComboKey, FrontierEntry)
+
+
+def materialise_py(prob: Stage1Problem, items: np.ndarray, region_names, meta) -> TemplateFrontier:
+    """Pure-Python twin of materialise (used by the tests to check the extension)."""
     NP = len(prob.phases)
     cache = {}
     segments = {}

@@ -366,3 +366,21 @@ def test_sweep_matches_reference_cmd_sweep():
     assert [(n, r, c, b) for n, r, c, _, b in rows] == [tuple(x) for x in g["c09"]]
     effs = [b for *_, b in rows]
     assert effs == sorted(effs)  # c09: best goodput/USD non-decreasing in the caps
+
+
+def test_native_materialise_equals_python():
+    """The CPython extension builds the same frontier objects as the Python twin."""
+    from paper_2605_04357_b200.frontier import _price_matrix, materialise, materialise_py
+    configs, models, slos, caps, ctx, regions, prices = workload("extended")
+    front, prob = build_frontier(configs, models, slos, caps, prices, regions=regions, ctx=ctx,
+                                 return_problem=True)
+    names, pm = _price_matrix(prob.configs, prices, regions)
+    items = prob.h.get_frontier(prob.h.frontier(pm))
+    a = materialise(prob, items, names, {})
+    b = materialise_py(prob, items, names, {})
+
+    def rows(f):
+        return [(k, e.template.template_id, e.template.placement, e.template.throughput_tps,
+                 e.template.slo, e.template.combo, e.price_usd_h) for k, v in f.segments.items() for e in v]
+    assert rows(a) == rows(b)
+    assert len(a) == 2225
