@@ -10,7 +10,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "coral_s1.cu")
 OUT = os.path.join(HERE, "_lib", "libcoral_s1.so")
-DEPS = [SRC] + [os.path.join(HERE, "csrc", f) for f in ("placement_dp.cuh", "roofline.cuh")] + \
+DEPS = [os.path.join(HERE, "csrc", f) for f in sorted(os.listdir(os.path.join(HERE, "csrc")))
+        if f.endswith((".cu", ".cuh", ".h"))] + \
        [os.path.join(os.path.dirname(HERE), "include", "coral_s1.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
