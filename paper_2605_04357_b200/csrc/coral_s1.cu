@@ -108,7 +108,7 @@ struct coral_s1_handle {
   long long lat_states = 0;
   std::vector<long long> lat_base;     // [R + 2]
   DevBuf lat_base_d, lat_binom_d, lat_key, lat_nsub, lat_off, lat_sub, lat_maxn, lat_flags_h;
-  DevBuf ws_value[kStreams], ws_f0[kStreams], ws_ch[kStreams];
+  DevBuf ws_value[kStreams], ws_f0[kStreams], ws_ch[kStreams], ws_ranks[kStreams];
   cudaStream_t side[kStreams] = {};
   cudaEvent_t side_ev[kStreams] = {};
   cudaEvent_t fork_ev = nullptr;
@@ -452,19 +452,11 @@ struct TopArgs {
   const uint2* subtab;
   coral_s1_record* rec;             // this (model, phase)'s records
   int4* win;                        // per candidate: best value (lo, hi), S, u code << 10 | j
+  const unsigned* ranks;            // [candidate][64] from lat_ranks_kernel
 };
 
 __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
-  __shared__ unsigned long long s_binom[160 * 8];
-  __shared__ unsigned char s_div[8][64];  // x / r for the mixed-radix digits (no IDIV)
-  for (int i = threadIdx.x; i < 160 * 8; i += blockDim.x) s_binom[i] = A.L.binom[i];
-  for (int i = threadIdx.x; i < 8 * 64; i += blockDim.x) {
-    const int r = i >> 6, x = i & 63;
-    s_div[r][x] = (unsigned char)(r ? x / r : 0);
-  }
-  __syncthreads();
-  LatModel L = A.L;
-  L.binom = s_binom;
+  const LatModel& L = A.L;
   const int lane = threadIdx.x & 31;
   const long long ci = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= A.ncombo) return;
@@ -474,25 +466,21 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
   for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; }
   const int Lu = A.Lu, LuP = Lu + 1;
   const int Smax = min(n, Lu);
-  // this lane's u codes (lane+1, lane+33): size, rank(u), rank(full-u), computed once
+  // this lane's u codes (lane+1, lane+33): size, idx(u), idx(full-u) from the model's
+  // rank table (code M-1-c is the complement of code c)
   int su[2];
   long long ru[2], rr[2];
+  const unsigned* rk = A.ranks + ci * 64;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int code = lane + 1 + 32 * k;
     su[k] = 1 << 20;
     ru[k] = rr[k] = 0;
     if (code < M) {
-      int d[kMaxC], e[kMaxC], rest = code;
-      for (int c = 0; c < C; ++c) {
-        const int q = s_div[cnt[c] + 1][rest];
-        d[c] = rest - q * (cnt[c] + 1);
-        rest = q;
-        e[c] = cnt[c] - d[c];
-      }
-      int sr;
-      ru[k] = lat_rank_tokens(L, cfg, d, C, &su[k]);
-      rr[k] = lat_rank_tokens(L, cfg, e, C, &sr);
+      const unsigned e = rk[code], ec = rk[M - 1 - code];
+      su[k] = (int)(e >> 24);
+      ru[k] = e & 0xFFFFFFu;
+      rr[k] = ec & 0xFFFFFFu;
     }
   }
   // S ascending; strict improvement (templates.py:322) -> smaller S on ties
@@ -1030,7 +1018,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
                     &h->lat_sub, &h->lat_maxn, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
-    h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release();
+    h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release(); h->ws_ranks[i].release();
     if (h->side[i]) cudaStreamDestroy(h->side[i]);
     if (h->side_ev[i]) cudaEventDestroy(h->side_ev[i]);
   }
@@ -1446,7 +1434,8 @@ static int lattice_prepare(coral_s1_handle* h) {
 
 // One (model, phase) chain on stream `slot`: lattice for every monotone S of the
 // chain, the exact per-candidate kernel for the others.
-static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss, int slot) {
+static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss, int slot,
+                         const unsigned* ranks) {
   cudaStream_t st = h->side[slot];
   const int m = mp / h->NP;
   const int K = h->K, Lu = h->Lu[m];
@@ -1513,6 +1502,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   T.subtab = h->lat_sub.as<uint2>();
   T.rec = h->rec.as<coral_s1_record>() + h->cand_off[mp];
   T.win = h->win.as<int4>() + h->cand_off[mp];
+  T.ranks = ranks;
   if (h->top_per_S) {  // one launch per S: working set value_S + f_S[S-1] stays in L2
     for (int S = 1; S <= Smax; ++S) {
       if (!((smask >> S) & 1u)) continue;
@@ -1562,21 +1552,36 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   CUDA_TRY(cudaStreamSynchronize(st));  // flags_h valid
   CUDA_TRY(cudaEventRecord(h->fork_ev, st));
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) CUDA_TRY(cudaStreamWaitEvent(h->side[i], h->fork_ev, 0));
-  // heaviest (model, phase) chains first, round-robin over the side streams
-  std::vector<int> order(NMP);
-  for (int i = 0; i < NMP; ++i) order[i] = i;
+  // one chain per model (its phases back to back on one stream, sharing the model's
+  // rank table), heaviest first, round-robin over the side streams
+  std::vector<int> order(h->NM);
+  for (int i = 0; i < h->NM; ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    const int ma = a / h->NP, mb = b / h->NP;
-    return (double)h->counts[ma] * h->Lu[ma] > (double)h->counts[mb] * h->Lu[mb];
+    return (double)h->counts[a] * h->Lu[a] > (double)h->counts[b] * h->Lu[b];
   });
+  int64_t maxc = 1;
+  for (int m = 0; m < h->NM; ++m) maxc = std::max<int64_t>(maxc, h->counts[m]);
+  for (int i = 0; i < h->nstreams; ++i)
+    if ((rc = h->ws_ranks[i].ensure(maxc * 64 * sizeof(unsigned)))) return rc;
   int slot = 0;
-  for (int mp : order) {
-    const int m = mp / h->NP;
-    std::vector<int> Ss;
-    for (int S = 1; S <= std::min(h->smax[m], h->Lu[m]); ++S)
-      if (take(mp, S)) Ss.push_back(S);
-    if (Ss.empty() || !h->counts[m]) continue;
-    if ((rc = lattice_units(h, mp, Ss, slot))) return rc;
+  for (int m : order) {
+    if (!h->counts[m]) continue;
+    std::vector<std::vector<int>> per_phase(h->NP);
+    bool any = false;
+    for (int p = 0; p < h->NP; ++p)
+      for (int S = 1; S <= std::min(h->smax[m], h->Lu[m]); ++S)
+        if (take(m * h->NP + p, S)) { per_phase[p].push_back(S); any = true; }
+    if (!any) continue;
+    unsigned* ranks = h->ws_ranks[slot].as<unsigned>();
+    if (h->n_max >= 2 && h->lat_states > 0) {
+      LatModel L{h->K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
+      lat_ranks_kernel<<<(unsigned)((h->counts[m] * 64 + 255) / 256), 256, 0, h->side[slot]>>>(
+          L, h->dp.inv_rank, h->keys.as<unsigned long long>() + h->koff[m], h->counts[m], ranks);
+      LAUNCH_CHECK(h);
+    }
+    for (int p = 0; p < h->NP; ++p)
+      if (!per_phase[p].empty() && (rc = lattice_units(h, m * h->NP + p, per_phase[p], slot, ranks)))
+        return rc;
     slot = (slot + 1) % h->nstreams;
   }
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {

@@ -154,6 +154,31 @@ __global__ void lat_maxn_closed_kernel(LatModel L, const int* __restrict__ inv_r
   maxn[idx] = best;
 }
 
+// Per candidate and u code: size(u) << 24 | idx(u) (0xFFFFFFFF past M, idx 0 when
+// |u| > R). The top cells read idx(full - u) as the entry of code M-1-code. Shared by
+// both phases of a model. One thread per (candidate, code).
+__global__ void lat_ranks_kernel(LatModel L, const int* __restrict__ inv_rank,
+                                 const unsigned long long* __restrict__ keys, long long ncombo,
+                                 unsigned* __restrict__ ranks) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long ci = t >> 6;
+  const int code = (int)(t & 63);
+  if (ci >= ncombo) return;
+  int cfg[kMaxC], cnt[kMaxC];
+  const int C = lat_tokens(inv_rank, keys[ci], cfg, cnt);
+  int M = 1;
+  for (int c = 0; c < C; ++c) M *= cnt[c] + 1;
+  unsigned out = 0xFFFFFFFFu;
+  if (code < M) {
+    int d[kMaxC], rest = code;
+    for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; }
+    int s;
+    const long long r = lat_rank_tokens(L, cfg, d, C, &s);
+    out = ((unsigned)s << 24) | (unsigned)(s >= 1 && s <= L.R ? r : 0);
+  }
+  ranks[t] = out;
+}
+
 // nsub[idx] = M(X) = prod(counts + 1)
 __global__ void lat_nsub_kernel(LatModel L, const unsigned long long* __restrict__ state_key,
                                 long long* __restrict__ nsub) {
