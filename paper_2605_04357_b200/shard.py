@@ -10,21 +10,21 @@ values of a chain together unless splitting balances better.
 
 Cost model (milliseconds on one B200, calibrated with tools/calibrate_units.py on
 BASELINE config 2, profiles/r01_calibration.txt):
-  fixed(chain)  = 0.12 + 3.2e-6 * candidates
-  unit(chain,S) = 6.6e-8 * candidates * layer_units * W[S]
+  fixed(chain)  = 0.09 + 1.4e-6 * candidates
+  unit(chain,S) = 6.8e-8 * candidates * layer_units * W[S]
 """
 
 from __future__ import annotations
 
-W = {1: 0.02, 2: 0.2, 3: 0.75, 4: 1.0, 5: 0.77, 6: 0.53}
+W = {1: 0.01, 2: 0.22, 3: 0.8, 4: 1.0, 5: 0.7, 6: 0.45}
 
 
 def chain_fixed(ncombo: int) -> float:
-    return 0.12 + 3.2e-6 * ncombo
+    return 0.09 + 1.4e-6 * ncombo
 
 
 def unit_cost(ncombo: int, lsteps: int, S: int) -> float:
-    return 6.6e-8 * ncombo * lsteps * W.get(S, 0.5) + 0.005
+    return 6.8e-8 * ncombo * lsteps * W.get(S, 0.5) + 0.005
 
 
 def assign_units(counts, lsteps, smax, num_phases: int, world: int) -> list:
