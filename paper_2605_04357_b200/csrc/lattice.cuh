@@ -282,23 +282,50 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
   const double* __restrict__ fprev = W.lay(S, sg - 1);
   double* __restrict__ fout = W.lay(S, sg);
   unsigned short* __restrict__ chout = W.chl(S, sg);
+  // u codes of X that pass the size filter (M(X) <= 2^5 = 32): one per lane, ballot
+  const int mycode = lane + 1;
+  uint2 myent = make_uint2(0u, 0u);
+  bool ok = false;
+  if (mycode < cmax) {
+    myent = subtab[o + mycode];
+    ok = (int)(myent.x >> 24) <= usz;
+  }
+  const unsigned vmask = __ballot_sync(0xffffffffu, ok);
+  const int nv = __popc(vmask);
   for (int l0 = sg; l0 <= lmax; l0 += 32) {
-    const int l = l0 + lane;
-    const bool act = l <= lmax;
+    // lanes = G groups x wp positions; group g takes valid codes g, g+G, g+2G, ...
+    const int w = min(32, lmax - l0 + 1);
+    int wp = 1;
+    while (wp < w) wp <<= 1;
+    const int G = 32 / wp;
+    const int g = lane / wp, i = lane - g * wp;
+    const int l = l0 + i;
+    const bool act = i < w;
     const int jmax = l - (sg - 1);
     double best = kNegInf;
-    int bu = 0, bj = 0;
-    for (int code = 1; code < cmax; ++code) {
-      const uint2 e = subtab[o + code];
-      if ((int)(e.x >> 24) > usz) continue;
-      if (!act) continue;
+    int bu = 1 << 20, bj = 0;
+    const int T = (nv + G - 1) / G;
+    for (int t = 0; t < T; ++t) {
+      const int kk = t * G + g;  // this group's kk-th valid code (ascending per group)
+      const int pos = kk < nv ? (int)__fns(vmask, 0, kk + 1) : 0;
+      const unsigned ex = __shfl_sync(0xffffffffu, myent.x, pos);
+      const unsigned ey = __shfl_sync(0xffffffffu, myent.y, pos);
+      if (!act || kk >= nv) continue;
       double cand;
       int cj;
-      dp_pair(value + (long long)(e.x & 0xFFFFFFu) * LuP, fprev + (long long)e.y * LuP, l, jmax, true,
+      dp_pair(value + (long long)(ex & 0xFFFFFFu) * LuP, fprev + (long long)ey * LuP, l, jmax, true,
               cand, cj);
-      if (cand > best) { best = cand; bu = code; bj = cj; }
+      if (cand > best) { best = cand; bu = pos + 1; bj = cj; }
     }
-    if (act) {
+    // merge the groups of each l: value desc, then smallest code (the reference's
+    // first strictly better u over the ascending code sequence)
+    for (int ofs = wp; ofs < 32; ofs <<= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, ofs);
+      const int ou = __shfl_xor_sync(0xffffffffu, bu, ofs);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, ofs);
+      if (ob > best || (ob == best && ou < bu)) { best = ob; bu = ou; bj = oj; }
+    }
+    if (act && g == 0) {
       fout[idx * LuP + l] = best;
       chout[idx * LuP + l] = (unsigned short)((bu << 10) | bj);
     }
