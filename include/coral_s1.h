@@ -209,6 +209,13 @@ int coral_s1_write_library(coral_s1_handle* h, const char* path, const char* hea
 int coral_s1_sweep(coral_s1_handle* h, int ncaps, const int32_t* n_max, const double* rho,
                    int num_regions, const double* prices, uint32_t phase_mask, int64_t* counts,
                    double* best);
+/* ---- T-hat queries (simulator reuse): node_max_throughput
+ * (perf.py:159-175, use_profile != 0) or planned_batch_and_tput (perf.py:186-230) for
+ * n (config, model, phase code, j layers, budget s) against the current problem's
+ * spec tables; host buffers. */
+int coral_s1_node_queries(coral_s1_handle* h, int64_t n, const int32_t* cfg, const int32_t* model,
+                          const int32_t* phase, const int32_t* j, const double* budget, int use_profile,
+                          double* tput, int64_t* batch);
 /* CPython repr(float) of v into out (cap >= 40); host-only helper, no device needed */
 int coral_s1_format_double(double v, char* out, int cap);
 

@@ -10,6 +10,8 @@ from .frontier import FrontierEntry, FrontierSession, TemplateFrontier, build_fr
 from .kernels import NEG_INF, placement_search, placement_search_batch
 from .library import (GenContext, LibraryCaps, LibraryGenError, Stage1Problem, TemplateLibrary,
                       build_library, enumerate_combos, stage_budget_s, throughput_table)
+from .roofline import (node_max_throughput, planned_batch, planned_batch_and_tput,
+                       recompute_throughput, stage_node_weights)
 from .specs import (DECODE, PHASES, PREFILL, DomainError, GpuSpec, MarketState, ModelSpec,
                     NodeComboKey, NodeConfig, PerfParams, Placement, ProfileTable, Region,
                     ServingTemplate, SloSpec, combo_key, template_cost)

@@ -108,6 +108,8 @@ def load():
                                                  C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
                                                  C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), _i64p]),
             "coral_s1_format_double": (C.c_int, [C.c_double, C.c_char_p, C.c_int]),
+            "coral_s1_node_queries": (C.c_int, [vp, C.c_int64, _i32p, _i32p, _i32p, _i32p, _f64p, C.c_int,
+                                                _f64p, _i64p]),
             "coral_s1_sweep": (C.c_int, [vp, C.c_int, _i32p, _f64p, C.c_int, _f64p, C.c_uint32, _i64p,
                                          _f64p]),
         }
@@ -341,6 +343,17 @@ class Handle:
                                         prices.shape[0], _ptr(prices, C.c_double), phase_mask,
                                         _ptr(counts, C.c_int64), _ptr(best, C.c_double)))
         return counts[:len(n_max)], best[:len(n_max)]
+
+    def node_queries(self, cfg, model, phase, j, budget, use_profile: bool):
+        a = [np.ascontiguousarray(x, dtype=np.int32) for x in (cfg, model, phase, j)]
+        bud = np.ascontiguousarray(budget, dtype=np.float64)
+        n = len(bud)
+        tput = np.zeros(max(n, 1))
+        batch = np.zeros(max(n, 1), dtype=np.int64)
+        _check(self._lib.coral_s1_node_queries(self._h, n, *[_ptr(x, C.c_int32) for x in a],
+                                               _ptr(bud, C.c_double), int(use_profile),
+                                               _ptr(tput, C.c_double), _ptr(batch, C.c_int64)))
+        return tput[:n], batch[:n]
 
     def stage_ms(self) -> dict:
         vals = [C.c_double() for _ in range(4)]

@@ -812,6 +812,23 @@ __global__ void sweep_kernel(FrontArgs A, int ncaps, const int* __restrict__ cap
   }
 }
 
+// Batched T-hat queries (perf.py:159-230) against the current spec tables: the
+// simulator-side reuse of the roofline model.
+__global__ void node_query_kernel(DevProblem P, int64_t n, const int* __restrict__ cfg,
+                                  const int* __restrict__ model, const int* __restrict__ phase,
+                                  const int* __restrict__ j, const double* __restrict__ budget,
+                                  int use_profile, double* __restrict__ tput, long long* __restrict__ batch) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long long b = 0;
+  double t;
+  double hit;
+  if (use_profile && profile_lookup(P, cfg[i], model[i], phase[i], j[i], budget[i], &hit)) t = hit;
+  else t = planned_batch_and_tput(P, cfg[i], model[i], phase[i], j[i], budget[i], &b);
+  tput[i] = t;
+  batch[i] = b;
+}
+
 // sort-key extraction for the 4 stable LSD passes
 __global__ void sortkey_kernel(const coral_s1_frontier_item* __restrict__ items,
                                const unsigned* __restrict__ perm, int64_t n, int field, int R,
@@ -1850,6 +1867,41 @@ int coral_s1_sweep(coral_s1_handle* h, int ncaps, const int32_t* n_max, const do
   }
   capn.release();
   caprho.release();
+  out.release();
+  return 0;
+}
+
+int coral_s1_node_queries(coral_s1_handle* h, int64_t n, const int32_t* cfg, const int32_t* model,
+                          const int32_t* phase, const int32_t* j, const double* budget, int use_profile,
+                          double* tput, int64_t* batch) {
+  if (!h || !h->have_problem) return fail(CORAL_S1_EINVAL, "set_problem first");
+  if (n <= 0) return 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (cfg[i] < 0 || cfg[i] >= h->K || model[i] < 0 || model[i] >= h->NM || j[i] < 1 || !(budget[i] > 0) ||
+        (phase[i] != CORAL_S1_PHASE_PREFILL && phase[i] != CORAL_S1_PHASE_DECODE))
+      return fail(CORAL_S1_EINVAL, "node query out of range (perf.py:189 asserts budget > 0, j >= 1)");
+  }
+  CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  DevBuf in, out;
+  const size_t bi = (size_t)n * 4;
+  int rc;
+  if ((rc = in.ensure(4 * ((bi + 15) & ~15ull) + n * 8)) || (rc = out.ensure(n * 16))) return rc;
+  auto* b = in.as<unsigned char>();
+  const size_t step = (bi + 15) & ~15ull;
+  CUDA_TRY(cudaMemcpyAsync(b, cfg, bi, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(b + step, model, bi, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(b + 2 * step, phase, bi, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(b + 3 * step, j, bi, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(b + 4 * step, budget, n * 8, cudaMemcpyHostToDevice, st));
+  node_query_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+      h->dp, n, (const int*)b, (const int*)(b + step), (const int*)(b + 2 * step), (const int*)(b + 3 * step),
+      (const double*)(b + 4 * step), use_profile, out.as<double>(), (long long*)(out.as<double>() + n));
+  LAUNCH_CHECK(h);
+  CUDA_TRY(cudaMemcpyAsync(tput, out.p, n * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(batch, out.as<double>() + n, n * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  in.release();
   out.release();
   return 0;
 }

@@ -98,12 +98,11 @@ struct NodeModel {
   }
 };
 
-// perf.py:159-175 node_max_throughput -> perf.py:186-230 planned_batch_and_tput.
+// perf.py:186-230 planned_batch_and_tput: returns the throughput, *b_out the batch.
 // j is in layers (jj * granularity), budget > 0.
-__device__ double node_max_throughput(const DevProblem& P, int c, int m, int phase, int j,
-                                      double budget) {
-  double hit;
-  if (profile_lookup(P, c, m, phase, j, budget, &hit)) return hit;
+__device__ double planned_batch_and_tput(const DevProblem& P, int c, int m, int phase, int j,
+                                         double budget, long long* b_out) {
+  *b_out = 0;
   const double gcd = (double)P.gc[c];
   const double Ld = (double)P.L[m];
   NodeModel nm;
@@ -153,7 +152,17 @@ __device__ double node_max_throughput(const DevProblem& P, int c, int m, int pha
   while (b >= 1 && nm.iter_t(b) > lim) --b;
   while (b < b_mem && nm.iter_t(b + 1) <= lim) ++b;
   if (b < 1) return 0.0;
+  *b_out = b;
   return rn_div(rn_mul((double)b, nm.tpr), nm.iter_t(b));
+}
+
+// perf.py:159-175 node_max_throughput: a profile hit wins verbatim.
+__device__ double node_max_throughput(const DevProblem& P, int c, int m, int phase, int j,
+                                      double budget) {
+  double hit;
+  if (profile_lookup(P, c, m, phase, j, budget, &hit)) return hit;
+  long long b;
+  return planned_batch_and_tput(P, c, m, phase, j, budget, &b);
 }
 
 }  // namespace coral

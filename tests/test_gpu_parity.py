@@ -384,3 +384,36 @@ def test_native_materialise_equals_python():
                  e.template.slo, e.template.combo, e.price_usd_h) for k, v in f.segments.items() for e in v]
     assert rows(a) == rows(b)
     assert len(a) == 2225
+
+
+def test_roofline_operators_match_reference_grid():
+    """node_max_throughput on the device == the reference's perf.py values on the
+    golden grid (nodes x models x phases x j x budgets, two PerfParams), one batch."""
+    from paper_2605_04357_b200 import catalog
+    from paper_2605_04357_b200.roofline import node_queries, planned_batch_and_tput
+    from paper_2605_04357_b200.specs import ModelSpec, NodeConfig, PerfParams
+    params = [PerfParams(), PerfParams(mfu=0.3, mbu=0.9, fixed_overhead_ms=0.0,
+                                       avg_prompt_tokens=333.3, avg_ctx_tokens=777.7)]
+    models = dict(catalog.MODEL_CATALOG)
+    models["tiny"] = ModelSpec("tiny", 4, 0.5, 0.5, 256, kv_bytes_per_token_per_layer=128.0)
+    grid = golden("perf_grid.json.gz")
+    for pi, p in enumerate(params):
+        rows = [e for e in grid if e["p"] == pi]
+        qs = [(NodeConfig(catalog.GPU_CATALOG[e["gpu"]], e["gc"]), models[e["model"]], e["phase"], e["j"],
+               e["budget"]) for e in rows]
+        got, _ = node_queries(qs, p)
+        assert got == [e["tput"] for e in rows]
+    b, t = planned_batch_and_tput(NodeConfig(catalog.GPU_CATALOG["H100"], 2), models["llama3-70b"],
+                                  "decode", 40, 0.05, params[0])
+    assert b > 0 and t > 0
+
+
+def test_recompute_throughput_invariant():
+    """templates.py:267-280 recomputed from the placement equals the template value
+    (test_templates.py:151-155 invariant, exact here)."""
+    from paper_2605_04357_b200.roofline import recompute_throughput
+    configs, models, slos, caps, ctx, regions, prices = workload("c1")
+    lib = build_library(configs, models, slos, caps, ctx)
+    m = models[0]
+    for t in lib.entries[::5]:
+        assert recompute_throughput(t, m, ctx) == t.throughput_tps
