@@ -12,8 +12,8 @@ from .library import (GenContext, LibraryCaps, LibraryGenError, Stage1Problem, T
                       build_library, enumerate_combos, stage_budget_s, throughput_table)
 from .roofline import (node_max_throughput, planned_batch, planned_batch_and_tput,
                        recompute_throughput, stage_node_weights)
-from .specs import (DECODE, PHASES, PREFILL, DomainError, GpuSpec, MarketState, ModelSpec,
-                    NodeComboKey, NodeConfig, PerfParams, Placement, ProfileTable, Region,
-                    ServingTemplate, SloSpec, combo_key, template_cost)
+from .specs import (DECODE, PHASES, PREFILL, DomainError, GpuSpec, ModelSpec, NodeComboKey,
+                    NodeConfig, PerfParams, Placement, ProfileTable, Region, ServingTemplate,
+                    SloSpec, combo_key)
 
 __version__ = "0.1.0"
