@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--workload", default=WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--c5", action="store_true", help="also time BASELINE config 5 (seconds)")
     return ap.parse_args()
 
 
@@ -165,6 +166,49 @@ def top_kernel_bytes(counts, lsteps, smax, masks, K, n_max):
             continue
         total += int(counts[m]) * 72 + nS2 * 2 * states * (int(lsteps[m]) + 1) * 8
     return total
+
+
+def other_configs(args, h_main):
+    """Device time of one stage-1 solve of BASELINE configs 3 (and 5 with --c5), and of
+    a config-4 epoch re-pricing from cached records (frontier only). Parity cases, not
+    the headline."""
+    import torch
+    from paper_2605_04357_b200 import FrontierSession, catalog
+    from paper_2605_04357_b200.frontier import _price_matrix
+    from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem
+    out = {}
+    names = ["c3"] + (["c5"] if args.c5 else [])
+    for name in names:
+        w = catalog.WORKLOADS[name]()
+        prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho),
+                             GenContext(perf=w.perf, granularity=w.granularity))
+        _, pm = _price_matrix(prob.configs, w.prices, w.regions)
+        times = []
+        for i in range(2):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            prob.run()
+            n = prob.h.frontier(pm)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        out[name] = {"candidates": prob.num_candidates, "frontier_survivors": int(n),
+                     "stage1_ms": times[-1], "candidates_per_s": prob.num_candidates / (times[-1] / 1e3)}
+    w = catalog.extended_workload()
+    sess = FrontierSession(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf))
+    ts = []
+    for epoch in range(1, 6):
+        prices = catalog.c4_epoch_prices(w, epoch)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        f = sess.frontier(prices, regions=w.regions)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    out["c4_reprice"] = {"epochs": len(ts), "ms_per_epoch": 1e3 * sum(ts[1:]) / (len(ts) - 1),
+                         "frontier_survivors_last": len(f), "note": "cached records, frontier only, host API"}
+    del h_main
+    return out
 
 
 def measured_peaks():
@@ -346,6 +390,8 @@ def main():
                      "note": "fp64 max-min DP over L2-resident lattice tables: latency-bound on dependent "
                              "L2 loads, not HBM bandwidth (DESIGN.md 5)"},
     }
+    if world == 1:
+        line["other_configs"] = other_configs(args, h)
     if rank == 0:
         line["clocks"] = clk.summary()
         if world == 1 and not args.no_cpu_baseline:
