@@ -126,7 +126,271 @@ fail:
   return NULL;
 }
 
-static PyMethodDef methods[] = {{"materialise", materialise, METH_VARARGS, NULL}, {NULL, NULL, 0, NULL}};
+/* ---------------------------------------------------------------------------------
+ * load_library(path, configs: dict name -> NodeConfig, ServingTemplate, Placement,
+ *              NodeComboKey, SloSpec) -> (header_line: str, entries: list, sorted: bool)
+ *
+ * TemplateLibrary.load (templates.py:379-401) for the JSON-lines format written by
+ * TemplateLibrary.save: one json.dumps(record) per line. A small parser for JSON
+ * values: numbers become int or float exactly as json.loads types them (floats via
+ * strtod, correctly rounded like float()); strings with escapes go through json.loads.
+ * Combo and placement objects are shared between records with identical text.
+ * `sorted` reports whether the entries are already in (model, phase, str(combo))
+ * order, so the caller can skip TemplateLibrary's re-sort.
+ * ------------------------------------------------------------------------------- */
+typedef struct { const char* p; const char* end; } Cur;
+
+static void ws(Cur* c) { while (c->p < c->end && (*c->p == ' ' || *c->p == '\t' || *c->p == '\r')) ++c->p; }
+
+static PyObject* parse_value(Cur* c);
+
+static PyObject* parse_string(Cur* c) {
+  if (c->p >= c->end || *c->p != '"') { PyErr_SetString(PyExc_ValueError, "expected string"); return NULL; }
+  const char* s = ++c->p;
+  int esc = 0;
+  while (c->p < c->end && *c->p != '"') {
+    if (*c->p == '\\') { esc = 1; ++c->p; }
+    ++c->p;
+  }
+  if (c->p >= c->end) { PyErr_SetString(PyExc_ValueError, "unterminated string"); return NULL; }
+  const char* e = c->p++;
+  if (!esc) return PyUnicode_DecodeUTF8(s, e - s, "strict");
+  PyObject* json = PyImport_ImportModule("json");
+  if (!json) return NULL;
+  PyObject* raw = PyUnicode_FromStringAndSize(s - 1, e - s + 2);
+  PyObject* out = raw ? PyObject_CallMethod(json, "loads", "O", raw) : NULL;
+  Py_XDECREF(raw);
+  Py_DECREF(json);
+  return out;
+}
+
+static PyObject* parse_number(Cur* c) {
+  const char* s = c->p;
+  int isf = 0;
+  while (c->p < c->end && strchr("+-0123456789.eE", *c->p)) {
+    if (*c->p == '.' || *c->p == 'e' || *c->p == 'E') isf = 1;
+    ++c->p;
+  }
+  char buf[64];
+  const size_t n = (size_t)(c->p - s);
+  if (n == 0 || n >= sizeof(buf)) { PyErr_SetString(PyExc_ValueError, "bad number"); return NULL; }
+  memcpy(buf, s, n);
+  buf[n] = 0;
+  if (isf) return PyFloat_FromDouble(strtod(buf, NULL));
+  return PyLong_FromString(buf, NULL, 10);
+}
+
+static PyObject* parse_array(Cur* c) {
+  ++c->p; /* [ */
+  PyObject* lst = PyList_New(0);
+  ws(c);
+  if (c->p < c->end && *c->p == ']') { ++c->p; return lst; }
+  for (;;) {
+    ws(c);
+    PyObject* v = parse_value(c);
+    if (!v) { Py_DECREF(lst); return NULL; }
+    PyList_Append(lst, v);
+    Py_DECREF(v);
+    ws(c);
+    if (c->p < c->end && *c->p == ',') { ++c->p; continue; }
+    if (c->p < c->end && *c->p == ']') { ++c->p; return lst; }
+    Py_DECREF(lst);
+    PyErr_SetString(PyExc_ValueError, "bad array");
+    return NULL;
+  }
+}
+
+static PyObject* parse_value(Cur* c) {
+  ws(c);
+  if (c->p >= c->end) { PyErr_SetString(PyExc_ValueError, "unexpected end"); return NULL; }
+  const char ch = *c->p;
+  if (ch == '"') return parse_string(c);
+  if (ch == '[') return parse_array(c);
+  if (ch == '{') {  /* generic object (unused keys): fall back to json.loads of the span */
+    int depth = 0, instr = 0;
+    const char* s = c->p;
+    for (; c->p < c->end; ++c->p) {
+      if (instr) { if (*c->p == '\\') ++c->p; else if (*c->p == '"') instr = 0; continue; }
+      if (*c->p == '"') instr = 1;
+      else if (*c->p == '{') ++depth;
+      else if (*c->p == '}' && --depth == 0) { ++c->p; break; }
+    }
+    PyObject* json = PyImport_ImportModule("json");
+    PyObject* raw = PyUnicode_FromStringAndSize(s, c->p - s);
+    PyObject* out = PyObject_CallMethod(json, "loads", "O", raw);
+    Py_XDECREF(raw);
+    Py_XDECREF(json);
+    return out;
+  }
+  if (!strncmp(c->p, "true", 4)) { c->p += 4; Py_RETURN_TRUE; }
+  if (!strncmp(c->p, "false", 5)) { c->p += 5; Py_RETURN_FALSE; }
+  if (!strncmp(c->p, "null", 4)) { c->p += 4; Py_RETURN_NONE; }
+  return parse_number(c);
+}
+
+static PyObject* tuple_of(PyObject* lst) { return PyList_AsTuple(lst); }
+
+static PyObject* load_library(PyObject* self, PyObject* args) {
+  const char* path;
+  PyObject *cfgs, *T_tmpl, *T_pl, *T_combo, *T_slo;
+  if (!PyArg_ParseTuple(args, "sOOOOO", &path, &cfgs, &T_tmpl, &T_pl, &T_combo, &T_slo)) return NULL;
+  FILE* f = fopen(path, "rb");
+  if (!f) return PyErr_SetFromErrnoWithFilename(PyExc_OSError, path);
+  fseek(f, 0, SEEK_END);
+  const long size = ftell(f);
+  fseek(f, 0, SEEK_SET);
+  char* data = (char*)PyMem_Malloc((size_t)size + 1);
+  if (!data) { fclose(f); return PyErr_NoMemory(); }
+  const size_t got = fread(data, 1, (size_t)size, f);
+  fclose(f);
+  data[got] = 0;
+  const char* p = data;
+  const char* end = data + got;
+  const char* nl = memchr(p, '\n', (size_t)(end - p));
+  if (!nl) nl = end;
+  PyObject* header = PyUnicode_DecodeUTF8(p, nl - p, "strict");
+  PyObject* entries = PyList_New(0);
+  PyObject* combos = PyDict_New();   /* raw combo text -> NodeComboKey */
+  PyObject* slos = PyDict_New();     /* raw slo text -> SloSpec */
+  PyObject *prev_key = NULL;
+  int sorted = 1;
+  if (!header || !entries || !combos || !slos) goto fail;
+  p = nl < end ? nl + 1 : end;
+  while (p < end) {
+    const char* le = memchr(p, '\n', (size_t)(end - p));
+    if (!le) le = end;
+    Cur c = {p, le};
+    ws(&c);
+    if (c.p >= le) { p = le + 1; continue; }
+    if (*c.p != '{') { PyErr_SetString(PyExc_ValueError, "record is not an object"); goto fail; }
+    ++c.p;
+    PyObject *model = NULL, *phase = NULL, *slo = NULL, *combo = NULL, *layers = NULL, *son = NULL,
+             *nst = NULL, *tps = NULL;
+    PyObject* combo_str = NULL;
+    for (;;) {
+      ws(&c);
+      if (c.p < le && *c.p == '}') { ++c.p; break; }
+      PyObject* key = parse_string(&c);
+      if (!key) goto fail;
+      ws(&c);
+      if (c.p >= le || *c.p != ':') { Py_DECREF(key); PyErr_SetString(PyExc_ValueError, "expected ':'"); goto fail; }
+      ++c.p;
+      ws(&c);
+      const char* vstart = c.p;
+      const char* k = PyUnicode_AsUTF8(key);
+      PyObject* v = NULL;
+      if (!strcmp(k, "combo") || !strcmp(k, "slo")) {
+        /* share objects between identical texts */
+        v = parse_value(&c);
+        if (!v) { Py_DECREF(key); goto fail; }
+        PyObject* raw = PyUnicode_DecodeUTF8(vstart, c.p - vstart, "strict");
+        PyObject* cache = !strcmp(k, "combo") ? combos : slos;
+        PyObject* obj = PyDict_GetItem(cache, raw);
+        if (obj) Py_INCREF(obj);
+        else if (!strcmp(k, "combo")) {
+          const Py_ssize_t nt = PyList_GET_SIZE(v);
+          PyObject* items = PyTuple_New(nt);
+          PyObject* parts = PyList_New(nt);
+          for (Py_ssize_t t = 0; t < nt; ++t) {
+            PyObject* pair = PyList_GET_ITEM(v, t);
+            PyObject* name = PyList_GetItem(pair, 0);
+            PyObject* cnt = PyList_GetItem(pair, 1);
+            PyObject* cfg = name ? PyDict_GetItem(cfgs, name) : NULL;
+            if (!cfg || !cnt) { PyErr_Format(PyExc_KeyError, "unknown config in %s", path); goto fail; }
+            Py_INCREF(cfg);
+            PyObject* cnt_int = PyNumber_Long(cnt);
+            PyTuple_SET_ITEM(items, t, PyTuple_Pack(2, cfg, cnt_int));
+            Py_DECREF(cfg);
+            PyList_SET_ITEM(parts, t, PyUnicode_FromFormat("%U*%S", name, cnt_int));
+            Py_DECREF(cnt_int);
+          }
+          /* cache entry: (NodeComboKey, str(combo)) -- the str is the sort key */
+          PyObject* d;
+          PyObject* ck = new_with_dict((PyTypeObject*)T_combo, &d);
+          set(d, s_items, items);
+          Py_DECREF(d);
+          PyObject* sep = PyUnicode_FromString("+");
+          PyObject* str = PyUnicode_Join(sep, parts);
+          Py_DECREF(sep);
+          Py_DECREF(parts);
+          obj = PyTuple_Pack(2, ck, str);
+          Py_DECREF(ck);
+          Py_DECREF(str);
+          PyDict_SetItem(cache, raw, obj);
+        } else {
+          PyObject* argt = PyList_AsTuple(v);
+          obj = PyObject_CallObject(T_slo, argt);
+          Py_XDECREF(argt);
+          if (!obj) { Py_DECREF(raw); Py_DECREF(v); Py_DECREF(key); goto fail; }
+          PyDict_SetItem(cache, raw, obj);
+        }
+        Py_DECREF(raw);
+        Py_DECREF(v);
+        v = obj;
+      } else {
+        v = parse_value(&c);
+      }
+      if (!v) { Py_DECREF(key); goto fail; }
+      if (!strcmp(k, "model")) model = v;
+      else if (!strcmp(k, "phase")) phase = v;
+      else if (!strcmp(k, "slo")) slo = v;
+      else if (!strcmp(k, "combo")) { combo = PyTuple_GET_ITEM(v, 0); combo_str = PyTuple_GET_ITEM(v, 1);
+                                      Py_INCREF(combo); Py_INCREF(combo_str); Py_DECREF(v); }
+      else if (!strcmp(k, "layers_per_stage")) { layers = tuple_of(v); Py_DECREF(v); }
+      else if (!strcmp(k, "stage_of_node")) { son = tuple_of(v); Py_DECREF(v); }
+      else if (!strcmp(k, "num_stages")) nst = v;
+      else if (!strcmp(k, "throughput_tps")) { tps = PyNumber_Float(v); Py_DECREF(v); }
+      else Py_DECREF(v);
+      Py_DECREF(key);
+      ws(&c);
+      if (c.p < le && *c.p == ',') ++c.p;
+    }
+    if (!model || !phase || !slo || !combo || !layers || !son || !nst || !tps) {
+      PyErr_SetString(PyExc_KeyError, "record misses a field");
+      goto fail;
+    }
+    PyObject *dp, *dt;
+    PyObject* pl = new_with_dict((PyTypeObject*)T_pl, &dp);
+    set(dp, s_num_stages, nst);
+    set(dp, s_layers, layers);
+    set(dp, s_son, son);
+    Py_DECREF(dp);
+    PyObject* key3 = PyTuple_Pack(3, model, phase, combo_str);
+    if (prev_key && sorted && PyObject_RichCompareBool(prev_key, key3, Py_GT) == 1) sorted = 0;
+    Py_XDECREF(prev_key);
+    prev_key = key3;
+    Py_DECREF(combo_str);
+    PyObject* t = new_with_dict((PyTypeObject*)T_tmpl, &dt);
+    set(dt, s_model, model);
+    set(dt, s_phase, phase);
+    set(dt, s_slo, slo);
+    set(dt, s_combo, combo);
+    set(dt, s_placement, pl);
+    set(dt, s_tps, tps);
+    Py_DECREF(dt);
+    PyList_Append(entries, t);
+    Py_DECREF(t);
+    p = le + 1;
+  }
+  Py_XDECREF(prev_key);
+  Py_DECREF(combos);
+  Py_DECREF(slos);
+  PyMem_Free(data);
+  return Py_BuildValue("(NNO)", header, entries, sorted ? Py_True : Py_False);
+fail:
+  Py_XDECREF(prev_key);
+  Py_XDECREF(header);
+  Py_XDECREF(entries);
+  Py_XDECREF(combos);
+  Py_XDECREF(slos);
+  PyMem_Free(data);
+  if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "malformed template library");
+  return NULL;
+}
+
+static PyMethodDef methods[] = {{"materialise", materialise, METH_VARARGS, NULL},
+                                {"load_library", load_library, METH_VARARGS, NULL},
+                                {NULL, NULL, 0, NULL}};
 static struct PyModuleDef mod = {PyModuleDef_HEAD_INIT, "_materialize", NULL, -1, methods};
 
 PyMODINIT_FUNC PyInit__materialize(void) {

@@ -149,7 +149,9 @@ def materialise(prob: Stage1Problem, items: np.ndarray, region_names, meta) -> T
     """Survivor records -> ServingTemplate objects (one per (mp, combo)), built by the
     CPython extension _lib/_materialize (csrc/materialize.c)."""
     from ._lib import _materialize
-    segments = _materialise_native(_materialize, prob, items, region_names)
+    from .library import _no_gc
+    with _no_gc():
+        segments = _materialise_native(_materialize, prob, items, region_names)
     return TemplateFrontier(segments=segments, meta=meta,
                             num_candidates=int(prob.cand_off[-1]) if prob.cand_off is not None else 0)
 

@@ -27,6 +27,21 @@ LIBRARY_VERSION = 1
 NEG_INF = _native.NEG_INF
 
 
+class _no_gc:
+    """Pause the cyclic GC while building many small immutable objects (the collector
+    otherwise re-traverses the growing young generation hundreds of times)."""
+
+    def __enter__(self):
+        import gc
+        self._was = gc.isenabled()
+        gc.disable()
+
+    def __exit__(self, *exc):
+        import gc
+        if self._was:
+            gc.enable()
+
+
 class LibraryGenError(RuntimeError):
     """A (model, phase) pair yielded no feasible template at all (templates.py:34-35)."""
 
@@ -219,6 +234,10 @@ class Stage1Problem:
 
     def library_entries(self):
         """All feasible templates in TemplateLibrary order (templates.py:340)."""
+        with _no_gc():
+            return self._library_entries()
+
+    def _library_entries(self):
         NP = len(self.phases)
         nmp = len(self.models) * NP
         recs_by_mp = [self.records(mp) for mp in range(nmp)]
@@ -360,6 +379,22 @@ class TemplateLibrary:
 
     @classmethod
     def load(cls, path: str) -> "TemplateLibrary":
+        """Read a library written by save (templates.py:379-401). The JSON-lines parse
+        and object construction run in the CPython extension (csrc/materialize.c)."""
+        from ._lib import _materialize
+        with open(path) as fh:
+            header = json.loads(fh.readline())
+        if header.get("format") != LIBRARY_FORMAT:
+            raise DomainError(f"{path} is not a template library file")
+        configs = {name: _config_from_meta(spec) for name, spec in header["configs"].items()}
+        with _no_gc():
+            _, entries, in_order = _materialize.load_library(path, configs, ServingTemplate, Placement,
+                                                             NodeComboKey, SloSpec)
+        return cls(entries=entries, meta=header, _presorted=bool(in_order))
+
+    @classmethod
+    def load_py(cls, path: str) -> "TemplateLibrary":
+        """Pure-Python twin of load (the reference's loop), kept for the tests."""
         with open(path) as fh:
             header = json.loads(fh.readline())
             if header.get("format") != LIBRARY_FORMAT:

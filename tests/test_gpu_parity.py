@@ -417,3 +417,25 @@ def test_recompute_throughput_invariant():
     m = models[0]
     for t in lib.entries[::5]:
         assert recompute_throughput(t, m, ctx) == t.throughput_tps
+
+
+def test_native_load_round_trip_extended(tmp_path):
+    """TemplateLibrary.load of the full config-2 file (285.7 MB): the same objects as
+    the reference-style Python loop on a sample, and a byte-identical re-save."""
+    import hashlib
+    import time
+    from paper_2605_04357_b200 import TemplateLibrary
+    ref = golden("saved_libraries.json.gz")["extended"]
+    configs, models, slos, caps, ctx, regions, prices = workload("extended")
+    path = str(tmp_path / "lib.jsonl")
+    build_library(configs, models, slos, caps, ctx, lazy=True).save(path)
+    t0 = time.perf_counter()
+    lib = TemplateLibrary.load(path)
+    dt = time.perf_counter() - t0
+    assert len(lib) == 1084362
+    lines = [template_line(t) for t in lib.entries]
+    assert lines[::97] == golden("library_extended.json.gz")["sample"]
+    out = str(tmp_path / "again.jsonl")
+    lib.save(out)
+    assert hashlib.sha256(open(out, "rb").read()).hexdigest() == ref["sha256"]
+    print(f"native load of {len(lib)} templates: {dt:.2f}s")
