@@ -126,6 +126,82 @@ fail:
   return NULL;
 }
 
+/* build_templates(records: bytes of coral_s1_record, keys: bytes of u64 (same count),
+ *                 cfg_by_rank: list, model: str, phase: str, slo, combo_cache: dict,
+ *                 ServingTemplate, Placement, NodeComboKey) -> list
+ * The feasible records of one (model, phase) as ServingTemplates in record order;
+ * combo objects are shared through combo_cache (key -> NodeComboKey) across phases. */
+static PyObject* build_templates(PyObject* self, PyObject* args) {
+  Py_buffer rb, kb;
+  PyObject *cfgs, *model, *phase, *slo, *cache, *T_tmpl, *T_pl, *T_combo;
+  if (!PyArg_ParseTuple(args, "y*y*OOOOOOOO", &rb, &kb, &cfgs, &model, &phase, &slo, &cache, &T_tmpl,
+                        &T_pl, &T_combo))
+    return NULL;
+  const coral_s1_record* rec = (const coral_s1_record*)rb.buf;
+  const uint64_t* keys = (const uint64_t*)kb.buf;
+  const Py_ssize_t n = rb.len / (Py_ssize_t)sizeof(coral_s1_record);
+  PyObject* out = PyList_New(0);
+  if (!out || kb.len / 8 < n) goto fail;
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    const coral_s1_record* r = &rec[i];
+    if (!r->num_stages) continue;
+    PyObject* kk = PyLong_FromUnsignedLongLong(keys[i]);
+    PyObject* combo = PyDict_GetItem(cache, kk);
+    if (combo) Py_INCREF(combo);
+    else {
+      int ntok = 0;
+      for (int k = 0; k < CORAL_S1_MAX_NODES; ++k)
+        if ((keys[i] >> (9 * (CORAL_S1_MAX_NODES - 1 - k))) & 511u) ++ntok;
+      PyObject* items = PyTuple_New(ntok);
+      for (int k = 0; k < ntok; ++k) {
+        const unsigned tok = (unsigned)(keys[i] >> (9 * (CORAL_S1_MAX_NODES - 1 - k))) & 511u;
+        PyObject* cfg = PyList_GetItem(cfgs, (Py_ssize_t)((tok >> 3) - 1));
+        Py_INCREF(cfg);
+        PyTuple_SET_ITEM(items, k, Py_BuildValue("(Ni)", cfg, (int)(tok & 7u)));
+      }
+      PyObject* dc;
+      combo = new_with_dict((PyTypeObject*)T_combo, &dc);
+      set(dc, s_items, items);
+      Py_DECREF(dc);
+      PyDict_SetItem(cache, kk, combo);
+    }
+    Py_DECREF(kk);
+    const int S = r->num_stages, nn = r->num_nodes;
+    PyObject* layers = PyTuple_New(S);
+    for (int s2 = 0; s2 < S; ++s2) PyTuple_SET_ITEM(layers, s2, PyLong_FromLong(r->layers_per_stage[s2]));
+    PyObject* son = PyTuple_New(nn);
+    for (int k = 0; k < nn; ++k) PyTuple_SET_ITEM(son, k, PyLong_FromLong(r->stage_of_node[k]));
+    PyObject *dp, *dt;
+    PyObject* pl = new_with_dict((PyTypeObject*)T_pl, &dp);
+    set(dp, s_num_stages, PyLong_FromLong(S));
+    set(dp, s_layers, layers);
+    set(dp, s_son, son);
+    Py_DECREF(dp);
+    PyObject* t = new_with_dict((PyTypeObject*)T_tmpl, &dt);
+    Py_INCREF(model);
+    Py_INCREF(phase);
+    Py_INCREF(slo);
+    set(dt, s_model, model);
+    set(dt, s_phase, phase);
+    set(dt, s_slo, slo);
+    set(dt, s_combo, combo);
+    set(dt, s_placement, pl);
+    set(dt, s_tps, PyFloat_FromDouble(r->throughput_tps));
+    Py_DECREF(dt);
+    PyList_Append(out, t);
+    Py_DECREF(t);
+  }
+  PyBuffer_Release(&rb);
+  PyBuffer_Release(&kb);
+  return out;
+fail:
+  Py_XDECREF(out);
+  PyBuffer_Release(&rb);
+  PyBuffer_Release(&kb);
+  if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "records/keys size mismatch");
+  return NULL;
+}
+
 /* ---------------------------------------------------------------------------------
  * load_library(path, configs: dict name -> NodeConfig, ServingTemplate, Placement,
  *              NodeComboKey, SloSpec) -> (header_line: str, entries: list, sorted: bool)
@@ -390,6 +466,7 @@ fail:
 
 static PyMethodDef methods[] = {{"materialise", materialise, METH_VARARGS, NULL},
                                 {"load_library", load_library, METH_VARARGS, NULL},
+                                {"build_templates", build_templates, METH_VARARGS, NULL},
                                 {NULL, NULL, 0, NULL}};
 static struct PyModuleDef mod = {PyModuleDef_HEAD_INIT, "_materialize", NULL, -1, methods};
 

@@ -238,6 +238,7 @@ class Stage1Problem:
             return self._library_entries()
 
     def _library_entries(self):
+        from ._lib import _materialize
         NP = len(self.phases)
         nmp = len(self.models) * NP
         recs_by_mp = [self.records(mp) for mp in range(nmp)]
@@ -246,37 +247,22 @@ class Stage1Problem:
         if missing:
             raise LibraryGenError(f"no feasible template for: {sorted(missing)}")
         order = sorted(range(nmp), key=lambda mp: (self.models[mp // NP].name, self.phases[mp % NP]))
-        combos_cache = {}
+        caches, keys = {}, {}
         entries = []
-        new = object.__new__
         for mp in order:
             m, ph = mp // NP, self.phases[mp % NP]
             model = self.models[m]
             g = self.ctx.layer_granularity(model)
             recs = recs_by_mp[mp]
-            feas = np.nonzero(recs["num_stages"] > 0)[0]
-            if len(feas) and model.num_layers % g:
+            if model.num_layers % g and np.any(recs["num_stages"] > 0):
                 raise DomainError(f"stage layers sum to {(model.num_layers // g) * g}, "
                                   f"model has {model.num_layers}")
-            if m not in combos_cache:
-                combos_cache[m] = self.combo_objects(self.keys(m))
-            combos = combos_cache[m]
-            sub = recs[feas]
-            tps = sub["throughput_tps"].tolist()
-            nst = sub["num_stages"].tolist()
-            nn = sub["num_nodes"].tolist()
-            lps = sub["layers_per_stage"].tolist()
-            son = sub["stage_of_node"].tolist()
-            slo, name = self.slos[model.name], model.name
-            for k, i in enumerate(feas.tolist()):
-                S = nst[k]
-                pl = new(Placement)
-                pl.__dict__.update(num_stages=S, layers_per_stage=tuple(lps[k][:S]),
-                                   stage_of_node=tuple(son[k][:nn[k]]))
-                t = new(ServingTemplate)
-                t.__dict__.update(model=name, phase=ph, slo=slo, combo=combos[i], placement=pl,
-                                  throughput_tps=tps[k])
-                entries.append(t)
+            if m not in keys:
+                keys[m] = np.ascontiguousarray(self.keys(m), dtype=np.uint64)
+                caches[m] = {}
+            entries += _materialize.build_templates(
+                np.ascontiguousarray(recs).tobytes(), keys[m].tobytes(), list(self.cfg_by_rank),
+                model.name, ph, self.slos[model.name], caches[m], ServingTemplate, Placement, NodeComboKey)
         return entries
 
 

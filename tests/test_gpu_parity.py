@@ -439,3 +439,17 @@ def test_native_load_round_trip_extended(tmp_path):
     lib.save(out)
     assert hashlib.sha256(open(out, "rb").read()).hexdigest() == ref["sha256"]
     print(f"native load of {len(lib)} templates: {dt:.2f}s")
+
+
+def test_eager_library_build_time_extended():
+    """build_library (eager objects) for config 2: 1,084,362 templates, sampled lines
+    identical to the reference; reports the end-to-end time."""
+    import time
+    configs, models, slos, caps, ctx, regions, prices = workload("extended")
+    t0 = time.perf_counter()
+    lib = build_library(configs, models, slos, caps, ctx)
+    dt = time.perf_counter() - t0
+    assert len(lib) == 1084362
+    g = golden("library_extended.json.gz")
+    assert [template_line(t) for t in lib.entries[::97]] == g["sample"]
+    print(f"eager build_library(c2): {dt:.2f}s")
