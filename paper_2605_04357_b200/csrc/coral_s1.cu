@@ -98,7 +98,7 @@ struct coral_s1_handle {
   DevProblem dp{};
   // device buffers
   DevBuf prob, tab, flags, budget, keys_raw, keys, keys_tmp, koff_d, nvalid, cand_off_d, rec, cub_tmp;
-  DevBuf items, items_sorted, sort_a, sort_b, perm_a, perm_b, segk, scanv, flagsel, nsel, front,
+  DevBuf items, items_sorted, sort_a, sort_b, segk, scanv, flagsel, nsel, front,
       prices, enum_tmp;
   DevBuf op_in, op_out, tab_off_d, win, fbucket;
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
@@ -829,38 +829,50 @@ __global__ void node_query_kernel(DevProblem P, int64_t n, const int* __restrict
   batch[i] = b;
 }
 
-// sort-key extraction for the 4 stable LSD passes
-__global__ void sortkey_kernel(const coral_s1_frontier_item* __restrict__ items,
-                               const unsigned* __restrict__ perm, int64_t n, int field, int R,
-                               unsigned long long* __restrict__ out) {
+// Frontier order: segment asc, price asc, T desc, combo key asc,
+// stages asc -- the last only separates the per-rank partial records of one
+// (model, phase, combo) in the multi-GPU merge (fewer stages first, the
+// templates.py:322 tie rule). One 32-byte composite key, compared lexicographically.
+struct FrontKey {
+  unsigned seg, idx;            // segment = mp * R + region; idx = position in items
+  unsigned long long price;     // bit pattern of price >= 0 (orders like the value)
+  unsigned long long neg_t;     // ~bits(T), T > 0: ascending = T descending
+  unsigned long long key_s;     // combo_key << 3 | num_stages
+};
+
+struct FrontLess {
+  __device__ __forceinline__ bool operator()(const FrontKey& a, const FrontKey& b) const {
+    if (a.seg != b.seg) return a.seg < b.seg;
+    if (a.price != b.price) return a.price < b.price;
+    if (a.neg_t != b.neg_t) return a.neg_t < b.neg_t;
+    return a.key_s < b.key_s;
+  }
+};
+
+__global__ void front_keys_kernel(const coral_s1_frontier_item* __restrict__ items, int64_t n, int R,
+                                  FrontKey* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const coral_s1_frontier_item& it = items[perm ? perm[i] : i];
-  unsigned long long k;
-  switch (field) {
-    case 0: k = it.combo_key; break;                                               // key asc
-    case 1: k = ~(unsigned long long)__double_as_longlong(it.throughput_tps); break; // T desc (T > 0)
-    case 2: k = (unsigned long long)__double_as_longlong(it.price_usd_h); break;     // p asc (p >= 0)
-    case 4: k = it.rec.num_stages; break;  // fewer stages first (templates.py:322 tie rule)
-    default: k = (unsigned long long)it.mp * (unsigned long long)R + (unsigned long long)it.region;
-  }
+  const coral_s1_frontier_item& it = items[i];
+  FrontKey k;
+  k.seg = (unsigned)it.mp * (unsigned)R + (unsigned)it.region;
+  k.idx = (unsigned)i;
+  k.price = (unsigned long long)__double_as_longlong(it.price_usd_h);
+  k.neg_t = ~(unsigned long long)__double_as_longlong(it.throughput_tps);
+  k.key_s = it.combo_key << 3 | it.rec.num_stages;
   out[i] = k;
 }
 
-__global__ void iota_kernel(unsigned* p, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = (unsigned)i;
-}
-
 __global__ void gather_items_kernel(const coral_s1_frontier_item* __restrict__ in,
-                                    const unsigned* __restrict__ perm, int64_t n, int R,
+                                    const FrontKey* __restrict__ order, int64_t n,
                                     coral_s1_frontier_item* __restrict__ out,
                                     unsigned long long* __restrict__ seg, double* __restrict__ tv) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const coral_s1_frontier_item it = in[perm[i]];
+  const FrontKey k = order[i];
+  const coral_s1_frontier_item it = in[k.idx];
   out[i] = it;
-  seg[i] = (unsigned long long)it.mp * (unsigned long long)R + (unsigned long long)it.region;
+  seg[i] = k.seg;
   tv[i] = it.throughput_tps;
 }
 
@@ -885,55 +897,38 @@ int frontier_from_items(coral_s1_handle* h, int64_t n, int R) {
   h->nfront = 0;
   if (n == 0) return 0;
   int rc;
-  if ((rc = h->sort_a.ensure(n * 8)) || (rc = h->sort_b.ensure(n * 8)) ||
-      (rc = h->perm_a.ensure(n * 4)) || (rc = h->perm_b.ensure(n * 4)) ||
+  if ((rc = h->sort_a.ensure(n * sizeof(FrontKey))) || (rc = h->sort_b.ensure(n * 8)) ||
       (rc = h->items_sorted.ensure(n * sizeof(coral_s1_frontier_item))) ||
       (rc = h->segk.ensure(n * 8)) || (rc = h->scanv.ensure(n * 8)) ||
       (rc = h->flagsel.ensure(n)) || (rc = h->nsel.ensure(32)))
     return rc;
   const int TB = 256;
   const unsigned gb = (unsigned)((n + TB - 1) / TB);
-  unsigned* perm = h->perm_a.as<unsigned>();
-  unsigned* perm_out = h->perm_b.as<unsigned>();
-  iota_kernel<<<gb, TB, 0, st>>>(perm, n);
-  LAUNCH_CHECK(h);
   const coral_s1_frontier_item* items = h->items.as<coral_s1_frontier_item>();
-  // LSD: stages asc, key asc, T desc, price asc, segment asc (all stable)
-  const int nseg = h->NM * h->NP * R;
-  int seg_bits = 1;
-  while ((1ll << seg_bits) < (long long)nseg) ++seg_bits;
-  const int passes[5] = {4, 0, 1, 2, 3};
-  for (int pi = 0; pi < 5; ++pi) {
-    const int field = passes[pi];
-    sortkey_kernel<<<gb, TB, 0, st>>>(items, pi == 0 ? nullptr : perm, n, field, R,
-                                      h->sort_a.as<unsigned long long>());
-    LAUNCH_CHECK(h);
-    const int end_bit = field == 3 ? seg_bits : (field == 0 ? kKeyTokenBits * kMaxC : (field == 4 ? 3 : 64));
+  FrontKey* keys = h->sort_a.as<FrontKey>();
+  front_keys_kernel<<<gb, TB, 0, st>>>(items, n, R, keys);
+  LAUNCH_CHECK(h);
+  {
     size_t tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, h->sort_a.as<unsigned long long>(),
-                                    h->sort_b.as<unsigned long long>(), perm, perm_out, (int)n, 0,
-                                    end_bit, st);
+    cub::DeviceMergeSort::StableSortKeys(nullptr, tmp, keys, n, FrontLess(), st);
     if ((rc = ensure_tmp(h, tmp))) return rc;
-    CUDA_TRY(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, h->sort_a.as<unsigned long long>(),
-                                             h->sort_b.as<unsigned long long>(), perm, perm_out,
-                                             (int)n, 0, end_bit, st));
-    h->launches += 4;
-    std::swap(perm, perm_out);
+    CUDA_TRY(cub::DeviceMergeSort::StableSortKeys(h->cub_tmp.p, tmp, keys, n, FrontLess(), st));
+    h->launches += 3;
   }
   coral_s1_frontier_item* sorted = h->items_sorted.as<coral_s1_frontier_item>();
-  gather_items_kernel<<<gb, TB, 0, st>>>(items, perm, n, R, sorted, h->segk.as<unsigned long long>(),
-                                         h->sort_a.as<double>());
+  gather_items_kernel<<<gb, TB, 0, st>>>(items, keys, n, sorted, h->segk.as<unsigned long long>(),
+                                         h->sort_b.as<double>());
   LAUNCH_CHECK(h);
   size_t tmp = 0;
   cub::DeviceScan::InclusiveScanByKey(nullptr, tmp, h->segk.as<unsigned long long>(),
-                                      h->sort_a.as<double>(), h->scanv.as<double>(), MaxOp(),
+                                      h->sort_b.as<double>(), h->scanv.as<double>(), MaxOp(),
                                       (int)n, cub::Equality(), st);
   if ((rc = ensure_tmp(h, tmp))) return rc;
   CUDA_TRY(cub::DeviceScan::InclusiveScanByKey(h->cub_tmp.p, tmp, h->segk.as<unsigned long long>(),
-                                               h->sort_a.as<double>(), h->scanv.as<double>(),
+                                               h->sort_b.as<double>(), h->scanv.as<double>(),
                                                MaxOp(), (int)n, cub::Equality(), st));
   h->launches += 2;
-  skyline_flags_kernel<<<gb, TB, 0, st>>>(h->segk.as<unsigned long long>(), h->sort_a.as<double>(),
+  skyline_flags_kernel<<<gb, TB, 0, st>>>(h->segk.as<unsigned long long>(), h->sort_b.as<double>(),
                                           h->scanv.as<double>(), n, h->flagsel.as<unsigned char>());
   LAUNCH_CHECK(h);
   if ((rc = h->front.ensure(n * sizeof(coral_s1_frontier_item)))) return rc;
@@ -1029,7 +1024,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
   cudaSetDevice(h->device);
   DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->keys_tmp, &h->koff_d,
                     &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
-                    &h->sort_a, &h->sort_b, &h->perm_a, &h->perm_b, &h->segk, &h->scanv,
+                    &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
                     &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
                     &h->lat_sub, &h->lat_maxn, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};

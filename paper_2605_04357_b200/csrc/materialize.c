@@ -17,19 +17,59 @@
 static PyObject *s_items, *s_num_stages, *s_layers, *s_son, *s_model, *s_phase, *s_slo, *s_combo,
     *s_placement, *s_tps;
 
-static PyObject* new_with_dict(PyTypeObject* tp, PyObject** dict) {
-  PyObject* o = tp->tp_alloc(tp, 0);
-  if (!o) return NULL;
-  *dict = PyObject_GenericGetDict(o, NULL);
-  if (!*dict) { Py_DECREF(o); return NULL; }
-  return o;
-}
+/* object.__new__(tp): on CPython >= 3.12 the instance keeps its attributes as inline
+ * values (no per-object dict), which is what makes building and freeing ~10^6 small
+ * frozen dataclass instances cheap. */
+static PyObject* s_empty;
+static PyObject* new_obj(PyTypeObject* tp) { return PyBaseObject_Type.tp_new(tp, s_empty, NULL); }
 
-static int set(PyObject* d, PyObject* k, PyObject* v) {  /* steals v */
+/* setattr bypassing the frozen dataclass __setattr__ (object.__setattr__); steals v */
+static int seta(PyObject* o, PyObject* k, PyObject* v) {
   if (!v) return -1;
-  int rc = PyDict_SetItem(d, k, v);
+  int rc = PyObject_GenericSetAttr(o, k, v);
   Py_DECREF(v);
   return rc;
+}
+
+/* The (cfg, count) pair of a packed token, built once per call (immutable). */
+static PyObject* pair_for(unsigned tok, PyObject* cfgs, PyObject** pairs) {
+  if (!pairs[tok]) {
+    PyObject* cfg = PyList_GetItem(cfgs, (Py_ssize_t)((tok >> 3) - 1));
+    if (!cfg) return NULL;
+    pairs[tok] = Py_BuildValue("(Oi)", cfg, (int)(tok & 7u));
+  }
+  return pairs[tok];
+}
+
+/* New reference to the NodeComboKey of a packed combo key, cached in `combos`. */
+static PyObject* combo_for(uint64_t key, PyObject* cfgs, PyObject* combos, PyObject** pairs,
+                           PyObject* T_combo) {
+  PyObject* kk = PyLong_FromUnsignedLongLong(key);
+  if (!kk) return NULL;
+  PyObject* combo = PyDict_GetItem(combos, kk);
+  if (combo) {
+    Py_DECREF(kk);
+    Py_INCREF(combo);
+    return combo;
+  }
+  int ntok = 0;
+  for (int k = 0; k < CORAL_S1_MAX_NODES; ++k)
+    if ((key >> (9 * (CORAL_S1_MAX_NODES - 1 - k))) & 511u) ++ntok;
+  PyObject* items = PyTuple_New(ntok);
+  for (int k = 0; items && k < ntok; ++k) {
+    PyObject* pr = pair_for((unsigned)(key >> (9 * (CORAL_S1_MAX_NODES - 1 - k))) & 511u, cfgs, pairs);
+    if (!pr) { Py_CLEAR(items); break; }
+    Py_INCREF(pr);
+    PyTuple_SET_ITEM(items, k, pr);
+  }
+  combo = items ? new_obj((PyTypeObject*)T_combo) : NULL;
+  if (!combo || seta(combo, s_items, items) < 0 || PyDict_SetItem(combos, kk, combo) < 0) {
+    Py_XDECREF(combo);
+    Py_DECREF(kk);
+    return NULL;
+  }
+  Py_DECREF(kk);
+  return combo;
 }
 
 /* materialise(items: bytes-like of coral_s1_frontier_item, cfg_by_rank: list,
@@ -45,67 +85,63 @@ static PyObject* materialise(PyObject* self, PyObject* args) {
     return NULL;
   const coral_s1_frontier_item* it = (const coral_s1_frontier_item*)buf.buf;
   const Py_ssize_t n = buf.len / (Py_ssize_t)sizeof(coral_s1_frontier_item);
+  const Py_ssize_t nreg = PyList_Size(regions), nmp = PyList_Size(mnames) * NP;
+  PyObject** seg_lists = PyMem_Calloc((size_t)(nmp * nreg + 1), sizeof(PyObject*));
+  PyObject* pairs[512] = {NULL};
   PyObject* segments = PyDict_New();
   PyObject* cache = PyDict_New();
-  if (!segments || !cache) goto fail;
+  PyObject* combos = PyDict_New();
+  if (!segments || !cache || !combos || !seg_lists) goto fail;
   for (Py_ssize_t i = 0; i < n; ++i) {
     const coral_s1_frontier_item* x = &it[i];
     const int mp = x->mp, m = mp / NP, ph = mp % NP;
-    PyObject* ck = Py_BuildValue("(iK)", mp, (unsigned long long)x->combo_key);
+    if (mp < 0 || mp >= nmp || x->region < 0 || x->region >= nreg) {
+      PyErr_SetString(PyExc_ValueError, "frontier item outside the problem's (model, phase, region)");
+      goto fail;
+    }
+    /* (mp, combo) as one int: the packed key uses 9 * CORAL_S1_MAX_NODES = 54 bits */
+    PyObject* ck = PyLong_FromUnsignedLongLong(((unsigned long long)mp << 54) | x->combo_key);
     if (!ck) goto fail;
     PyObject* t = PyDict_GetItem(cache, ck); /* borrowed */
     if (!t) {
-      /* NodeComboKey(items=((cfg, n), ...)) */
-      int ntok = 0;
-      for (int k = 0; k < CORAL_S1_MAX_NODES; ++k)
-        if ((x->combo_key >> (9 * (CORAL_S1_MAX_NODES - 1 - k))) & 511u) ++ntok;
-      PyObject* items = PyTuple_New(ntok);
-      for (int k = 0; k < ntok; ++k) {
-        const unsigned tok = (unsigned)(x->combo_key >> (9 * (CORAL_S1_MAX_NODES - 1 - k))) & 511u;
-        PyObject* cfg = PyList_GetItem(cfgs, (Py_ssize_t)((tok >> 3) - 1));
-        Py_INCREF(cfg);
-        PyTuple_SET_ITEM(items, k, Py_BuildValue("(Ni)", cfg, (int)(tok & 7u)));
-      }
-      PyObject *dc, *dp, *dt;
-      PyObject* combo = new_with_dict((PyTypeObject*)T_combo, &dc);
-      if (!combo || set(dc, s_items, items) < 0) goto fail;
-      Py_DECREF(dc);
+      /* NodeComboKey(items=((cfg, n), ...)), shared by every (model, phase) of the combo */
+      PyObject* combo = combo_for(x->combo_key, cfgs, combos, pairs, T_combo);
+      if (!combo) goto fail;
       const int S = x->rec.num_stages, nn = x->rec.num_nodes;
       PyObject* layers = PyTuple_New(S);
       for (int s = 0; s < S; ++s) PyTuple_SET_ITEM(layers, s, PyLong_FromLong(x->rec.layers_per_stage[s]));
       PyObject* son = PyTuple_New(nn);
       for (int k = 0; k < nn; ++k) PyTuple_SET_ITEM(son, k, PyLong_FromLong(x->rec.stage_of_node[k]));
-      PyObject* pl = new_with_dict((PyTypeObject*)T_pl, &dp);
-      if (!pl || set(dp, s_num_stages, PyLong_FromLong(S)) < 0 || set(dp, s_layers, layers) < 0 ||
-          set(dp, s_son, son) < 0)
+      PyObject* pl = new_obj((PyTypeObject*)T_pl);
+      if (!pl || seta(pl, s_num_stages, PyLong_FromLong(S)) < 0 || seta(pl, s_layers, layers) < 0 ||
+          seta(pl, s_son, son) < 0)
         goto fail;
-      Py_DECREF(dp);
-      PyObject* tmpl = new_with_dict((PyTypeObject*)T_tmpl, &dt);
+      PyObject* tmpl = new_obj((PyTypeObject*)T_tmpl);
       PyObject* mname = PyList_GetItem(mnames, m);
       PyObject* phs = PyTuple_GetItem(phases, ph);
       PyObject* slo = PyList_GetItem(slos, m);
       Py_INCREF(mname);
       Py_INCREF(phs);
       Py_INCREF(slo);
-      if (!tmpl || set(dt, s_model, mname) < 0 || set(dt, s_phase, phs) < 0 || set(dt, s_slo, slo) < 0 ||
-          set(dt, s_combo, combo) < 0 || set(dt, s_placement, pl) < 0 ||
-          set(dt, s_tps, PyFloat_FromDouble(x->rec.throughput_tps)) < 0)
+      if (!tmpl || seta(tmpl, s_model, mname) < 0 || seta(tmpl, s_phase, phs) < 0 || seta(tmpl, s_slo, slo) < 0 ||
+          seta(tmpl, s_combo, combo) < 0 || seta(tmpl, s_placement, pl) < 0 ||
+          seta(tmpl, s_tps, PyFloat_FromDouble(x->rec.throughput_tps)) < 0)
         goto fail;
-      Py_DECREF(dt);
       if (PyDict_SetItem(cache, ck, tmpl) < 0) goto fail;
       Py_DECREF(tmpl);
       t = tmpl; /* owned by cache */
     }
     Py_DECREF(ck);
-    PyObject* seg = Py_BuildValue("(OOO)", PyList_GetItem(mnames, m), PyTuple_GetItem(phases, ph),
-                                  PyList_GetItem(regions, x->region));
-    PyObject* lst = PyDict_GetItem(segments, seg);
-    if (!lst) {
-      lst = PyList_New(0);
-      PyDict_SetItem(segments, seg, lst);
-      Py_DECREF(lst);
+    PyObject** slot = &seg_lists[(Py_ssize_t)mp * nreg + x->region];
+    if (!*slot) {
+      PyObject* seg = PyTuple_Pack(3, PyList_GetItem(mnames, m), PyTuple_GetItem(phases, ph),
+                                   PyList_GetItem(regions, x->region));
+      *slot = PyList_New(0);
+      if (!seg || !*slot || PyDict_SetItem(segments, seg, *slot) < 0) { Py_XDECREF(seg); goto fail; }
+      Py_DECREF(seg);
+      Py_DECREF(*slot); /* owned by segments */
     }
-    Py_DECREF(seg);
+    PyObject* lst = *slot;
     /* FrontierEntry is a 2-field namedtuple subclass: allocate the tuple directly */
     PyObject* entry = ((PyTypeObject*)T_entry)->tp_alloc((PyTypeObject*)T_entry, 2);
     if (!entry) goto fail;
@@ -116,11 +152,17 @@ static PyObject* materialise(PyObject* self, PyObject* args) {
     Py_DECREF(entry);
   }
   Py_DECREF(cache);
+  Py_DECREF(combos);
+  for (int k = 0; k < 512; ++k) Py_XDECREF(pairs[k]);
+  PyMem_Free(seg_lists);
   PyBuffer_Release(&buf);
   return segments;
 fail:
   Py_XDECREF(segments);
   Py_XDECREF(cache);
+  Py_XDECREF(combos);
+  for (int k = 0; k < 512; ++k) Py_XDECREF(pairs[k]);
+  PyMem_Free(seg_lists);
   PyBuffer_Release(&buf);
   if (!PyErr_Occurred()) PyErr_SetString(PyExc_RuntimeError, "materialise failed");
   return NULL;
@@ -159,10 +201,8 @@ static PyObject* build_templates(PyObject* self, PyObject* args) {
         Py_INCREF(cfg);
         PyTuple_SET_ITEM(items, k, Py_BuildValue("(Ni)", cfg, (int)(tok & 7u)));
       }
-      PyObject* dc;
-      combo = new_with_dict((PyTypeObject*)T_combo, &dc);
-      set(dc, s_items, items);
-      Py_DECREF(dc);
+      combo = new_obj((PyTypeObject*)T_combo);
+      seta(combo, s_items, items);
       PyDict_SetItem(cache, kk, combo);
     }
     Py_DECREF(kk);
@@ -171,23 +211,20 @@ static PyObject* build_templates(PyObject* self, PyObject* args) {
     for (int s2 = 0; s2 < S; ++s2) PyTuple_SET_ITEM(layers, s2, PyLong_FromLong(r->layers_per_stage[s2]));
     PyObject* son = PyTuple_New(nn);
     for (int k = 0; k < nn; ++k) PyTuple_SET_ITEM(son, k, PyLong_FromLong(r->stage_of_node[k]));
-    PyObject *dp, *dt;
-    PyObject* pl = new_with_dict((PyTypeObject*)T_pl, &dp);
-    set(dp, s_num_stages, PyLong_FromLong(S));
-    set(dp, s_layers, layers);
-    set(dp, s_son, son);
-    Py_DECREF(dp);
-    PyObject* t = new_with_dict((PyTypeObject*)T_tmpl, &dt);
+    PyObject* pl = new_obj((PyTypeObject*)T_pl);
+    seta(pl, s_num_stages, PyLong_FromLong(S));
+    seta(pl, s_layers, layers);
+    seta(pl, s_son, son);
+    PyObject* t = new_obj((PyTypeObject*)T_tmpl);
     Py_INCREF(model);
     Py_INCREF(phase);
     Py_INCREF(slo);
-    set(dt, s_model, model);
-    set(dt, s_phase, phase);
-    set(dt, s_slo, slo);
-    set(dt, s_combo, combo);
-    set(dt, s_placement, pl);
-    set(dt, s_tps, PyFloat_FromDouble(r->throughput_tps));
-    Py_DECREF(dt);
+    seta(t, s_model, model);
+    seta(t, s_phase, phase);
+    seta(t, s_slo, slo);
+    seta(t, s_combo, combo);
+    seta(t, s_placement, pl);
+    seta(t, s_tps, PyFloat_FromDouble(r->throughput_tps));
     PyList_Append(out, t);
     Py_DECREF(t);
   }
@@ -381,10 +418,8 @@ static PyObject* load_library(PyObject* self, PyObject* args) {
             Py_DECREF(cnt_int);
           }
           /* cache entry: (NodeComboKey, str(combo)) -- the str is the sort key */
-          PyObject* d;
-          PyObject* ck = new_with_dict((PyTypeObject*)T_combo, &d);
-          set(d, s_items, items);
-          Py_DECREF(d);
+          PyObject* ck = new_obj((PyTypeObject*)T_combo);
+          seta(ck, s_items, items);
           PyObject* sep = PyUnicode_FromString("+");
           PyObject* str = PyUnicode_Join(sep, parts);
           Py_DECREF(sep);
@@ -425,25 +460,22 @@ static PyObject* load_library(PyObject* self, PyObject* args) {
       PyErr_SetString(PyExc_KeyError, "record misses a field");
       goto fail;
     }
-    PyObject *dp, *dt;
-    PyObject* pl = new_with_dict((PyTypeObject*)T_pl, &dp);
-    set(dp, s_num_stages, nst);
-    set(dp, s_layers, layers);
-    set(dp, s_son, son);
-    Py_DECREF(dp);
+    PyObject* pl = new_obj((PyTypeObject*)T_pl);
+    seta(pl, s_num_stages, nst);
+    seta(pl, s_layers, layers);
+    seta(pl, s_son, son);
     PyObject* key3 = PyTuple_Pack(3, model, phase, combo_str);
     if (prev_key && sorted && PyObject_RichCompareBool(prev_key, key3, Py_GT) == 1) sorted = 0;
     Py_XDECREF(prev_key);
     prev_key = key3;
     Py_DECREF(combo_str);
-    PyObject* t = new_with_dict((PyTypeObject*)T_tmpl, &dt);
-    set(dt, s_model, model);
-    set(dt, s_phase, phase);
-    set(dt, s_slo, slo);
-    set(dt, s_combo, combo);
-    set(dt, s_placement, pl);
-    set(dt, s_tps, tps);
-    Py_DECREF(dt);
+    PyObject* t = new_obj((PyTypeObject*)T_tmpl);
+    seta(t, s_model, model);
+    seta(t, s_phase, phase);
+    seta(t, s_slo, slo);
+    seta(t, s_combo, combo);
+    seta(t, s_placement, pl);
+    seta(t, s_tps, tps);
     PyList_Append(entries, t);
     Py_DECREF(t);
     p = le + 1;
@@ -471,6 +503,7 @@ static PyMethodDef methods[] = {{"materialise", materialise, METH_VARARGS, NULL}
 static struct PyModuleDef mod = {PyModuleDef_HEAD_INIT, "_materialize", NULL, -1, methods};
 
 PyMODINIT_FUNC PyInit__materialize(void) {
+  s_empty = PyTuple_New(0);
   s_items = PyUnicode_InternFromString("items");
   s_num_stages = PyUnicode_InternFromString("num_stages");
   s_layers = PyUnicode_InternFromString("layers_per_stage");
