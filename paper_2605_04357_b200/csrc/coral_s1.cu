@@ -80,6 +80,7 @@ struct DevBuf {
 
 struct coral_s1_handle {
   int device = 0;
+  int num_sms = 148, ranks_blocks_per_sm = 1;
   cudaStream_t stream = nullptr;
   long long launches = 0;
   bool have_problem = false, have_tables = false, have_enum = false, have_eval = false;
@@ -986,6 +987,9 @@ int coral_s1_create(int device, coral_s1_handle** out) {
   CUDA_TRY(cudaSetDevice(device));
   auto* h = new coral_s1_handle();
   h->device = device;
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ranks_blocks_per_sm, lat_ranks_kernel, kRanksWarps * 32, 0);
+  h->ranks_blocks_per_sm = std::max(h->ranks_blocks_per_sm, 1);
   static unsigned long long tab[160][8];
   for (int N = 0; N < 160; ++N)
     for (int k = 0; k < 8; ++k) {
@@ -1392,7 +1396,7 @@ static int lattice_prepare(coral_s1_handle* h) {
   h->launches += 2;
   // upper bound (every state has at most 2^R sub-multiset codes): no host round trip
   if ((rc = h->lat_sub.ensure(std::max<long long>(ns << R, 1) * sizeof(uint2)))) return rc;
-  lat_subtab_kernel<<<gb, 256, 0, st>>>(L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(),
+  lat_subtab_kernel<<<(unsigned)((ns * 32 + 255) / 256), 256, 0, st>>>(L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(),
                                         h->lat_off.as<long long>(), h->lat_sub.as<uint2>());
   LAUNCH_CHECK(h);
   // maxn per model in closed form from the achievable memory sums of k configs
@@ -1587,7 +1591,8 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
     unsigned* ranks = h->ws_ranks[slot].as<unsigned>();
     if (h->n_max >= 2 && h->lat_states > 0) {
       LatModel L{h->K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
-      lat_ranks_kernel<<<(unsigned)((h->counts[m] * 64 + 255) / 256), 256, 0, h->side[slot]>>>(
+      const long long rb = std::min<long long>((h->counts[m] + kRanksWarps - 1) / kRanksWarps, (long long)h->num_sms * h->ranks_blocks_per_sm);
+      lat_ranks_kernel<<<(unsigned)rb, kRanksWarps * 32, 0, h->side[slot]>>>(
           L, h->dp.inv_rank, h->keys.as<unsigned long long>() + h->koff[m], h->counts[m], ranks);
       LAUNCH_CHECK(h);
     }

@@ -154,29 +154,106 @@ __global__ void lat_maxn_closed_kernel(LatModel L, const int* __restrict__ inv_r
   maxn[idx] = best;
 }
 
-// Per candidate and u code: size(u) << 24 | idx(u) (0xFFFFFFFF past M, idx 0 when
-// |u| > R). The top cells read idx(full - u) as the entry of code M-1-code. Shared by
-// both phases of a model. One thread per (candidate, code).
-__global__ void lat_ranks_kernel(LatModel L, const int* __restrict__ inv_rank,
-                                 const unsigned long long* __restrict__ keys, long long ncombo,
-                                 unsigned* __restrict__ ranks) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long ci = t >> 6;
-  const int code = (int)(t & 63);
-  if (ci >= ncombo) return;
-  int cfg[kMaxC], cnt[kMaxC];
-  const int C = lat_tokens(inv_rank, keys[ci], cfg, cnt);
-  int M = 1;
-  for (int c = 0; c < C; ++c) M *= cnt[c] + 1;
-  unsigned out = 0xFFFFFFFFu;
-  if (code < M) {
-    int d[kMaxC], rest = code;
-    for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; }
-    int s;
-    const long long r = lat_rank_tokens(L, cfg, d, C, &s);
-    out = ((unsigned)s << 24) | (unsigned)(s >= 1 && s <= L.R ? r : 0);
+// ceil(2^16 / r) for radices r = 1..7: q = (x * kLatMagic[r]) >> 16 equals x / r for
+// every x < 2^16 / 7 (the error term x * (m r - 2^16) stays below 2^16), and sub-multiset
+// codes are < 64.
+__constant__ unsigned kLatMagic[8] = {0u, 65536u, 32768u, 21846u, 16384u, 13108u, 10923u, 9363u};
+
+// Colex sums of the sub-multiset u = digits(code) of the packed key (token 0 is the
+// least significant mixed-radix digit, radix count + 1 -- the code order of
+// kernels.py:204) and, with kRest, of its complement key - u. The picks of u are
+// d_t copies of cfg_t in token order, so pick i contributes C(cfg_t + i, i + 1)
+// (lat_rank); a token's run of picks telescopes to two table entries. Registers only:
+// the token loop is unrolled and digits come from a multiply-high, not a division.
+template <bool kRest>
+__device__ __forceinline__ int lat_code_ranks(const LatModel& L, const int* __restrict__ inv_rank,
+                                              unsigned long long key, unsigned code, int* su,
+                                              unsigned long long* au, int* sr, unsigned long long* ar) {
+  unsigned rest = code;
+  int M = 1, pu = 0, pr = 0;
+  unsigned long long accu = 0, accr = 0;
+#pragma unroll
+  for (int t = 0; t < kMaxC; ++t) {
+    const unsigned tok = (unsigned)(key >> (9 * (kMaxC - 1 - t))) & 511u;
+    if (tok) {
+      const int cfg = __ldg(inv_rank + (tok >> 3) - 1);
+      const unsigned c = tok & 7u, radix = c + 1u;
+      const unsigned q = (rest * kLatMagic[radix]) >> 16;
+      const unsigned d = rest - q * radix;
+      rest = q;
+      M *= (int)radix;
+      // picks p..p+d-1 of value a add sum_{j=p+1}^{p+d} C(a-1+j, j)
+      //   = C(a+p+d, p+d) - C(a+p, p)   (hockey stick; 0 for a = 0)
+      accu += __ldg(L.binom + (cfg + pu + (int)d) * 8 + pu + (int)d) - __ldg(L.binom + (cfg + pu) * 8 + pu);
+      pu += (int)d;
+      if (kRest) {
+        const int e = (int)(c - d);
+        accr += __ldg(L.binom + (cfg + pr + e) * 8 + pr + e) - __ldg(L.binom + (cfg + pr) * 8 + pr);
+        pr += e;
+      }
+    }
   }
-  ranks[t] = out;
+  *su = pu;
+  *au = accu;
+  if (kRest) {
+    *sr = pr;
+    *ar = accr;
+  }
+  return M;
+}
+
+// Per candidate and u code < M: size(u) << 24 | idx(u) (idx 0 when |u| > R; entries
+// past M are never read). The top cells read idx(full - u) as the entry of code
+// M-1-code. Shared by both phases of a model. Persistent warps, one candidate per
+// warp iteration (next key prefetched), lane = code (two rounds when M > 32). Every
+// table entry lat_code_ranks' telescoped sums touch is C(cfg + k, k) with cfg < K and
+// k <= n_max, so the block stages those rows (32-bit: C(62 + 6, 6) < 2^32) and the
+// config ranks in shared memory once; the (cfg + p) * 8 + p addresses of a warp's
+// lanes fall in distinct banks.
+constexpr int kRanksWarps = 8;
+constexpr int kRanksRows = CORAL_S1_MAX_CONFIGS + kMaxC + 1;
+__global__ void __launch_bounds__(kRanksWarps * 32) lat_ranks_kernel(
+    LatModel L, const int* __restrict__ inv_rank, const unsigned long long* __restrict__ keys,
+    long long ncombo, unsigned* __restrict__ ranks) {
+  __shared__ unsigned sBin[kRanksRows * 8];  // [N][k] flattened: C(N, k) at N * 8 + k
+  __shared__ int sInv[CORAL_S1_MAX_CONFIGS];
+  for (int e = threadIdx.x; e < (L.K + kMaxC + 1) * 8; e += blockDim.x) sBin[e] = (unsigned)L.binom[e];
+  for (int e = threadIdx.x; e < L.K; e += blockDim.x) sInv[e] = inv_rank[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = (long long)gridDim.x * kRanksWarps;
+  long long ci = (long long)blockIdx.x * kRanksWarps + (threadIdx.x >> 5);
+  unsigned long long key = ci < ncombo ? keys[ci] : 0ull;
+  for (; ci < ncombo; ci += nwarps) {
+    const unsigned long long cur = key;
+    if (ci + nwarps < ncombo) key = keys[ci + nwarps];
+    // per token: table row base cfg * 8, radix, multiply-high constant. An empty slot
+    // has radix 1 (digit 0), so it adds C(N, p) - C(N, p) = 0: no branches below.
+    unsigned cb[kMaxC], radix[kMaxC], magic[kMaxC];
+    int M = 1;
+#pragma unroll
+    for (int t = 0; t < kMaxC; ++t) {
+      const unsigned tok = (unsigned)(cur >> (9 * (kMaxC - 1 - t))) & 511u;
+      cb[t] = (unsigned)sInv[max((int)(tok >> 3) - 1, 0)] * 8u;
+      radix[t] = (tok & 7u) + 1u;
+      magic[t] = kLatMagic[radix[t]];
+      M *= (int)radix[t];
+    }
+    unsigned* out = ranks + ci * 64;
+    for (unsigned code = lane; (int)code < M; code += 32) {
+      unsigned rest = code, acc = 0, p9 = 0;  // p9 = 9 * picks so far: C(cfg + p, p) at cb + 9p
+#pragma unroll
+      for (int t = 0; t < kMaxC; ++t) {
+        const unsigned q = (rest * magic[t]) >> 16;
+        const unsigned d9 = (rest - q * radix[t]) * 9u;
+        rest = q;
+        acc += sBin[cb[t] + p9 + d9] - sBin[cb[t] + p9];
+        p9 += d9;
+      }
+      const int pu = (int)(p9 / 9u);
+      out[code] = ((unsigned)pu << 24) | (pu >= 1 && pu <= L.R ? (unsigned)(L.base[pu] + (long long)acc) : 0u);
+    }
+  }
 }
 
 // nsub[idx] = M(X) = prod(counts + 1)
@@ -197,24 +274,20 @@ __global__ void lat_nsub_kernel(LatModel L, const unsigned long long* __restrict
 }
 
 // subtab[off[X] + code] = {size(u) << 24 | idx(u), idx(X - u)} for code in [0, M(X)).
+// Warp per state X, lane = code: |X| <= R <= 5 gives M(X) <= 32.
 __global__ void lat_subtab_kernel(LatModel L, const int* __restrict__ inv_rank,
                                   const unsigned long long* __restrict__ state_key,
                                   const long long* __restrict__ off, uint2* __restrict__ subtab) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (idx >= L.base[L.R + 1]) return;
-  int cfg[kMaxC], cnt[kMaxC];
-  const int C = lat_tokens(inv_rank, state_key[idx], cfg, cnt);
-  int M = 1;
-  for (int c = 0; c < C; ++c) M *= cnt[c] + 1;
-  uint2* out = subtab + off[idx];
-  for (int code = 0; code < M; ++code) {
-    int d[kMaxC], e[kMaxC], rest = code;
-    for (int c = 0; c < C; ++c) { d[c] = rest % (cnt[c] + 1); rest /= cnt[c] + 1; e[c] = cnt[c] - d[c]; }
-    int su, sr;
-    const long long ru = lat_rank_tokens(L, cfg, d, C, &su);
-    const long long rr = lat_rank_tokens(L, cfg, e, C, &sr);
-    out[code] = make_uint2(((unsigned)su << 24) | (unsigned)(ru < 0 ? 0 : ru), (unsigned)(rr < 0 ? 0 : rr));
-  }
+  const unsigned code = threadIdx.x & 31u;
+  int su, sr;
+  unsigned long long au, ar;
+  const int M = lat_code_ranks<true>(L, inv_rank, state_key[idx], code, &su, &au, &sr, &ar);
+  if ((int)code < M)
+    subtab[off[idx] + code] =
+        make_uint2(((unsigned)su << 24) | (su ? (unsigned)(L.base[su] + (long long)au) : 0u),
+                   sr ? (unsigned)(L.base[sr] + (long long)ar) : 0u);
 }
 
 // ---- per (model, phase): every S at once ----------------------------------------
