@@ -297,6 +297,7 @@ def main():
     torch.cuda.synchronize()
     ncand = h.num_candidates()
     top_ms, top_n, total_ms = 0.0, 0, 0.0
+    kstat = {1: [0.0, 0], 2: [0.0, 0]}  # lat_layer_kernel, lat_value_kernel: (ms, launches)
     launches0 = h.launches
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -313,6 +314,10 @@ def main():
             t_ms, t_n = h.kernel_stats(0)
             top_ms += t_ms
             top_n += t_n
+            for kind in kstat:
+                k_ms, k_n = h.kernel_stats(kind)
+                kstat[kind][0] += k_ms
+                kstat[kind][1] += k_n
     launches = h.launches - launches0
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -348,23 +353,38 @@ def main():
         tdist.all_reduce(et, op=tdist.ReduceOp.MAX)
     e2e_s = float(et.item())
 
-    # roofline of the dominant kernel (lat_top_kernel), timed live per launch
+    # roofline of the dominant kernel (lat_layer_kernel, 46% of a serialised solve in
+    # profiles/r01_launches_solve.txt; lat_top_kernel 37%), timed live per launch with
+    # CUDA events on its stream. Algorithmic bytes per launch from one census solve
+    # outside the timed region (csrc/lattice.cuh: 10 B per f/choice cell written + one
+    # read of each computed state's value_S and f_{sg-1} rows + its sub-table entries).
     peaks, peak_kind = measured_peaks()
+    h.set_census(True)
+    step()
+    layer_alg = h.census()
+    h.set_census(False)
+    layer_ms, layer_n = kstat[1]
+    per_step = max(layer_n // max(args.steps, 1), 1)
+    layer_launch_s = (layer_ms / max(layer_n, 1)) / 1e3
+    alg_per_launch = layer_alg / per_step
+    achieved = alg_per_launch / layer_launch_s / 1e9 if layer_n else 0.0
     counts = h.num_combos()
     _, lsteps, smax = h.table_layout()
     if masks is None:
         masks = [sum(1 << S for S in range(1, 7))] * (len(w.models) * NP)
-    alg = top_kernel_bytes(counts, lsteps, smax, masks, len(w.configs), w.n_max)
-    per_step = max(top_n // max(args.steps, 1), 1)
+    top_alg = top_kernel_bytes(counts, lsteps, smax, masks, len(w.configs), w.n_max)
+    top_per_step = max(top_n // max(args.steps, 1), 1)
     top_launch_s = (top_ms / max(top_n, 1)) / 1e3
-    alg_per_launch = alg / per_step
-    achieved = alg_per_launch / top_launch_s / 1e9 if top_n else 0.0
-    traffic = None
+    top_achieved = (top_alg / top_per_step) / top_launch_s / 1e9 if top_n else 0.0
+    traffic, top_traffic = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh).get("lat_top_kernel_dram_bytes_per_launch")
+            tj = json.load(fh)
+        traffic = tj.get("lat_layer_kernel_dram_bytes_per_launch")
+        top_traffic = tj.get("lat_top_kernel_dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
+    lattice_ms = layer_ms + top_ms + kstat[2][0]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -381,14 +401,20 @@ def main():
         "e2e": {"value": ncand / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "stage1_solve_s": e2e_s},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "lat_top_kernel", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": "lat_layer_kernel", "achieved": achieved,
                      "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved / peaks.get("hbm_gbs", 6650.0), "traffic": traffic,
-                     "peak_kind": peak_kind, "launch_ms": 1e3 * top_launch_s,
-                     "launches_per_step": per_step, "share_of_step": top_ms / max(total_ms, 1e-9),
+                     "peak_kind": peak_kind, "launch_ms": 1e3 * layer_launch_s,
+                     "launches_per_step": per_step,
+                     "share_of_lattice_kernel_time": layer_ms / max(lattice_ms, 1e-9),
                      "alg_bytes_per_launch": alg_per_launch,
-                     "note": "fp64 max-min DP over L2-resident lattice tables: latency-bound on dependent "
-                             "L2 loads, not HBM bandwidth (DESIGN.md 5)"},
+                     "note": "fp64 max-min crossing searches over L2-resident lattice tables: issue- and "
+                             "L2-latency-bound, not HBM bandwidth (DESIGN.md 5)"},
+        "roofline_top": {"kernel": "lat_top_kernel", "achieved": top_achieved, "unit": "GB/s",
+                         "frac": top_achieved / peaks.get("hbm_gbs", 6650.0), "traffic": top_traffic,
+                         "launch_ms": 1e3 * top_launch_s, "launches_per_step": top_per_step,
+                         "share_of_lattice_kernel_time": top_ms / max(lattice_ms, 1e-9),
+                         "alg_bytes_per_launch": top_alg / top_per_step},
     }
     if world == 1:
         line["other_configs"] = other_configs(args, h)

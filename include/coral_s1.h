@@ -222,6 +222,12 @@ int coral_s1_format_double(double v, char* out, int cap);
 /* device time of the last evaluate's lattice kernels of one kind (0 top cells,
  * 1 layers, 2 value tables): summed CUDA-event time of each launch on its stream */
 int coral_s1_kernel_stats(const coral_s1_handle* h, int kind, double* total_ms, int64_t* launches);
+/* layer-kernel census for the bench roofline: while on, each evaluate counts the
+ * algorithmic bytes of its lat_layer_kernel launches (10 B per f/choice cell written +
+ * one read of each computed state's value_S and f_{sg-1} rows + 8 B per valid
+ * sub-table entry); off (default) passes no counter to the kernel */
+int coral_s1_set_census(coral_s1_handle* h, int on);
+int coral_s1_census(coral_s1_handle* h, int64_t* layer_bytes);
 
 #ifdef __cplusplus
 }

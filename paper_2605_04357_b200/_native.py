@@ -104,6 +104,8 @@ def load():
                                                     _f64p, C.c_int64, _i32p, _f64p, _i64p, _i64p]),
             "coral_s1_stage_ms": (C.c_int, [vp, _f64p, _f64p, _f64p, _f64p]),
             "coral_s1_kernel_stats": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
+            "coral_s1_set_census": (C.c_int, [vp, C.c_int]),
+            "coral_s1_census": (C.c_int, [vp, _i64p]),
             "coral_s1_write_library": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_int, _i32p,
                                                  C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
                                                  C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), _i64p]),
@@ -312,6 +314,15 @@ class Handle:
             _ptr(tput_off, C.c_int64), _ptr(tp, C.c_double), tput.size, _ptr(S, C.c_int32),
             _ptr(best, C.c_double), _ptr(sj, C.c_int64), _ptr(sc, C.c_int64)))
         return best, sj, sc
+
+    def set_census(self, on: bool) -> None:
+        _check(self._lib.coral_s1_set_census(self._h, 1 if on else 0))
+
+    def census(self) -> int:
+        """Algorithmic bytes of the last evaluate's lat_layer_kernel launches (census on)."""
+        v = C.c_int64()
+        _check(self._lib.coral_s1_census(self._h, C.byref(v)))
+        return v.value
 
     def kernel_stats(self, kind: int):
         """(total ms, launches) of the last evaluate's lattice kernels: 0 top, 1 layer, 2 value."""

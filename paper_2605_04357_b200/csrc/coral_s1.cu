@@ -126,6 +126,9 @@ struct coral_s1_handle {
   int ntimed = 0;
   cudaEvent_t ev[8] = {};
   float ms[4] = {0, 0, 0, 0};
+  // layer-kernel census (coral_s1_set_census): algorithmic bytes of the last evaluate
+  bool census_on = false;
+  DevBuf census;
 };
 
 namespace {
@@ -694,19 +697,33 @@ __device__ __forceinline__ unsigned long long dbits(double x) {
   return (unsigned long long)__double_as_longlong(x);  // monotone for x >= 0
 }
 
-// Exact prefilter, pass 1: the price range (bit patterns) over all items.
-__global__ void frontier_range_kernel(FrontArgs A, unsigned long long* __restrict__ range) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  coral_s1_frontier_item it;
-  const bool ok = frontier_item(A, t / A.R, (int)(t % A.R), &it);
-  unsigned long long lo = ok ? dbits(it.price_usd_h) : ~0ull, hi = ok ? dbits(it.price_usd_h) : 0ull;
+// Exact prefilter, pass 1: the price range (bit patterns) over all items. Grid-stride
+// over (candidate, region) with a block reduction: one atomic pair per block (a pair
+// per warp serialised ~10^5 atomics on the same two words).
+__global__ void __launch_bounds__(256) frontier_range_kernel(FrontArgs A, unsigned long long* __restrict__ range) {
+  __shared__ unsigned long long slo[8], shi[8];
+  unsigned long long lo = ~0ull, hi = 0ull;
+  const int64_t n = A.ncand * A.R;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    coral_s1_frontier_item it;
+    if (frontier_item(A, t / A.R, (int)(t % A.R), &it)) {
+      lo = min(lo, dbits(it.price_usd_h));
+      hi = max(hi, dbits(it.price_usd_h));
+    }
+  }
   for (int o = 16; o > 0; o >>= 1) {
     lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
   }
-  if ((threadIdx.x & 31) == 0 && hi) {
-    atomicMin(range, lo);
-    atomicMax(range + 1, hi);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { slo[w] = lo; shi[w] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) { lo = min(lo, slo[k]); hi = max(hi, shi[k]); }
+    if (hi) {
+      atomicMin(range, lo);
+      atomicMax(range + 1, hi);
+    }
   }
 }
 
@@ -1031,7 +1048,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
                     &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
-                    &h->lat_sub, &h->lat_maxn, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};
+                    &h->lat_sub, &h->lat_maxn, &h->census, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release(); h->ws_ranks[i].release();
@@ -1487,7 +1504,8 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
     const long long nv = ns * Lu;
     const int ti = timed_begin(h, st, 2);
     lat_value_kernel<<<dim3((unsigned)((nv + 255) / 256), Smax - 1), 256, 0, st>>>(
-        L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(), tab_mp, K, Lu, 2, smask, W);
+        L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(), h->lat_maxn.as<unsigned>() + (size_t)m * ns,
+        tab_mp, K, Lu, 2, smask, W);
     timed_end(h, st, ti);
     LAUNCH_CHECK(h);
   }
@@ -1497,7 +1515,8 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
     const int ti = timed_begin(h, st, 1);
     lat_layer_kernel<<<dim3((unsigned)((nst * 32 + 255) / 256), Smax - sg), 256, 0, st>>>(
         L, sg, sg + 1, smask, xmask, h->n_max, Lu, h->lat_maxn.as<unsigned>() + (size_t)m * ns,
-        h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), W);
+        h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), W,
+        h->census_on ? h->census.as<unsigned long long>() : nullptr);
     timed_end(h, st, ti);
     LAUNCH_CHECK(h);
   }
@@ -1560,6 +1579,7 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   h->ntimed = 0;
   // records not improved by any unit read as infeasible (num_stages 0)
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), st));
+  if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 8, st));
   h->model_used.assign(h->NM, 0);  // lattice tables only for the models this call evaluates
   for (int mp = 0; mp < NMP; ++mp)
     for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
@@ -1623,6 +1643,7 @@ int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi) {
   if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record)))) return rc;
   CUDA_TRY(cudaEventRecord(h->ev[4], h->stream));
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), h->stream));
+  if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 8, h->stream));
   if ((rc = launch_percombo(h, h->stream, lo, hi, 1, 1, CORAL_S1_MAX_NODES))) return rc;
   CUDA_TRY(cudaEventRecord(h->ev[5], h->stream));
   h->have_eval = true;
@@ -1684,7 +1705,8 @@ int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices,
     const unsigned gb = (unsigned)((nmax + 255) / 256);
     unsigned long long init[2] = {~0ull, 0ull}, range[2];
     CUDA_TRY(cudaMemcpyAsync(h->nsel.as<unsigned long long>() + 1, init, 16, cudaMemcpyHostToDevice, st));
-    frontier_range_kernel<<<gb, 256, 0, st>>>(A, h->nsel.as<unsigned long long>() + 1);
+    frontier_range_kernel<<<(unsigned)std::min<int64_t>(gb, (int64_t)h->num_sms * 8), 256, 0, st>>>(
+        A, h->nsel.as<unsigned long long>() + 1);
     LAUNCH_CHECK(h);
     CUDA_TRY(cudaMemcpyAsync(range, h->nsel.as<unsigned long long>() + 1, 16, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -2007,6 +2029,25 @@ int coral_s1_kernel_stats(const coral_s1_handle* h, int kind, double* total_ms, 
   }
   if (total_ms) *total_ms = tot;
   if (launches) *launches = n;
+  return 0;
+}
+
+int coral_s1_set_census(coral_s1_handle* h, int on) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  int rc;
+  if (on && (rc = h->census.ensure(8))) return rc;
+  h->census_on = on != 0;
+  return 0;
+}
+
+int coral_s1_census(coral_s1_handle* h, int64_t* layer_bytes) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  unsigned long long v = 0;
+  if (h->census_on) {
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    CUDA_TRY(cudaMemcpy(&v, h->census.p, 8, cudaMemcpyDeviceToHost));
+  }
+  if (layer_bytes) *layer_bytes = (int64_t)v;
   return 0;
 }
 

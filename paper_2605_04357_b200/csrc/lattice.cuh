@@ -309,8 +309,13 @@ struct LatWork {
 };
 
 // value_S[idx][j], j = 1..Lu (kernels.py:164-170) for S in [S_lo, S_lo + gridDim.y).
+// Only rows some reader can touch: u is one stage of a candidate whose other S - 1
+// stages hold >= 1 node each, so |candidate| >= |u| + S - 1 <= maxn(u) -- true for
+// every u the layers (maxn(u) >= maxn(X)), the layer-2 X - u side and the top cell
+// read; maxn is a superset bound, so no needed row is skipped.
 __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
                                  const unsigned long long* __restrict__ state_key,
+                                 const unsigned* __restrict__ maxn,
                                  const double* __restrict__ tab_mp /* [S][K][Lu] */, int K, int Lu,
                                  int S_lo, unsigned smask, LatWork W) {
   const int S = S_lo + blockIdx.y;
@@ -321,7 +326,11 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
   if (idx >= L.base[L.R + 1]) return;
   const double* tabS = tab_mp + (long long)(S - 1) * K * Lu;
   int cfg[kMaxC], cnt[kMaxC];
-  const int C = lat_tokens(inv_rank, state_key[idx], cfg, cnt);
+  const unsigned long long key = state_key[idx];
+  int n = 0;
+  for (int t2 = 0; t2 < kMaxC; ++t2) n += (int)((key >> (9 * t2)) & 7u);
+  if ((int)maxn[idx] < n + S - 1) return;
+  const int C = lat_tokens(inv_rank, key, cfg, cnt);
   double v = 0.0;
   for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], tabS[cfg[c] * Lu + (j - 1)]));
   W.val(S)[idx * (Lu + 1) + j] = v;
@@ -332,7 +341,7 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
 __global__ void __launch_bounds__(256) lat_layer_kernel(
     LatModel L, int sg, int S_lo, unsigned smask, unsigned xmask, int n_max, int Lu,
     const unsigned* __restrict__ maxn, const long long* __restrict__ off,
-    const uint2* __restrict__ subtab, LatWork W) {
+    const uint2* __restrict__ subtab, LatWork W, unsigned long long* __restrict__ census) {
   const int S = S_lo + blockIdx.y;
   if (!((smask >> S) & 1u) || S <= sg) return;
   const int lane = threadIdx.x & 31;
@@ -365,6 +374,11 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
   }
   const unsigned vmask = __ballot_sync(0xffffffffu, ok);
   const int nv = __popc(vmask);
+  // census (bench roofline, off in timed runs): algorithmic bytes of this state = its
+  // f + choice cells written (10 B each), one read of its value_S and f_{sg-1} rows
+  // and of its valid sub-table entries
+  if (census && lane == 0)
+    atomicAdd(census, (unsigned long long)(10 * (lmax - sg + 1) + 16 * LuP + 8 * nv));
   for (int l0 = sg; l0 <= lmax; l0 += 32) {
     // lanes = G groups x wp positions; group g takes valid codes g, g+G, g+2G, ...
     const int w = min(32, lmax - l0 + 1);
