@@ -24,6 +24,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -385,13 +387,22 @@ def main():
     except (OSError, ValueError):
         pass
     lattice_ms = layer_ms + top_ms + kstat[2][0]
+    # (model, phase, combo, S) DP evaluations the reference performs: its per-combo S
+    # loop runs S = 1..min(n, Lu) (templates.py:314-316: 8.125 M for c2)
+    dp_evals = 0
+    for m in range(len(w.models)):
+        keys = h.get_combos(m)
+        nodes = sum(((keys >> np.uint64(9 * t)) & np.uint64(7)).astype(np.int64) for t in range(6))
+        dp_evals += int(np.minimum(nodes, int(lsteps[m])).sum()) * NP
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic spec tables (reference catalog, BASELINE config 2)",
         "config": {"workload": f"{w.name} (BASELINE config 2: 6 models x 20 node configs x 3 regions)",
-                   "candidates": ncand, "frontier_survivors": int(nf),
+                   "candidates": ncand, "dp_evaluations": dp_evals,
+                   "dp_evaluations_per_s": dp_evals * args.steps / (total_ms / 1e3),
+                   "frontier_survivors": int(nf),
                    "parallelism": f"(model, phase, S) units over {world} GPUs + NCCL all-gather of frontiers"
                                   if world > 1 else "single GPU",
                    "l2": "256 MB buffer written between timed steps",

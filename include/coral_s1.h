@@ -220,8 +220,13 @@ int coral_s1_node_queries(coral_s1_handle* h, int64_t n, const int32_t* cfg, con
 int coral_s1_format_double(double v, char* out, int cap);
 
 /* device time of the last evaluate's lattice kernels of one kind (0 top cells,
- * 1 layers, 2 value tables): summed CUDA-event time of each launch on its stream */
+ * 1 layers, 2 value tables, 3 decode, 4 sub-multiset ranks): summed CUDA-event time of each launch on its stream */
 int coral_s1_kernel_stats(const coral_s1_handle* h, int kind, double* total_ms, int64_t* launches);
+/* per-launch timeline of the last evaluate's lattice kernels (kinds as above plus
+ * 3 decode, 4 sub-multiset ranks): side-stream slot and begin/end in ms from the
+ * evaluate's start event; up to cap launches, count in *n (diagnostics) */
+int coral_s1_kernel_timeline(const coral_s1_handle* h, int64_t cap, int32_t* kind, int32_t* stream,
+                             double* begin_ms, double* end_ms, int64_t* n);
 /* layer-kernel census for the bench roofline: while on, each evaluate counts the
  * algorithmic bytes of its lat_layer_kernel launches (10 B per f/choice cell written +
  * one read of each computed state's value_S and f_{sg-1} rows + 8 B per valid

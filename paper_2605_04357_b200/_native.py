@@ -14,7 +14,9 @@ import numpy as np
 
 from .specs import DomainError
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libcoral_s1.so")
+# CORAL_S1_LIB: alternative build of the same library (A/B timing runs only)
+_LIB_PATH = os.environ.get("CORAL_S1_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                           "libcoral_s1.so")
 
 OK, EINVAL, ENOTEMPLATE, ECUDA, EUNSUPPORTED = 0, 1, 2, 3, 4
 PHASE_CODE = {"prefill": 0, "decode": 1}
@@ -105,6 +107,7 @@ def load():
             "coral_s1_stage_ms": (C.c_int, [vp, _f64p, _f64p, _f64p, _f64p]),
             "coral_s1_kernel_stats": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
             "coral_s1_set_census": (C.c_int, [vp, C.c_int]),
+            "coral_s1_kernel_timeline": (C.c_int, [vp, C.c_int64, _i32p, _i32p, _f64p, _f64p, _i64p]),
             "coral_s1_census": (C.c_int, [vp, _i64p]),
             "coral_s1_write_library": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_int, _i32p,
                                                  C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
@@ -323,6 +326,18 @@ class Handle:
         v = C.c_int64()
         _check(self._lib.coral_s1_census(self._h, C.byref(v)))
         return v.value
+
+    def kernel_timeline(self, cap: int = 512):
+        """[(kind, stream slot, begin ms, end ms)] of the last evaluate's lattice launches."""
+        kind = np.zeros(cap, np.int32)
+        slot = np.zeros(cap, np.int32)
+        b = np.zeros(cap)
+        e = np.zeros(cap)
+        n = C.c_int64()
+        _check(self._lib.coral_s1_kernel_timeline(self._h, cap, _ptr(kind, C.c_int32), _ptr(slot, C.c_int32),
+                                                  _ptr(b, C.c_double), _ptr(e, C.c_double), C.byref(n)))
+        k = n.value
+        return list(zip(kind[:k].tolist(), slot[:k].tolist(), b[:k].tolist(), e[:k].tolist()))
 
     def kernel_stats(self, kind: int):
         """(total ms, launches) of the last evaluate's lattice kernels: 0 top, 1 layer, 2 value."""

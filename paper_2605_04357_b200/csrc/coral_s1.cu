@@ -123,6 +123,7 @@ struct coral_s1_handle {
   static constexpr int kTimedMax = 512;
   cudaEvent_t tev[kTimedMax][2] = {};
   int tkind[kTimedMax] = {};
+  int tslot[kTimedMax] = {};
   int ntimed = 0;
   cudaEvent_t ev[8] = {};
   float ms[4] = {0, 0, 0, 0};
@@ -503,11 +504,12 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
     int bu = 1 << 20, bj = 0;
     // S == 2 reads value rows on both sides: symmetric, search the lower half only
     const int chalf = (S == 2 && ((A.xmask >> 2) & 1u)) ? (M - 1) / 2 : M;
+    const bool cap = (A.xmask >> S) & 1u;  // exactly monotone rows: capped crossing search
     for (int k = 0; k < 2; ++k) {
       if (su[k] > n - (S - 1) || lane + 1 + 32 * k > chalf) continue;
       double cand;
       int cj;
-      dp_pair(val + ru[k] * LuP, lay + rr[k] * LuP, Lu, Lu - (S - 1), true, cand, cj);
+      dp_pair(val + ru[k] * LuP, lay + rr[k] * LuP, Lu, Lu - (S - 1), true, cand, cj, cap);
       if (cand > best) { best = cand; bu = lane + 1 + 32 * k; bj = cj; }
     }
     warp_argmax_code(best, bu, bj);
@@ -1366,11 +1368,15 @@ static int launch_percombo(coral_s1_handle* h, cudaStream_t st, int64_t lo, int6
 }
 
 // Bracket one launch on stream st with a timing-event pair of kind `kind`
-// (0 = lat_top_kernel, 1 = lat_layer_kernel, 2 = lat_value_kernel).
+// (0 = lat_top_kernel, 1 = lat_layer_kernel, 2 = lat_value_kernel, 3 = lat_decode_kernel,
+// 4 = lat_ranks_kernel).
 static int timed_begin(coral_s1_handle* h, cudaStream_t st, int kind) {
   if (h->ntimed >= coral_s1_handle::kTimedMax) return -1;
   const int i = h->ntimed++;
   h->tkind[i] = kind;
+  h->tslot[i] = -1;
+  for (int k = 0; k < coral_s1_handle::kStreams; ++k)
+    if (h->side[k] == st) h->tslot[i] = k;
   cudaEventRecord(h->tev[i][0], st);
   return i;
 }
@@ -1501,9 +1507,8 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   (void)LuP;
   const double* tab_mp = h->tab.as<double>() + h->tab_off[mp];
   if (Smax >= 2 && ns > 0) {
-    const long long nv = ns * Lu;
     const int ti = timed_begin(h, st, 2);
-    lat_value_kernel<<<dim3((unsigned)((nv + 255) / 256), Smax - 1), 256, 0, st>>>(
+    lat_value_kernel<<<dim3((unsigned)((ns * 32 + 255) / 256), Smax - 1), 256, 0, st>>>(
         L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(), h->lat_maxn.as<unsigned>() + (size_t)m * ns,
         tab_mp, K, Lu, 2, smask, W);
     timed_end(h, st, ti);
@@ -1612,8 +1617,10 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
     if (h->n_max >= 2 && h->lat_states > 0) {
       LatModel L{h->K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
       const long long rb = std::min<long long>((h->counts[m] + kRanksWarps - 1) / kRanksWarps, (long long)h->num_sms * h->ranks_blocks_per_sm);
+      const int tr = timed_begin(h, h->side[slot], 4);
       lat_ranks_kernel<<<(unsigned)rb, kRanksWarps * 32, 0, h->side[slot]>>>(
           L, h->dp.inv_rank, h->keys.as<unsigned long long>() + h->koff[m], h->counts[m], ranks);
+      timed_end(h, h->side[slot], tr);
       LAUNCH_CHECK(h);
     }
     for (int p = 0; p < h->NP; ++p)
@@ -2048,6 +2055,24 @@ int coral_s1_census(coral_s1_handle* h, int64_t* layer_bytes) {
     CUDA_TRY(cudaMemcpy(&v, h->census.p, 8, cudaMemcpyDeviceToHost));
   }
   if (layer_bytes) *layer_bytes = (int64_t)v;
+  return 0;
+}
+
+int coral_s1_kernel_timeline(const coral_s1_handle* h, int64_t cap, int32_t* kind, int32_t* stream,
+                             double* begin_ms, double* end_ms, int64_t* n) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  const int64_t m = std::min<int64_t>(cap, h->ntimed);
+  for (int64_t i = 0; i < m; ++i) {
+    float b = 0, e = 0;
+    CUDA_TRY(cudaEventSynchronize(h->tev[i][1]));
+    CUDA_TRY(cudaEventElapsedTime(&b, h->ev[4], h->tev[i][0]));
+    CUDA_TRY(cudaEventElapsedTime(&e, h->ev[4], h->tev[i][1]));
+    kind[i] = h->tkind[i];
+    stream[i] = h->tslot[i];
+    begin_ms[i] = b;
+    end_ms[i] = e;
+  }
+  if (n) *n = m;
   return 0;
 }
 

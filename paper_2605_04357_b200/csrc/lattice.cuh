@@ -308,7 +308,9 @@ struct LatWork {
   }
 };
 
-// value_S[idx][j], j = 1..Lu (kernels.py:164-170) for S in [S_lo, S_lo + gridDim.y).
+// value_S[idx][j], j = 1..Lu (kernels.py:164-170) for S in [S_lo, S_lo + gridDim.y);
+// warp per row, lanes over j. Column 0 (never read as a value) receives J, the last j
+// with value > 0, for dp_pair's search cap.
 // Only rows some reader can touch: u is one stage of a candidate whose other S - 1
 // stages hold >= 1 node each, so |candidate| >= |u| + S - 1 <= maxn(u) -- true for
 // every u the layers (maxn(u) >= maxn(X)), the layer-2 X - u side and the top cell
@@ -320,20 +322,29 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
                                  int S_lo, unsigned smask, LatWork W) {
   const int S = S_lo + blockIdx.y;
   if (!((smask >> S) & 1u)) return;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long idx = t / Lu;
-  const int j = (int)(t - idx * Lu) + 1;
+  const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (idx >= L.base[L.R + 1]) return;
-  const double* tabS = tab_mp + (long long)(S - 1) * K * Lu;
-  int cfg[kMaxC], cnt[kMaxC];
   const unsigned long long key = state_key[idx];
   int n = 0;
-  for (int t2 = 0; t2 < kMaxC; ++t2) n += (int)((key >> (9 * t2)) & 7u);
-  if ((int)maxn[idx] < n + S - 1) return;
+  for (int t = 0; t < kMaxC; ++t) n += (int)((key >> (9 * t)) & 7u);
+  if ((int)maxn[idx] < n + S - 1) return;  // uniform per warp
+  const double* tabS = tab_mp + (long long)(S - 1) * K * Lu;
+  int cfg[kMaxC], cnt[kMaxC];
   const int C = lat_tokens(inv_rank, key, cfg, cnt);
-  double v = 0.0;
-  for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], tabS[cfg[c] * Lu + (j - 1)]));
-  W.val(S)[idx * (Lu + 1) + j] = v;
+  double* row = W.val(S) + idx * (Lu + 1);
+  int J = 0;
+  for (int j0 = 1; j0 <= Lu; j0 += 32) {
+    const int j = j0 + lane;
+    double v = 0.0;
+    if (j <= Lu) {
+      for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], tabS[cfg[c] * Lu + (j - 1)]));
+      row[j] = v;
+    }
+    const unsigned pos = __ballot_sync(0xffffffffu, j <= Lu && v > 0.0);
+    if (pos) J = j0 + 31 - __clz(pos);
+  }
+  if (lane == 0) row[0] = (double)J;
 }
 
 // DP layer sg for every S in [S_lo, S_lo + gridDim.y) with S > sg: warp per state X,
@@ -360,6 +371,7 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
   // is the true max, so cand(u) == cand(X-u) (j <-> l-j); the smallest maximising
   // code lies in the lower half (code(X-u) = M-1-code(u)) and only it is searched.
   const long long cmax = (sg == 2 && ((xmask >> S) & 1u)) ? (M - 1) / 2 + 1 : M;
+  const bool cap = (xmask >> S) & 1u;  // exactly monotone rows: capped crossing search
   const double* __restrict__ value = W.val(S);
   const double* __restrict__ fprev = W.lay(S, sg - 1);
   double* __restrict__ fout = W.lay(S, sg);
@@ -374,6 +386,7 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
   }
   const unsigned vmask = __ballot_sync(0xffffffffu, ok);
   const int nv = __popc(vmask);
+  int kpos = 0;  // last l with f > 0 -> column 0 of the f row (dp_pair's search cap)
   // census (bench roofline, off in timed runs): algorithmic bytes of this state = its
   // f + choice cells written (10 B each), one read of its value_S and f_{sg-1} rows
   // and of its valid sub-table entries
@@ -401,7 +414,7 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
       double cand;
       int cj;
       dp_pair(value + (long long)(ex & 0xFFFFFFu) * LuP, fprev + (long long)ey * LuP, l, jmax, true,
-              cand, cj);
+              cand, cj, cap);
       if (cand > best) { best = cand; bu = pos + 1; bj = cj; }
     }
     // merge the groups of each l: value desc, then smallest code (the reference's
@@ -416,7 +429,10 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
       fout[idx * LuP + l] = best;
       chout[idx * LuP + l] = (unsigned short)((bu << 10) | bj);
     }
+    const unsigned pos = __ballot_sync(0xffffffffu, act && g == 0 && best > 0.0);  // group 0 = lanes 0..wp-1
+    if (pos) kpos = l0 + 31 - __clz(pos);
   }
+  if (lane == 0) fout[idx * LuP] = (double)kpos;
 }
 
 }  // namespace coral

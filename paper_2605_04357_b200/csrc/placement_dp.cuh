@@ -148,22 +148,37 @@ __device__ inline void dp_build_value(const DpShared& sh, const DpBuffers& B) {
 // One (u, l) pair of the reference's per-cell rule: crossing of g(j) = gv[j]
 // (non-increasing) and h(j) = hv[l-j] (non-decreasing) for j in [1, jmax].
 // kernels.py:210-249, literally (including the branch order and tie choices).
+//
+// cap (lattice tables with exactly non-increasing rows only): column 0 of every value
+// and f row holds its last positive index (J for g = value[u], K for the h source row:
+// f[Y][m] = 0 for m > K, and every DP cell is >= 0). So P(j) = g(j) > h(j) is false
+// for j > J (g = 0 <= h) and true for j <= J with j < l - K (g > 0 = h). With exactly
+// monotone rows P is monotone and its boundary unique, so searching from
+// lo = min(J, l - K - 1), hi = J + 1 (clamped to [1, jmax]) returns the reference
+// search's (lo, hi) in fewer probes. (Past the two shortcuts P(1) is true and P(jmax)
+// false, so J >= 1 and the clamped bracket is never empty.)
 __device__ __forceinline__ void dp_pair(const double* __restrict__ gv,
                                         const double* __restrict__ hv, int l, int jmax,
-                                        bool mono, double& cand, int& cj) {
+                                        bool mono, double& cand, int& cj, bool cap = false) {
   if (mono) {
+    const double* __restrict__ hl = hv + l;  // hv[l - j] == hl[-j]: one address op per probe
+    const double g0 = cap ? gv[0] : 0.0, h0 = cap ? hv[0] : 0.0;
     const double g1 = gv[1];
-    const double h1 = hv[l - 1];
+    const double h1 = hl[-1];
     if (g1 <= h1) { cand = g1; cj = 1; return; }
     const double gm = gv[jmax];
-    const double hm = hv[l - jmax];
+    const double hm = hl[-jmax];
     if (gm >= hm) { cand = hm; cj = jmax; return; }
     int lo = 1, hi = jmax;
+    if (cap) {
+      hi = min(jmax, (int)g0 + 1);
+      lo = max(1, min(min((int)g0, l - (int)h0 - 1), hi - 1));
+    }
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (gv[mid] > hv[l - mid]) lo = mid; else hi = mid;
+      if (gv[mid] > hl[-mid]) lo = mid; else hi = mid;
     }
-    const double vlo = hv[l - lo];
+    const double vlo = hl[-lo];
     const double vhi = gv[hi];
     if (vlo >= vhi) { cand = vlo; cj = lo; } else { cand = vhi; cj = hi; }
   } else {

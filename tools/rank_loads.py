@@ -45,7 +45,7 @@ def main():
                 if not m:
                     continue
                 nc = int(counts[mp // 2])
-                pred += chain_fixed(nc) + sum(unit_cost(nc, int(lsteps[mp // 2]), S)
+                pred += chain_fixed(nc) + sum(unit_cost(nc, int(lsteps[mp // 2]), S, mp % 2)
                                               for S in range(1, 7) if m >> S & 1)
             ts = []
             for _ in range(6):
