@@ -387,6 +387,11 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
   const unsigned vmask = __ballot_sync(0xffffffffu, ok);
   const int nv = __popc(vmask);
   int kpos = 0;  // last l with f > 0 -> column 0 of the f row (dp_pair's search cap)
+  // compact once per state: lane k holds the k-th valid code (ascending) and the
+  // 32-bit row offsets of its value_S[u] and f[X-u] rows (< 2^32 in the envelope)
+  const int cpos = lane < nv ? (int)__fns(vmask, 0, lane + 1) : 0;
+  const unsigned cvo = (__shfl_sync(0xffffffffu, myent.x, cpos) & 0xFFFFFFu) * (unsigned)LuP;
+  const unsigned cfo = __shfl_sync(0xffffffffu, myent.y, cpos) * (unsigned)LuP;
   // census (bench roofline, off in timed runs): algorithmic bytes of this state = its
   // f + choice cells written (10 B each), one read of its value_S and f_{sg-1} rows
   // and of its valid sub-table entries
@@ -407,14 +412,14 @@ __global__ void __launch_bounds__(256) lat_layer_kernel(
     const int T = (nv + G - 1) / G;
     for (int t = 0; t < T; ++t) {
       const int kk = t * G + g;  // this group's kk-th valid code (ascending per group)
-      const int pos = kk < nv ? (int)__fns(vmask, 0, kk + 1) : 0;
-      const unsigned ex = __shfl_sync(0xffffffffu, myent.x, pos);
-      const unsigned ey = __shfl_sync(0xffffffffu, myent.y, pos);
+      const int src = kk < nv ? kk : 0;
+      const unsigned vo = __shfl_sync(0xffffffffu, cvo, src);
+      const unsigned fo = __shfl_sync(0xffffffffu, cfo, src);
+      const int pos = __shfl_sync(0xffffffffu, cpos, src);
       if (!act || kk >= nv) continue;
       double cand;
       int cj;
-      dp_pair(value + (long long)(ex & 0xFFFFFFu) * LuP, fprev + (long long)ey * LuP, l, jmax, true,
-              cand, cj, cap);
+      dp_pair(value + vo, fprev + fo, l, jmax, true, cand, cj, cap);
       if (cand > best) { best = cand; bu = pos + 1; bj = cj; }
     }
     // merge the groups of each l: value desc, then smallest code (the reference's
