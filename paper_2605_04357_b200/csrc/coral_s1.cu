@@ -473,8 +473,9 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
   const int Smax = min(n, Lu);
   // this lane's u codes (lane+1, lane+33): size, idx(u), idx(full-u) from the model's
   // rank table (code M-1-c is the complement of code c)
+  // (row offsets idx * LuP fit 32 bits in the GPU envelope)
   int su[2];
-  long long ru[2], rr[2];
+  unsigned ru[2], rr[2];
   const unsigned* rk = A.ranks + ci * 64;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
@@ -484,8 +485,8 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
     if (code < M) {
       const unsigned e = rk[code], ec = rk[M - 1 - code];
       su[k] = (int)(e >> 24);
-      ru[k] = e & 0xFFFFFFu;
-      rr[k] = ec & 0xFFFFFFu;
+      ru[k] = (e & 0xFFFFFFu) * (unsigned)LuP;
+      rr[k] = (ec & 0xFFFFFFu) * (unsigned)LuP;
     }
   }
   // S ascending; strict improvement (templates.py:322) -> smaller S on ties
@@ -509,7 +510,7 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
       if (su[k] > n - (S - 1) || lane + 1 + 32 * k > chalf) continue;
       double cand;
       int cj;
-      dp_pair(val + ru[k] * LuP, lay + rr[k] * LuP, Lu, Lu - (S - 1), true, cand, cj, cap);
+      dp_pair(val + ru[k], lay + rr[k], Lu, Lu - (S - 1), true, cand, cj, cap);
       if (cand > best) { best = cand; bu = lane + 1 + 32 * k; bj = cj; }
     }
     warp_argmax_code(best, bu, bj);

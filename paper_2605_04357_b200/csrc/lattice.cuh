@@ -349,7 +349,7 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
 
 // DP layer sg for every S in [S_lo, S_lo + gridDim.y) with S > sg: warp per state X,
 // lanes over l. Cells: sg <= |X| <= maxn(X) - (S - sg), sg <= l <= Lu - (S - sg).
-__global__ void __launch_bounds__(256) lat_layer_kernel(
+__global__ void __launch_bounds__(256, 8) lat_layer_kernel(
     LatModel L, int sg, int S_lo, unsigned smask, unsigned xmask, int n_max, int Lu,
     const unsigned* __restrict__ maxn, const long long* __restrict__ off,
     const uint2* __restrict__ subtab, LatWork W, unsigned long long* __restrict__ census) {
