@@ -269,7 +269,7 @@ def main():
     from paper_2605_04357_b200 import _native, build_frontier, catalog
     from paper_2605_04357_b200.frontier import _merge_across_ranks, _price_matrix
     from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem
-    from paper_2605_04357_b200.shard import assign_units
+    from paper_2605_04357_b200.shard import assign_units, table_posfrac
 
     w = catalog.WORKLOADS[args.workload]()
     caps, ctx = LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf, granularity=w.granularity)
@@ -287,7 +287,8 @@ def main():
         if world > 1:
             prob.counts = h.num_combos()
             _, lsteps, smax = h.table_layout()
-            masks = assign_units(prob.counts, lsteps, smax, NP, world)[rank]
+            masks = assign_units(prob.counts, lsteps, smax, NP, world,
+                                 table_posfrac(h, len(prob.configs)))[rank]
             h.evaluate_units(masks)
             n_local = h.frontier(pmat)
             return _merge_across_ranks(prob, n_local, tdist)

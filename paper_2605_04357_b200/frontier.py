@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _native
 from .library import GenContext, Stage1Problem, TemplateLibrary, library_meta
-from .shard import assign_units
+from .shard import assign_units, table_posfrac
 from .specs import PHASES, NodeComboKey, Placement, ServingTemplate
 
 
@@ -133,7 +133,8 @@ def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,
         for mp in range(len(prob.models) * NP):
             prob.cand_off[mp + 1] = prob.cand_off[mp] + prob.counts[mp // NP]
         _, lsteps, smax = prob.h.table_layout()
-        masks = assign_units(prob.counts, lsteps, smax, NP, tdist.get_world_size())
+        masks = assign_units(prob.counts, lsteps, smax, NP, tdist.get_world_size(),
+                             table_posfrac(prob.h, len(prob.configs)))
         prob.h.evaluate_units(masks[tdist.get_rank()])
         n_local = prob.h.frontier(pmat)
         n = _merge_across_ranks(prob, n_local, tdist)

@@ -5,57 +5,123 @@ cells, and a candidate's best over S is combined with an order-independent rule
 (ties -> fewer stages), so any rank may own any subset of S values of a (model,
 phase). A rank that owns at least one S of a (model, phase) also pays that chain's
 fixed part (its top-cell setup per candidate, memory-window table, decode, launches),
-so the greedy below charges the fixed part once per (rank, chain) and keeps the S
-values of a chain together unless splitting balances better.
+so assign_units places whole chains first and splits one only where moving an S unit
+lowers the peak load by more than the repeated fixed part.
 
-Cost model (milliseconds on one B200, calibrated with tools/calibrate_units.py on
-BASELINE config 2, profiles/r01_calibration.txt):
-  fixed(chain)  = 0.09 + 1.4e-6 * candidates
-  unit(chain,S) = 6.8e-8 * candidates * layer_units * W[S] * PHASE_W[phase]
+Cost model (milliseconds on one B200, fitted by tools/fit_shard.py to the unit and
+chain timings of tools/calibrate_units.py on BASELINE config 2,
+profiles/r01_calibration_v2.txt; relative rms error 0.18):
+  fixed(chain)  = 0.045 + 9.0e-7 * candidates
+  unit(chain,S) = 0.032 + 2.42e-8 * candidates * layer_units * W[S] * (1 + 2.2 * p[S])
 
-PHASE_W: prefill chains of the same model measure 1.01-1.37x their decode twins
-(profiles/r01_calibration.txt: more crossing searches survive the dp_pair end-point
-shortcuts). Without a weight the two phases tie in the greedy and land on
-alternating ranks, so every prefill chain piles onto the same ranks; 1.1 balanced
-best over 2, 4 and 8 ranks (tools/sweep_phase_w.sh).
+p[S] is the fraction of positive entries of the chain's T-hat table at S (read from
+the device tables before the split). Rows that fall to zero early let the capped
+crossing searches stop early (csrc/placement_dp.cuh), so a chain's per-pair cost
+tracks p: decode chains of the big models (p ~ 0.05-0.3) cost 1.2-1.6x less than their
+prefill twins (p ~ 0.4-0.6). Without p the two phases tie in the greedy and land on
+alternating ranks, so every prefill chain piles onto the same ranks.
 """
 
 from __future__ import annotations
 
-import os
+import numpy as np
 
-W = {1: 0.01, 2: 0.22, 3: 0.8, 4: 1.0, 5: 0.7, 6: 0.45}
-PHASE_W = (float(os.environ.get("CORAL_SHARD_PREFILL_W", "1.1")), 1.0)  # (prefill, decode)
+W = {1: 0.0, 2: 0.075, 3: 0.71, 4: 1.0, 5: 0.79, 6: 0.59}
+OVERLAP = 0.8  # a rank with >= 3 chains runs them concurrently on 4 streams: ~0.8x their sum
 
 
 def chain_fixed(ncombo: int) -> float:
-    return 0.09 + 1.4e-6 * ncombo
+    return 0.045 + 9.0e-7 * ncombo
 
 
-def unit_cost(ncombo: int, lsteps: int, S: int, phase: int = 1) -> float:
-    return 6.8e-8 * ncombo * lsteps * W.get(S, 0.5) * PHASE_W[phase if phase < len(PHASE_W) else 1] + 0.005
+def unit_cost(ncombo: int, lsteps: int, S: int, posfrac: float = 0.5) -> float:
+    if S == 1:
+        return 0.005
+    return 0.032 + 2.42e-8 * ncombo * lsteps * W.get(S, 0.6) * (1.0 + 2.2 * posfrac)
 
 
-def assign_units(counts, lsteps, smax, num_phases: int, world: int) -> list:
-    """-> per rank, a list of S bit-masks indexed by mp = model * num_phases + phase."""
-    units = []
+def table_posfrac(handle, num_configs: int) -> list:
+    """Per (model, phase) chain, {S: fraction of positive T-hat entries} from the
+    device tables (layout of coral_s1_table_layout: per chain [S][config][unit])."""
+    tabs, offs, lsteps = handle.get_tables()
+    nmp = len(offs) - 1
+    NP = nmp // max(len(lsteps), 1)
+    out = []
+    for mp in range(nmp):
+        lu = int(lsteps[mp // NP]) if len(lsteps) else 0
+        blk = tabs[int(offs[mp]):int(offs[mp + 1])]
+        if not lu or not num_configs or not blk.size:
+            out.append({})
+            continue
+        rows = blk.reshape(-1, num_configs * lu)
+        out.append({S: float(np.count_nonzero(rows[S - 1] > 0)) / rows.shape[1] for S in range(1, rows.shape[0] + 1)})
+    return out
+
+
+def assign_units(counts, lsteps, smax, num_phases: int, world: int, posfrac=None) -> list:
+    """-> per rank, a list of S bit-masks indexed by mp = model * num_phases + phase.
+    posfrac: table_posfrac() of the problem (None: 0.5 everywhere).
+
+    Whole chains first (longest-processing-time order onto the least loaded rank),
+    then single S units move from the most to the least loaded rank while that lowers
+    the larger of the two loads; a rank receiving a piece of a chain pays the chain's
+    fixed part again, so chains split only where the balance gains more than that."""
+    nmp = len(counts) * num_phases
+    unit = {}   # mp -> {S: cost}
+    fixed = {}
     for m, (nc, lu, sm) in enumerate(zip(counts, lsteps, smax)):
         if not nc:
             continue
         for p in range(num_phases):
+            mp = m * num_phases + p
+            unit[mp] = {}
             for S in range(1, min(int(sm), int(lu)) + 1):
-                units.append((unit_cost(int(nc), int(lu), S, p if num_phases == 2 else 1), m * num_phases + p, S))
-    units.sort(key=lambda u: -u[0])  # stable: ties keep (mp, S) order
-    load = [0.0] * world
-    nmp = len(counts) * num_phases
+                pf = posfrac[mp].get(S, 0.5) if posfrac is not None else 0.5
+                unit[mp][S] = unit_cost(int(nc), int(lu), S, pf)
+            fixed[mp] = chain_fixed(int(nc))
     masks = [[0] * nmp for _ in range(world)]
-    for cost, mp, S in units:
-        fixed = chain_fixed(int(counts[mp // num_phases]))
+    raw = [0.0] * world
+    nch = [0] * world
 
-        def after(r):
-            return load[r] + cost + (0.0 if masks[r][mp] else fixed)
+    def eff(load, n):  # chains of one rank overlap on its streams (OVERLAP)
+        return load * (1.0 if n <= 2 else OVERLAP)
 
-        r = min(range(world), key=lambda i: (after(i), i))
-        load[r] = after(r)
-        masks[r][mp] |= 1 << S
+    chains = sorted(unit, key=lambda mp: (-(fixed[mp] + sum(unit[mp].values())), mp))
+    for mp in chains:
+        c = fixed[mp] + sum(unit[mp].values())
+        r = min(range(world), key=lambda i: (eff(raw[i] + c, nch[i] + 1), i))
+        masks[r][mp] = sum(1 << S for S in unit[mp])
+        raw[r] += c
+        nch[r] += 1
+    for _ in range(4 * len(unit) * 6):
+        load = [eff(raw[i], nch[i]) for i in range(world)]
+        hi = max(range(world), key=lambda i: (load[i], -i))
+        best = None
+        for lo in range(world):
+            if lo == hi:
+                continue
+            for mp in range(nmp):
+                mk = masks[hi][mp]
+                if not mk:
+                    continue
+                for S, c in unit[mp].items():
+                    if not (mk >> S) & 1:
+                        continue
+                    gone = mk == (1 << S)  # hi drops the chain entirely
+                    new_hi = eff(raw[hi] - c - (fixed[mp] if gone else 0.0), nch[hi] - gone)
+                    new_lo = eff(raw[lo] + c + (0.0 if masks[lo][mp] else fixed[mp]),
+                                 nch[lo] + (0 if masks[lo][mp] else 1))
+                    peak = max(new_hi, new_lo)
+                    if peak < load[hi] - 1e-6 and (best is None or peak < best[0]):
+                        best = (peak, lo, mp, S, gone)
+        if best is None:
+            break
+        _, lo, mp, S, gone = best
+        c = unit[mp][S]
+        raw[hi] -= c + (fixed[mp] if gone else 0.0)
+        nch[hi] -= int(gone)
+        raw[lo] += c + (0.0 if masks[lo][mp] else fixed[mp])
+        nch[lo] += 0 if masks[lo][mp] else 1
+        masks[hi][mp] &= ~(1 << S)
+        masks[lo][mp] |= 1 << S
     return masks

@@ -12,7 +12,7 @@ import torch.distributed as tdist  # noqa: E402
 from paper_2605_04357_b200 import catalog  # noqa: E402
 from paper_2605_04357_b200.frontier import _merge_across_ranks, _price_matrix, materialise  # noqa: E402
 from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem, library_meta  # noqa: E402
-from paper_2605_04357_b200.shard import assign_units  # noqa: E402
+from paper_2605_04357_b200.shard import assign_units, table_posfrac  # noqa: E402
 
 
 def main():
@@ -44,7 +44,8 @@ def main():
             prob.cand_off[mp + 1] = prob.cand_off[mp] + prob.counts[mp // NP]
         mark("tables+enum")
         _, lsteps, smax = prob.h.table_layout()
-        prob.h.evaluate_units(assign_units(prob.counts, lsteps, smax, NP, tdist.get_world_size())[tdist.get_rank()])
+        prob.h.evaluate_units(assign_units(prob.counts, lsteps, smax, NP, tdist.get_world_size(),
+                                            table_posfrac(prob.h, len(prob.configs)))[tdist.get_rank()])
         mark("evaluate")
         n_local = prob.h.frontier(pm)
         mark("local frontier")

@@ -23,7 +23,7 @@ def main():
     _, pm = _price_matrix(prob.configs, w.prices, w.regions)
     shard = None
     if "--rank" in sys.argv:  # emulate one rank of a multi-GPU solve on this device
-        from paper_2605_04357_b200.shard import assign_units
+        from paper_2605_04357_b200.shard import assign_units, table_posfrac
         shard = (int(sys.argv[sys.argv.index("--rank") + 1]), int(sys.argv[sys.argv.index("--world") + 1]))
     for _ in range(solves):
         if shard is None:
@@ -34,7 +34,8 @@ def main():
             prob.counts = prob.h.num_combos()
             _, lsteps, smax = prob.h.table_layout()
             prob.cand_off = [0]
-            prob.h.evaluate_units(assign_units(prob.counts, lsteps, smax, 2, shard[1])[shard[0]])
+            prob.h.evaluate_units(assign_units(prob.counts, lsteps, smax, 2, shard[1],
+                                               table_posfrac(prob.h, len(prob.configs)))[shard[0]])
         n = prob.h.frontier(pm)
     torch.cuda.synchronize()
     print(name, prob.h.num_candidates(), "candidates;", n, "survivors;", prob.h.stage_ms())

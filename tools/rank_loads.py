@@ -9,7 +9,7 @@ import torch  # noqa: E402
 
 from paper_2605_04357_b200 import catalog  # noqa: E402
 from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem  # noqa: E402
-from paper_2605_04357_b200.shard import assign_units, chain_fixed, unit_cost  # noqa: E402
+from paper_2605_04357_b200.shard import assign_units, chain_fixed, table_posfrac, unit_cost  # noqa: E402
 
 
 def main():
@@ -27,8 +27,9 @@ def main():
     _, lsteps, smax = prob.h.table_layout()
     print("counts", list(counts), "lsteps", list(lsteps), "smax", list(smax))
     full = [sum(1 << S for S in range(1, 7))] * (len(counts) * 2)
+    pf = table_posfrac(prob.h, len(prob.configs))
     if only is not None:
-        mk = assign_units(counts, lsteps, smax, 2, only[0])[only[1]] if only[0] > 1 else full
+        mk = assign_units(counts, lsteps, smax, 2, only[0], pf)[only[1]] if only[0] > 1 else full
         for _ in range(3):
             prob.h.evaluate_units(mk)
         torch.cuda.synchronize()
@@ -38,14 +39,14 @@ def main():
         torch.cuda.profiler.stop()
         return
     for world in [1] + worlds:
-        masks = [full] if world == 1 else assign_units(counts, lsteps, smax, 2, world)
+        masks = [full] if world == 1 else assign_units(counts, lsteps, smax, 2, world, pf)
         for r, mk in enumerate(masks):
             pred = 0.0
             for mp, m in enumerate(mk):
                 if not m:
                     continue
                 nc = int(counts[mp // 2])
-                pred += chain_fixed(nc) + sum(unit_cost(nc, int(lsteps[mp // 2]), S, mp % 2)
+                pred += chain_fixed(nc) + sum(unit_cost(nc, int(lsteps[mp // 2]), S, pf[mp].get(S, 0.5))
                                               for S in range(1, 7) if m >> S & 1)
             ts = []
             for _ in range(6):
