@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
   const int C = lat_tokens(A.inv_rank, A.keys[ci], cfg, cnt);
   int M = 1, n = 0;
   for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; }
-  const int Lu = A.Lu, LuP = Lu + 1;
+  const int Lu = A.Lu, LuP = lat_pitch(Lu);
   const int Smax = min(n, Lu);
   // this lane's u codes (lane+1, lane+33): size, idx(u), idx(full-u) from the model's
   // rank table (code M-1-c is the complement of code c)
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(256) lat_decode_kernel(TopArgs A) {
   const int C = lat_tokens(A.inv_rank, A.keys[ci], cfg, cnt);
   int n = 0;
   for (int c = 0; c < C; ++c) n += cnt[c];
-  const int Lu = A.Lu, LuP = Lu + 1;
+  const int Lu = A.Lu, LuP = lat_pitch(Lu);
   int sj[kMaxC], sc[kMaxC][kMaxC];
   if (twin == 1) {
     sj[0] = Lu;
@@ -1461,7 +1461,7 @@ static int lattice_prepare(coral_s1_handle* h) {
     }
   }
   // workspaces
-  const long long LuP = h->maxLu + 1;
+  const long long LuP = lat_pitch(h->maxLu);
   const long long nS = std::max(h->n_max - 1, 1);                         // S = 2..n_max
   const long long nch = std::max((h->n_max - 2) * (h->n_max - 1) / 2, 1);  // (S, sg) choice layers
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
@@ -1479,7 +1479,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   cudaStream_t st = h->side[slot];
   const int m = mp / h->NP;
   const int K = h->K, Lu = h->Lu[m];
-  const long long ns = h->lat_states, LuP = h->maxLu + 1;
+  const long long ns = h->lat_states, LuP = lat_pitch(h->maxLu);
   const long long ncombo = h->counts[m];
   if (!ncombo) return 0;
   LatModel L{K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
@@ -1504,7 +1504,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   W.value = h->ws_value[slot].as<double>();
   W.f = h->ws_f0[slot].as<double>();
   W.ch = h->ws_ch[slot].as<unsigned short>();
-  W.stride = ns * (Lu + 1);
+  W.stride = ns * lat_pitch(Lu);
   (void)LuP;
   const double* tab_mp = h->tab.as<double>() + h->tab_off[mp];
   if (Smax >= 2 && ns > 0) {

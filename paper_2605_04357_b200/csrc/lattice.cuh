@@ -30,6 +30,11 @@ namespace coral {
 
 constexpr int kLatMaxState = kMaxC - 1;  // lattice tables hold |X| <= 5
 
+// Row pitch of the lattice value / f / choice tables: Lu + 1 rounded up to even, so
+// every row starts 16-byte aligned and dp_pair's capped search fetches (J, g[1]) with
+// one vector load (column 0 holds J / K, columns 1..Lu the values).
+__host__ __device__ constexpr int lat_pitch(int Lu) { return (Lu + 2) & ~1; }
+
 struct LatModel {
   int K, R;                 // configs, largest state size (n_max - 1)
   const long long* base;    // [R + 2]: first index of each size (base[1] = 0), base[R+1] = total
@@ -332,7 +337,7 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
   const double* tabS = tab_mp + (long long)(S - 1) * K * Lu;
   int cfg[kMaxC], cnt[kMaxC];
   const int C = lat_tokens(inv_rank, key, cfg, cnt);
-  double* row = W.val(S) + idx * (Lu + 1);
+  double* row = W.val(S) + idx * lat_pitch(Lu);
   int J = 0;
   for (int j0 = 1; j0 <= Lu; j0 += 32) {
     const int j = j0 + lane;
@@ -344,7 +349,7 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
     const unsigned pos = __ballot_sync(0xffffffffu, j <= Lu && v > 0.0);
     if (pos) J = j0 + 31 - __clz(pos);
   }
-  if (lane == 0) row[0] = (double)J;
+  if (lane == 0) row[0] = __longlong_as_double((long long)J);  // J as integer bits
 }
 
 // DP layer sg for every S in [S_lo, S_lo + gridDim.y) with S > sg: warp per state X,
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
   int s = sg;
   while (idx >= L.base[s + 1]) ++s;
   if (s > (int)maxn[idx] - (S - sg)) return;  // no candidate reaches this cell
-  const int LuP = Lu + 1;
+  const int LuP = lat_pitch(Lu);
   const int lmax = Lu - (S - sg);
   const int usz = s - (sg - 1);  // |u| <= |X| - (sg - 1)
   const long long o = off[idx];
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
   // f + choice cells written (10 B each), one read of its value_S and f_{sg-1} rows
   // and of its valid sub-table entries
   if (census && lane == 0)
-    atomicAdd(census, (unsigned long long)(10 * (lmax - sg + 1) + 16 * LuP + 8 * nv));
+    atomicAdd(census, (unsigned long long)(10 * (lmax - sg + 1) + 16 * (Lu + 1) + 8 * nv));
   for (int l0 = sg; l0 <= lmax; l0 += 32) {
     // lanes = G groups x wp positions; group g takes valid codes g, g+G, g+2G, ...
     const int w = min(32, lmax - l0 + 1);
@@ -437,7 +442,7 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
     const unsigned pos = __ballot_sync(0xffffffffu, act && g == 0 && best > 0.0);  // group 0 = lanes 0..wp-1
     if (pos) kpos = l0 + 31 - __clz(pos);
   }
-  if (lane == 0) fout[idx * LuP] = (double)kpos;
+  if (lane == 0) fout[idx * LuP] = __longlong_as_double((long long)kpos);  // K as integer bits
 }
 
 }  // namespace coral

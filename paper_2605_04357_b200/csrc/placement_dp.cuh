@@ -162,8 +162,17 @@ __device__ __forceinline__ void dp_pair(const double* __restrict__ gv,
                                         bool mono, double& cand, int& cj, bool cap = false) {
   if (mono) {
     const double* __restrict__ hl = hv + l;  // hv[l - j] == hl[-j]: one address op per probe
-    const double g0 = cap ? gv[0] : 0.0, h0 = cap ? hv[0] : 0.0;
-    const double g1 = gv[1];
+    // capped rows are 16-byte aligned (lat_pitch): (J, g[1]) in one vector load; J and
+    // K are stored as integer bits in the double slots
+    double g0 = 0.0, g1, h0 = 0.0;
+    if (cap) {
+      const double2 g01 = *reinterpret_cast<const double2*>(gv);
+      g0 = g01.x;
+      g1 = g01.y;
+      h0 = hv[0];
+    } else {
+      g1 = gv[1];
+    }
     const double h1 = hl[-1];
     if (g1 <= h1) { cand = g1; cj = 1; return; }
     const double gm = gv[jmax];
@@ -171,8 +180,9 @@ __device__ __forceinline__ void dp_pair(const double* __restrict__ gv,
     if (gm >= hm) { cand = hm; cj = jmax; return; }
     int lo = 1, hi = jmax;
     if (cap) {
-      hi = min(jmax, (int)g0 + 1);
-      lo = max(1, min(min((int)g0, l - (int)h0 - 1), hi - 1));
+      const int J = __double2loint(g0), K = __double2loint(h0);
+      hi = min(jmax, J + 1);
+      lo = max(1, min(min(J, l - K - 1), hi - 1));
     }
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
