@@ -139,6 +139,9 @@ int coral_s1_table_layout(const coral_s1_handle* h, int64_t* offsets, int32_t* l
                           int32_t* smax);
 int coral_s1_get_tables(coral_s1_handle* h, double* out, int64_t n);
 int coral_s1_get_budgets(coral_s1_handle* h, double* out, int64_t n); /* [mp][n_max] */
+/* fraction of positive T-hat entries per (mp, S), [mp][n_max] (S > smax: 0); input of
+ * the multi-GPU shard cost model (paper_2605_04357_b200/shard.py) */
+int coral_s1_table_posfrac(coral_s1_handle* h, double* out, int64_t n);
 
 /* ---- enumeration: enumerate_combos (templates.py:99-113) -------------- */
 int coral_s1_enumerate(coral_s1_handle* h);

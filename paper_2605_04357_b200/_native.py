@@ -107,6 +107,7 @@ def load():
             "coral_s1_stage_ms": (C.c_int, [vp, _f64p, _f64p, _f64p, _f64p]),
             "coral_s1_kernel_stats": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
             "coral_s1_set_census": (C.c_int, [vp, C.c_int]),
+            "coral_s1_table_posfrac": (C.c_int, [vp, _f64p, C.c_int64]),
             "coral_s1_kernel_timeline": (C.c_int, [vp, C.c_int64, _i32p, _i32p, _f64p, _f64p, _i64p]),
             "coral_s1_census": (C.c_int, [vp, _i64p]),
             "coral_s1_write_library": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_int, _i32p,
@@ -238,6 +239,12 @@ class Handle:
         out = np.zeros(max(int(offs[-1]), 1))
         _check(self._lib.coral_s1_get_tables(self._h, _ptr(out, C.c_double), out.size))
         return out, offs, ls
+
+    def table_posfrac(self):
+        """[mp][n_max] fraction of positive T-hat entries (device-counted by the tables kernel)."""
+        out = np.zeros(max(self.NM * self.NP * self.n_max, 1))
+        _check(self._lib.coral_s1_table_posfrac(self._h, _ptr(out, C.c_double), out.size))
+        return out[:self.NM * self.NP * self.n_max].reshape(self.NM * self.NP, self.n_max)
 
     def get_budgets(self):
         out = np.zeros(max(self.NM * self.NP * self.n_max, 1))

@@ -130,6 +130,7 @@ struct coral_s1_handle {
   // layer-kernel census (coral_s1_set_census): algorithmic bytes of the last evaluate
   bool census_on = false;
   DevBuf census;
+  DevBuf poscnt;  // positive T-hat entries per (mp, S)
 };
 
 namespace {
@@ -141,7 +142,8 @@ namespace {
 // --------------------------------------------------------------------------------
 __global__ void tables_kernel(DevProblem P, const int64_t* __restrict__ tab_off,
                               double* __restrict__ tab, unsigned char* __restrict__ flags,
-                              double* __restrict__ budgets) {
+                              double* __restrict__ budgets, unsigned* __restrict__ poscnt) {
+  __shared__ unsigned npos;
   const int c = blockIdx.x;
   const int S = blockIdx.y + 1;
   const int mp = blockIdx.z;
@@ -157,7 +159,11 @@ __global__ void tables_kernel(DevProblem P, const int64_t* __restrict__ tab_off,
     // templates.py:89-95: zeros when the budget is exhausted
     row[jj] = (budget <= 0.0) ? 0.0 : node_max_throughput(P, c, m, phase, (jj + 1) * g, budget);
   }
+  if (threadIdx.x == 0) npos = 0;
   __syncthreads();
+  unsigned mine = 0;  // positive entries (shard cost model, coral_s1_table_posfrac)
+  for (int jj = threadIdx.x; jj < Lu; jj += blockDim.x) mine += row[jj] > 0.0;
+  if (mine) atomicAdd(&npos, mine);
   int tol = 1, exact = 1;
   for (int jj = threadIdx.x; jj + 1 < Lu; jj += blockDim.x) {
     const double d = rn_sub(row[jj + 1], row[jj]);  // np.diff
@@ -166,8 +172,10 @@ __global__ void tables_kernel(DevProblem P, const int64_t* __restrict__ tab_off,
   }
   tol = __syncthreads_and(tol);
   exact = __syncthreads_and(exact);
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
     flags[((int64_t)mp * P.n_max + (S - 1)) * P.K + c] = (unsigned char)(tol | (exact << 1));
+    if (npos) atomicAdd(poscnt + (int64_t)mp * P.n_max + (S - 1), npos);
+  }
 }
 
 // --------------------------------------------------------------------------------
@@ -1051,7 +1059,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
                     &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
-                    &h->lat_sub, &h->lat_maxn, &h->census, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};
+                    &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release(); h->ws_ranks[i].release();
@@ -1186,20 +1194,40 @@ int coral_s1_tables(coral_s1_handle* h) {
   if ((rc = h->tab.ensure(std::max<int64_t>(h->tab_off[NMP], 1) * 8)) ||
       (rc = h->flags.ensure(std::max<int64_t>((int64_t)NMP * h->n_max * h->K, 1))) ||
       (rc = h->budget.ensure(std::max<int64_t>((int64_t)NMP * h->n_max, 1) * 8)) ||
+      (rc = h->poscnt.ensure(std::max<int64_t>((int64_t)NMP * h->n_max, 1) * 4)) ||
       (rc = upload(h, h->tab_off_d, h->tab_off)))
     return rc;
   CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
   if (NMP > 0 && h->K > 0) {
     CUDA_TRY(cudaMemsetAsync(h->budget.p, 0, (size_t)NMP * h->n_max * 8, h->stream));
+    CUDA_TRY(cudaMemsetAsync(h->poscnt.p, 0, (size_t)NMP * h->n_max * 4, h->stream));
     const int tpb = std::min(128, ((h->maxLu + 31) / 32) * 32);
     dim3 grid(h->K, h->n_max, NMP);
     tables_kernel<<<grid, tpb, 0, h->stream>>>(h->dp, h->tab_off_d.as<int64_t>(), h->tab.as<double>(),
-                                               h->flags.as<unsigned char>(), h->budget.as<double>());
+                                               h->flags.as<unsigned char>(), h->budget.as<double>(),
+                                               h->poscnt.as<unsigned>());
     LAUNCH_CHECK(h);
   }
   CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
   h->have_tables = true;
   h->have_eval = false;
+  return 0;
+}
+
+int coral_s1_table_posfrac(coral_s1_handle* h, double* out, int64_t n) {
+  if (!h || !h->have_tables) return fail(CORAL_S1_EINVAL, "tables first");
+  const int NMP = h->NM * h->NP;
+  if (n < (int64_t)NMP * h->n_max) return fail(CORAL_S1_EINVAL, "output too small");
+  std::vector<unsigned> cnt((size_t)NMP * h->n_max, 0u);
+  if (!cnt.empty())
+    CUDA_TRY(cudaMemcpyAsync(cnt.data(), h->poscnt.p, cnt.size() * 4, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  for (int mp = 0; mp < NMP; ++mp) {
+    const int m = mp / h->NP;
+    const double cells = (double)h->K * h->Lu[m];
+    for (int S = 1; S <= h->n_max; ++S)
+      out[(size_t)mp * h->n_max + S - 1] = cells > 0 ? cnt[(size_t)mp * h->n_max + S - 1] / cells : 0.0;
+  }
   return 0;
 }
 

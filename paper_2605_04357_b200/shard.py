@@ -24,7 +24,7 @@ alternating ranks, so every prefill chain piles onto the same ranks.
 
 from __future__ import annotations
 
-import numpy as np
+import functools
 
 W = {1: 0.0, 2: 0.075, 3: 0.71, 4: 1.0, 5: 0.79, 6: 0.59}
 OVERLAP = 0.8  # a rank with >= 3 chains runs them concurrently on 4 streams: ~0.8x their sum
@@ -40,27 +40,27 @@ def unit_cost(ncombo: int, lsteps: int, S: int, posfrac: float = 0.5) -> float:
     return 0.032 + 2.42e-8 * ncombo * lsteps * W.get(S, 0.6) * (1.0 + 2.2 * posfrac)
 
 
-def table_posfrac(handle, num_configs: int) -> list:
-    """Per (model, phase) chain, {S: fraction of positive T-hat entries} from the
-    device tables (layout of coral_s1_table_layout: per chain [S][config][unit])."""
-    tabs, offs, lsteps = handle.get_tables()
-    nmp = len(offs) - 1
-    NP = nmp // max(len(lsteps), 1)
-    out = []
-    for mp in range(nmp):
-        lu = int(lsteps[mp // NP]) if len(lsteps) else 0
-        blk = tabs[int(offs[mp]):int(offs[mp + 1])]
-        if not lu or not num_configs or not blk.size:
-            out.append({})
-            continue
-        rows = blk.reshape(-1, num_configs * lu)
-        out.append({S: float(np.count_nonzero(rows[S - 1] > 0)) / rows.shape[1] for S in range(1, rows.shape[0] + 1)})
-    return out
+def table_posfrac(handle, num_configs: int = 0) -> tuple:
+    """Per (model, phase) chain, {S: fraction of positive T-hat entries}, counted by the
+    device tables kernel (coral_s1_table_posfrac)."""
+    pf = handle.table_posfrac()
+    return tuple(tuple((S, float(pf[mp, S - 1])) for S in range(1, pf.shape[1] + 1))
+                 for mp in range(pf.shape[0]))
 
 
 def assign_units(counts, lsteps, smax, num_phases: int, world: int, posfrac=None) -> list:
     """-> per rank, a list of S bit-masks indexed by mp = model * num_phases + phase.
-    posfrac: table_posfrac() of the problem (None: 0.5 everywhere).
+    posfrac: table_posfrac() of the problem (None: 0.5 everywhere). A pure function of
+    its inputs, memoised (repeated solves of one problem reuse the split)."""
+    key = (tuple(int(c) for c in counts), tuple(int(x) for x in lsteps), tuple(int(x) for x in smax),
+           int(num_phases), int(world), posfrac if posfrac is None or isinstance(posfrac, tuple)
+           else tuple(tuple(sorted(d.items())) for d in posfrac))
+    return [list(r) for r in _assign_units(*key)]
+
+
+@functools.lru_cache(maxsize=64)
+def _assign_units(counts, lsteps, smax, num_phases, world, posfrac):
+    """The split of assign_units (hashable arguments; posfrac as ((S, p), ...) per mp).
 
     Whole chains first (longest-processing-time order onto the least loaded rank),
     then single S units move from the most to the least loaded rank while that lowers
@@ -76,7 +76,7 @@ def assign_units(counts, lsteps, smax, num_phases: int, world: int, posfrac=None
             mp = m * num_phases + p
             unit[mp] = {}
             for S in range(1, min(int(sm), int(lu)) + 1):
-                pf = posfrac[mp].get(S, 0.5) if posfrac is not None else 0.5
+                pf = dict(posfrac[mp]).get(S, 0.5) if posfrac is not None else 0.5
                 unit[mp][S] = unit_cost(int(nc), int(lu), S, pf)
             fixed[mp] = chain_fixed(int(nc))
     masks = [[0] * nmp for _ in range(world)]
@@ -124,4 +124,4 @@ def assign_units(counts, lsteps, smax, num_phases: int, world: int, posfrac=None
         nch[lo] += 0 if masks[lo][mp] else 1
         masks[hi][mp] &= ~(1 << S)
         masks[lo][mp] |= 1 << S
-    return masks
+    return tuple(tuple(r) for r in masks)

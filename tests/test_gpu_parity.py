@@ -211,7 +211,8 @@ def test_sharded_evaluation_and_merge_equal_single_gpu():
     parts = []
     W = 3
     _, lsteps, smax = prob.h.table_layout()
-    masks = assign_units(prob.counts, lsteps, smax, 2, W)
+    from paper_2605_04357_b200.shard import table_posfrac
+    masks = assign_units(prob.counts, lsteps, smax, 2, W, table_posfrac(prob.h))
     for r in range(W):
         prob.h.evaluate_units(masks[r])
         n = prob.h.frontier(pm)
@@ -453,3 +454,19 @@ def test_eager_library_build_time_extended():
     g = golden("library_extended.json.gz")
     assert [template_line(t) for t in lib.entries[::97]] == g["sample"]
     print(f"eager build_library(c2): {dt:.2f}s")
+
+
+def test_table_posfrac_counts_positive_entries():
+    """The tables kernel's positive-entry counts (shard cost model input) equal a host
+    count over the same T-hat tables."""
+    from paper_2605_04357_b200 import catalog
+    w = catalog.extended_workload()
+    prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf))
+    prob.h.tables()
+    tabs, offs, lsteps = prob.h.get_tables()
+    pf = prob.h.table_posfrac()
+    K = len(w.configs)
+    for mp in range(len(offs) - 1):
+        blk = tabs[offs[mp]:offs[mp + 1]].reshape(-1, K * int(lsteps[mp // 2]))
+        for S in range(1, blk.shape[0] + 1):
+            assert pf[mp, S - 1] == np.count_nonzero(blk[S - 1] > 0) / blk.shape[1]

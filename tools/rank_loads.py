@@ -46,7 +46,7 @@ def main():
                 if not m:
                     continue
                 nc = int(counts[mp // 2])
-                pred += chain_fixed(nc) + sum(unit_cost(nc, int(lsteps[mp // 2]), S, pf[mp].get(S, 0.5))
+                pred += chain_fixed(nc) + sum(unit_cost(nc, int(lsteps[mp // 2]), S, dict(pf[mp]).get(S, 0.5))
                                               for S in range(1, 7) if m >> S & 1)
             ts = []
             for _ in range(6):
