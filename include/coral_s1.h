@@ -178,6 +178,11 @@ int coral_s1_frontier_export_device(coral_s1_handle* h, void* dev_items, int64_t
                                     int64_t* n);
 int coral_s1_frontier_merge_device(coral_s1_handle* h, const void* dev_items, int64_t n,
                                    int64_t* num_survivors);
+/* Multi-GPU merge from one all-gather: `parts` partial frontiers laid out at
+ * dev_base + p * stride_bytes + item_offset_bytes (counts[p] items each, host array),
+ * merged with the same skyline as coral_s1_frontier_merge_device. */
+int coral_s1_frontier_merge_parts(coral_s1_handle* h, const void* dev_base, int parts, int64_t stride_bytes,
+                                  int64_t item_offset_bytes, const int64_t* counts, int64_t* num_survivors);
 
 /* ---- operator: placement_search (kernels.py:279-295), batched ----------
  * case i: counts[i*6 .. +C_i) (int64), C_i = ncfg[i] <= 6, tput rows at

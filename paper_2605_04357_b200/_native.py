@@ -108,6 +108,7 @@ def load():
             "coral_s1_kernel_stats": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
             "coral_s1_set_census": (C.c_int, [vp, C.c_int]),
             "coral_s1_table_posfrac": (C.c_int, [vp, _f64p, C.c_int64]),
+            "coral_s1_frontier_merge_parts": (C.c_int, [vp, vp, C.c_int, C.c_int64, C.c_int64, _i64p, _i64p]),
             "coral_s1_kernel_timeline": (C.c_int, [vp, C.c_int64, _i32p, _i32p, _f64p, _f64p, _i64p]),
             "coral_s1_census": (C.c_int, [vp, _i64p]),
             "coral_s1_write_library": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_int, _i32p,
@@ -299,6 +300,13 @@ class Handle:
     def frontier_export_device(self, dev_ptr: int, cap: int) -> int:
         n = C.c_int64()
         _check(self._lib.coral_s1_frontier_export_device(self._h, C.c_void_p(dev_ptr), cap, C.byref(n)))
+        return n.value
+
+    def frontier_merge_parts(self, dev_ptr: int, stride_bytes: int, item_offset_bytes: int, counts) -> int:
+        cnt = np.ascontiguousarray(counts, dtype=np.int64)
+        n = C.c_int64()
+        _check(self._lib.coral_s1_frontier_merge_parts(self._h, C.c_void_p(dev_ptr), len(cnt), stride_bytes,
+                                                       item_offset_bytes, _ptr(cnt, C.c_int64), C.byref(n)))
         return n.value
 
     def frontier_merge_device(self, dev_ptr: int, n_items: int) -> int:

@@ -1808,6 +1808,31 @@ int coral_s1_frontier_merge_device(coral_s1_handle* h, const void* dev_items, in
   return 0;
 }
 
+int coral_s1_frontier_merge_parts(coral_s1_handle* h, const void* dev_base, int parts, int64_t stride_bytes,
+                                  int64_t item_offset_bytes, const int64_t* counts, int64_t* num_survivors) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  if (parts < 0 || (parts && !dev_base) || (parts && !counts)) return fail(CORAL_S1_EINVAL, "bad parts");
+  CUDA_TRY(cudaSetDevice(h->device));
+  int64_t n = 0;
+  for (int p = 0; p < parts; ++p) {
+    if (counts[p] < 0) return fail(CORAL_S1_EINVAL, "negative part count");
+    n += counts[p];
+  }
+  int rc;
+  if ((rc = h->items.ensure(std::max<int64_t>(n, 1) * sizeof(coral_s1_frontier_item)))) return rc;
+  int64_t at = 0;
+  for (int p = 0; p < parts; ++p) {
+    if (!counts[p]) continue;
+    const char* src = static_cast<const char*>(dev_base) + p * stride_bytes + item_offset_bytes;
+    CUDA_TRY(cudaMemcpyAsync(h->items.as<coral_s1_frontier_item>() + at, src,
+                             counts[p] * sizeof(coral_s1_frontier_item), cudaMemcpyDeviceToDevice, h->stream));
+    at += counts[p];
+  }
+  if ((rc = frontier_from_items(h, n, h->num_regions))) return rc;
+  if (num_survivors) *num_survivors = h->nfront;
+  return 0;
+}
+
 int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t* ncfg,
                               const int64_t* counts, const int32_t* lsteps, const int64_t* tput_off,
                               const double* tput, int64_t tput_len, const int32_t* S, double* best,

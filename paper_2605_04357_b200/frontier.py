@@ -88,25 +88,53 @@ def _dist_info(dist):
     return tdist
 
 
+# Items per rank of the single all-gather. Grown (never shrunk) from the largest
+# partial frontier seen; every rank derives it from the same gathered headers, so all
+# ranks always agree on it without a separate exchange.
+_MERGE_CAP = [16384]
+
+
+def _gather_partials(n_local: int, export, tdist, device, item_bytes: int):
+    """ONE all-gather of fixed-capacity partial frontiers (north_star: "merged with a
+    single NCCL all-gather"). Each rank sends [header | cap items]; the header's first
+    int64 is its item count. If any rank overflowed the agreed capacity (all ranks see
+    the same headers), all grow it to the next power of two and repeat once.
+    export(buffer, offset_bytes, cap) writes this rank's items. -> (recv, stride, counts)."""
+    import torch
+    world = tdist.get_world_size()
+    hdr = item_bytes
+    for _ in range(2):
+        cap = _MERGE_CAP[0]
+        stride = hdr + cap * item_bytes
+        send = torch.empty(stride, dtype=torch.uint8, device=device)
+        send[:8].view(torch.int64).fill_(n_local)
+        if n_local <= cap:
+            export(send, hdr, cap)
+        recv = torch.empty(world * stride, dtype=torch.uint8, device=device)
+        tdist.all_gather_into_tensor(recv, send)
+        counts = recv.view(world, stride)[:, :8].contiguous().view(torch.int64).view(-1).tolist()
+        mx = max(counts)
+        if mx <= cap:
+            return recv, stride, counts
+        grow = 1
+        while grow < mx:
+            grow <<= 1
+        _MERGE_CAP[0] = max(cap, grow)
+    raise RuntimeError("partial frontier capacity did not converge")
+
+
 def _merge_across_ranks(prob: Stage1Problem, n_local: int, tdist) -> int:
-    """ONE all-gather of the fixed-capacity partial frontiers, then the same skyline
-    over their union on every rank (associative: all ranks end identical)."""
+    """Single all-gather of the partial frontiers, then the same skyline over their
+    union on every rank (associative: all ranks end identical)."""
     import torch
     dev = torch.device("cuda", prob.h.device)
-    world = tdist.get_world_size()
-    cnt = torch.tensor([n_local], dtype=torch.int64, device=dev)
-    counts = torch.empty(world, dtype=torch.int64, device=dev)
-    tdist.all_gather_into_tensor(counts, cnt)
-    counts_h = counts.tolist()
-    cap = max(1, max(counts_h))
     item = _native.FRONTIER_DTYPE.itemsize
-    send = torch.zeros(cap * item, dtype=torch.uint8, device=dev)
-    prob.h.frontier_export_device(send.data_ptr(), cap)
-    recv = torch.empty(world * cap * item, dtype=torch.uint8, device=dev)
-    tdist.all_gather_into_tensor(recv, send)
-    parts = recv.view(world, cap, item)
-    union = torch.cat([parts[r, :counts_h[r]] for r in range(world)]).contiguous()
-    return prob.h.frontier_merge_device(union.data_ptr(), int(sum(counts_h)))
+
+    def export(buf, offset, cap):
+        prob.h.frontier_export_device(buf.data_ptr() + offset, cap)
+
+    recv, stride, counts = _gather_partials(n_local, export, tdist, dev, item)
+    return prob.h.frontier_merge_parts(recv.data_ptr(), stride, item, counts)
 
 
 def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,

@@ -115,3 +115,54 @@ def test_two_rank_gloo_protocol_matches_single_process():
         assert p.exitcode == 0
     assert merged == ref
     assert len(ref) > 50
+
+
+def _gather_worker(rank, world, port, out):
+    """The frontier merge's single all-gather (frontier._gather_partials) over gloo:
+    fixed-capacity parts with a count header, capacity regrown on overflow."""
+    import torch
+    from paper_2605_04357_b200 import _native, frontier
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    frontier._MERGE_CAP[0] = 4
+    item = _native.FRONTIER_DTYPE.itemsize
+    n_local = 3 if rank == 0 else 10  # rank 1 overflows the first capacity
+    mine = np.zeros(n_local, dtype=_native.FRONTIER_DTYPE)
+    mine["price_usd_h"] = np.arange(n_local) + 100 * rank
+    mine["combo_key"] = np.arange(n_local) * 7 + rank
+    raw = torch.from_numpy(mine.view(np.uint8).copy())
+
+    def export(buf, offset, cap):
+        assert n_local <= cap
+        buf[offset:offset + raw.numel()].copy_(raw)
+
+    recv, stride, counts = frontier._gather_partials(n_local, export, dist, torch.device("cpu"), item)
+    parts = []
+    for r, c in enumerate(counts):
+        blob = recv[r * stride + item: r * stride + item + c * item].numpy().tobytes()
+        parts.append(np.frombuffer(blob, dtype=_native.FRONTIER_DTYPE))
+    out.put((rank, counts, frontier._MERGE_CAP[0], [p["price_usd_h"].tolist() for p in parts],
+             [p["combo_key"].tolist() for p in parts]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_single_all_gather_protocol_regrows_capacity():
+    world = 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(out.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, counts, cap, prices, keys in res:
+        assert counts == [3, 10]
+        assert cap == 16  # next power of two >= 10, identical on every rank
+        assert prices == [[0.0, 1.0, 2.0], [100.0 + i for i in range(10)]]
+        assert keys == [[0, 7, 14], [1 + 7 * i for i in range(10)]]

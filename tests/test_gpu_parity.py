@@ -222,6 +222,16 @@ def test_sharded_evaluation_and_merge_equal_single_gpu():
     n = prob.h.frontier_merge_device(dev.data_ptr(), len(union))
     merged = prob.h.get_frontier(n)
     assert merged.tobytes() == full.tobytes()
+    # the multi-GPU path's layout: one strided buffer [header | cap items] per part
+    item = _native.FRONTIER_DTYPE.itemsize
+    cap = max(len(p) for p in parts) + 3
+    stride = item + cap * item
+    buf = np.zeros(W * stride, dtype=np.uint8)
+    for r, part in enumerate(parts):
+        buf[r * stride + item: r * stride + item + len(part) * item] = part.view(np.uint8)
+    dbuf = torch.from_numpy(buf).cuda()
+    n = prob.h.frontier_merge_parts(dbuf.data_ptr(), stride, item, [len(p) for p in parts])
+    assert prob.h.get_frontier(n).tobytes() == full.tobytes()
     assert _native.FRONTIER_DTYPE.itemsize == 64
 
 
