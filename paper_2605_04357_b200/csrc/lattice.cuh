@@ -405,16 +405,17 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
   for (int l0 = sg; l0 <= lmax; l0 += 32) {
     // lanes = G groups x wp positions; group g takes valid codes g, g+G, g+2G, ...
     const int w = min(32, lmax - l0 + 1);
-    int wp = 1;
-    while (wp < w) wp <<= 1;
-    const int G = 32 / wp;
-    const int g = lane / wp, i = lane - g * wp;
+    int lw = 0;  // wp = 2^lw >= w (powers of two: shifts, not divisions)
+    while ((1 << lw) < w) ++lw;
+    const int wp = 1 << lw;
+    const int G = 32 >> lw;
+    const int g = lane >> lw, i = lane & (wp - 1);
     const int l = l0 + i;
     const bool act = i < w;
     const int jmax = l - (sg - 1);
     double best = kNegInf;
     int bu = 1 << 20, bj = 0;
-    const int T = (nv + G - 1) / G;
+    const int T = (nv + G - 1) >> (5 - lw);
     for (int t = 0; t < T; ++t) {
       const int kk = t * G + g;  // this group's kk-th valid code (ascending per group)
       const int src = kk < nv ? kk : 0;
