@@ -521,6 +521,9 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
       dp_pair(val + ru[k], lay + rr[k], Lu, Lu - (S - 1), true, cand, cj, cap);
       if (cand > best) { best = cand; bu = lane + 1 + 32 * k; bj = cj; }
     }
+    // an S only matters if some lane beats the best so far (strict, templates.py:322);
+    // otherwise its winning code / j are never used: skip the reduction
+    if (!__any_sync(0xffffffffu, best > tbest && best > 1e-9)) continue;
     warp_argmax_code(best, bu, bj);
     if (best > tbest && best > 1e-9) { tbest = best; twin = S; tcode = bu; tj = bj; }
   }
