@@ -518,7 +518,8 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
       if (su[k] > n - (S - 1) || lane + 1 + 32 * k > chalf) continue;
       double cand;
       int cj;
-      dp_pair(val + ru[k], lay + rr[k], Lu, Lu - (S - 1), true, cand, cj, cap);
+      // only values above the best earlier S (and 1e-9) can matter (templates.py:322)
+      dp_pair<true>(val + ru[k], lay + rr[k], Lu, Lu - (S - 1), true, cand, cj, cap, tbest > 1e-9 ? tbest : 1e-9);
       if (cand > best) { best = cand; bu = lane + 1 + 32 * k; bj = cj; }
     }
     // an S only matters if some lane beats the best so far (strict, templates.py:322);

@@ -157,9 +157,15 @@ __device__ inline void dp_build_value(const DpShared& sh, const DpBuffers& B) {
 // lo = min(J, l - K - 1), hi = J + 1 (clamped to [1, jmax]) returns the reference
 // search's (lo, hi) in fewer probes. (Past the two shortcuts P(1) is true and P(jmax)
 // false, so J >= 1 and the clamped bracket is never empty.)
+//
+// floor (callers that keep only strictly better values): with g non-increasing and h
+// non-decreasing no j gives more than min(g(1), h(jmax)); a pair whose bound is <= floor
+// cannot change the caller's result, so it returns -inf without searching.
+template <bool kFloor = false>
 __device__ __forceinline__ void dp_pair(const double* __restrict__ gv,
                                         const double* __restrict__ hv, int l, int jmax,
-                                        bool mono, double& cand, int& cj, bool cap = false) {
+                                        bool mono, double& cand, int& cj, bool cap = false,
+                                        double floor = kNegInf) {
   if (mono) {
     const double* __restrict__ hl = hv + l;  // hv[l - j] == hl[-j]: one address op per probe
     // capped rows are 16-byte aligned (lat_pitch): (J, g[1]) in one vector load; J and
@@ -178,6 +184,7 @@ __device__ __forceinline__ void dp_pair(const double* __restrict__ gv,
     const double gm = gv[jmax];
     const double hm = hl[-jmax];
     if (gm >= hm) { cand = hm; cj = jmax; return; }
+    if (kFloor && (g1 < hm ? g1 : hm) <= floor) { cand = kNegInf; cj = 0; return; }
     int lo = 1, hi = jmax;
     if (cap) {
       const int J = __double2loint(g0), K = __double2loint(h0);
