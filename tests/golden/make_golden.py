@@ -14,6 +14,8 @@ fixtures into tests/golden/ that pin the CPU oracle and the CUDA path:
                       sha256 + every 97th record (extended)
   frontier_<w>.json.gz SURVEY.md 8c frontier computed on the reference library
   perf_grid.json.gz   node_max_throughput on a grid in the style of test_perf.py
+  tolmono.json.gz     library on T-hat rows monotone only within the 1e-12 tolerance
+                      (--tolmono)
 
 Usage: python tests/golden/make_golden.py [--extended-pkl /tmp/ref_extended.pkl]
 """
@@ -237,8 +239,31 @@ def profile_case():
     return {"profile": entries, "library": library_fixture("profile", lib_records(lib), True)}
 
 
+def tolmono_case():
+    """T-hat rows (ProfileTable overrides for every S) that rise by < 1e-12: monotone for
+    kernels.py:291 but not exactly, so the reference's binary search runs on a
+    predicate that is not monotone; includes an equal adjacent pair (ties)."""
+    configs = [NodeConfig(RC.GPU_CATALOG["A100"], 1), NodeConfig(RC.GPU_CATALOG["A100"], 2),
+               NodeConfig(RC.GPU_CATALOG["L40S"], 2)]
+    model = ModelSpec("m8", num_layers=8, params_total_b=14, params_active_b=14, hidden_size=5120)
+    slo = SloSpec(1500, 80)
+    prof = ProfileTable()
+    for k, cfg in enumerate(configs):
+        for ph in (PREFILL, DECODE):
+            base = 1000.0 * (k + 1) + (0.5 if ph == DECODE else 0.0)
+            row = [base, base * 0.9, base * 0.8, base * 0.8 + 3e-13 * (k + 1), base * 0.65, base * 0.65,
+                   base * 0.5 + 4e-13, base * 0.3]
+            for j, v in enumerate(row, start=1):
+                prof.add(cfg.name, "m8", ph, j, -1, v)
+    lib = build_library(configs, [model], {"m8": slo}, LibraryCaps(4, 40.0), GenContext(profile=prof))
+    entries = [[k[0], k[1], k[2], k[3], k[4], v] for k, v in prof.entries.items()]
+    return {"profile": entries, "library": library_fixture("tolmono", lib_records(lib), True)}
+
+
 def main():
     argv = sys.argv[1:]
+    if "--tolmono" in argv:
+        return dump("tolmono.json.gz", tolmono_case())
     ext_pkl = argv[argv.index("--extended-pkl") + 1] if "--extended-pkl" in argv else None
     if "--only-extended" in argv:
         return extended(ext_pkl)

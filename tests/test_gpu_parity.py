@@ -480,3 +480,23 @@ def test_table_posfrac_counts_positive_entries():
         blk = tabs[offs[mp]:offs[mp + 1]].reshape(-1, K * int(lsteps[mp // 2]))
         for S in range(1, blk.shape[0] + 1):
             assert pf[mp, S - 1] == np.count_nonzero(blk[S - 1] > 0) / blk.shape[1]
+
+
+def test_rows_monotone_only_within_tolerance_take_the_literal_search():
+    """T-hat rows that rise by < 1e-12 pass the reference's monotone test
+    (kernels.py:291) but are not exactly monotone: the lattice must then run the
+    literal [1, jmax] search without the cap bracket or the u <-> X-u symmetry, and
+    match the unmodified reference (golden tolmono.json.gz) and the oracle exactly."""
+    from tests.test_oracle_golden import tolmono_inputs
+    g, inputs = tolmono_inputs()
+    configs, models, slos, caps, ctx = inputs
+    prob = Stage1Problem(configs, models, slos, caps, ctx)
+    prob.h.tables()
+    tabs, offs, lsteps = prob.h.get_tables()
+    rows = tabs[offs[0]:offs[1]].reshape(-1, int(lsteps[0]))
+    d = np.diff(rows, axis=1)
+    assert (d <= 1e-12).all() and (d > 0).any()  # tolerance-monotone, not exactly
+    lib = build_library(configs, models, slos, caps, ctx)
+    lines = [template_line(t) for t in lib.entries]
+    assert lines == g["library"]["records"]
+    assert lines == oracle_library_lines(oracle_problem(inputs))

@@ -131,6 +131,28 @@ def test_profile_override_library():
     assert oracle_library_lines(op) == g["library"]["records"]
 
 
+def tolmono_inputs():
+    """Inputs of tests/golden/tolmono.json.gz (make_golden.tolmono_case)."""
+    from paper_2605_04357_b200 import catalog
+    from paper_2605_04357_b200.library import GenContext, LibraryCaps
+    from paper_2605_04357_b200.specs import ModelSpec, NodeConfig, ProfileTable, SloSpec
+    g = golden("tolmono.json.gz")
+    configs = [NodeConfig(catalog.GPU_CATALOG["A100"], 1), NodeConfig(catalog.GPU_CATALOG["A100"], 2),
+               NodeConfig(catalog.GPU_CATALOG["L40S"], 2)]
+    model = ModelSpec("m8", num_layers=8, params_total_b=14, params_active_b=14, hidden_size=5120)
+    prof = ProfileTable()
+    for cfg, mdl, ph, j, b, v in g["profile"]:
+        prof.add(cfg, mdl, ph, j, b, v)
+    return g, (configs, [model], {"m8": SloSpec(1500, 80)}, LibraryCaps(4, 40.0), GenContext(profile=prof))
+
+
+def test_tolerance_monotone_rows_library():
+    """Rows monotone only within kernels.py:291's 1e-12: the reference's binary search
+    on a non-monotone predicate, reproduced literally."""
+    g, inputs = tolmono_inputs()
+    assert oracle_library_lines(oracle_problem(inputs)) == g["library"]["records"]
+
+
 @pytest.mark.parametrize("w", ["c1", "core"])
 def test_frontier_matches_reference_library_frontier(w):
     """SURVEY.md 8c frontier: the oracle's skyline over its own records equals the
