@@ -11,7 +11,8 @@ import torch  # noqa: E402
 
 from paper_2605_04357_b200 import build_frontier, catalog  # noqa: E402
 from paper_2605_04357_b200.frontier import _price_matrix, materialise  # noqa: E402
-from paper_2605_04357_b200.library import GenContext, LibraryCaps, library_meta  # noqa: E402
+from paper_2605_04357_b200.library import (GenContext, LibraryCaps, Stage1Problem, _pack_problem,  # noqa: E402
+                                           library_meta)
 
 
 def main():
@@ -34,10 +35,15 @@ def main():
     n = len(front)
     for label, fn in [
         ("library_meta", lambda: library_meta(cfgs, w.models, w.slos, caps, ctx)),
+
         ("price_matrix", lambda: _price_matrix(cfgs, w.prices, w.regions)),
         ("frontier()", lambda: prob.h.frontier(pm)),
         ("get_frontier", lambda: prob.h.get_frontier(n)),
         ("materialise", lambda: materialise(prob, prob.h.get_frontier(n), names, meta)),
+        # last: a new problem re-targets the shared per-device handle
+        ("_pack_problem", lambda: _pack_problem(sorted(w.configs, key=lambda c: c.name), w.models, w.slos,
+                                                ("prefill", "decode"), caps, ctx)),
+        ("Stage1Problem", lambda: Stage1Problem(w.configs, w.models, w.slos, caps, ctx)),
     ]:
         fn()
         t0 = time.perf_counter()
