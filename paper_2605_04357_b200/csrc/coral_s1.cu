@@ -712,49 +712,28 @@ __device__ __forceinline__ unsigned long long dbits(double x) {
   return (unsigned long long)__double_as_longlong(x);  // monotone for x >= 0
 }
 
-// Exact prefilter, pass 1: the price range (bit patterns) over all items. Grid-stride
-// over (candidate, region) with a block reduction: one atomic pair per block (a pair
-// per warp serialised ~10^5 atomics on the same two words).
-__global__ void __launch_bounds__(256) frontier_range_kernel(FrontArgs A, unsigned long long* __restrict__ range) {
-  __shared__ unsigned long long slo[8], shi[8];
-  unsigned long long lo = ~0ull, hi = 0ull;
-  const int64_t n = A.ncand * A.R;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    coral_s1_frontier_item it;
-    if (frontier_item(A, t / A.R, (int)(t % A.R), &it)) {
-      lo = min(lo, dbits(it.price_usd_h));
-      hi = max(hi, dbits(it.price_usd_h));
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) { slo[w] = lo; shi[w] = hi; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) { lo = min(lo, slo[k]); hi = max(hi, shi[k]); }
-    if (hi) {
-      atomicMin(range, lo);
-      atomicMax(range + 1, hi);
-    }
-  }
+// price bucket: top bits of the (non-negative) price's bit pattern relative to the range
+// start, clamped to [0, nb) -- a non-decreasing map of the price
+__device__ __forceinline__ int bucket_of(double price, int shift, unsigned long long base, int nb) {
+  const unsigned long long q = dbits(price) >> shift;
+  if (q <= base) return 0;
+  const unsigned long long d = q - base;
+  return d >= (unsigned long long)nb ? nb - 1 : (int)d;
 }
 
-// pass 2: per (segment, price bucket) the max throughput (bit pattern, T > 0)
+// pass 1: per (segment, price bucket) the max throughput (bit pattern, T > 0)
 __global__ void frontier_bucket_kernel(FrontArgs A, int shift, unsigned long long base, int nb,
                                        unsigned long long* __restrict__ bmax) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   coral_s1_frontier_item it;
   if (!frontier_item(A, t / A.R, (int)(t % A.R), &it)) return;
-  const int b = (int)((dbits(it.price_usd_h) >> shift) - base);
+  const int b = bucket_of(it.price_usd_h, shift, base, nb);
   unsigned long long* slot = bmax + ((int64_t)it.mp * A.R + it.region) * nb + b;
   const unsigned long long tb = dbits(it.throughput_tps);
   if (*slot < tb) atomicMax(slot, tb);
 }
 
-// pass 3: exclusive prefix max over the buckets of each segment (block per segment)
+// pass 2: exclusive prefix max over the buckets of each segment (block per segment)
 __global__ void frontier_prefix_kernel(int nb, unsigned long long* __restrict__ bmax) {
   typedef cub::BlockScan<unsigned long long, 256> Scan;
   __shared__ typename Scan::TempStorage tmp;
@@ -774,7 +753,7 @@ __global__ void frontier_prefix_kernel(int nb, unsigned long long* __restrict__ 
   }
 }
 
-// pass 4: write the items that can still be on the frontier: T must exceed every
+// pass 3: write the items that can still be on the frontier: T must exceed every
 // throughput of a strictly cheaper bucket, else a cheaper candidate dominates it
 // (SURVEY.md 8c keep rule: T > running max of the earlier items).
 __global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long base, int nb,
@@ -783,7 +762,7 @@ __global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long
   coral_s1_frontier_item it;
   bool keep = frontier_item(A, t / A.R, (int)(t % A.R), &it);
   if (keep && nb > 0) {
-    const int b = (int)((dbits(it.price_usd_h) >> shift) - base);
+    const int b = bucket_of(it.price_usd_h, shift, base, nb);
     keep = dbits(it.throughput_tps) > pmax[((int64_t)it.mp * A.R + it.region) * nb + b];
   }
   const unsigned ballot = __ballot_sync(0xffffffffu, keep);
@@ -1741,15 +1720,23 @@ int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices,
     A.R = num_regions;
     A.items = h->items.as<coral_s1_frontier_item>();
     A.nitems = h->nsel.as<unsigned long long>();
-    // exact prefilter: range -> per (segment, price bucket) max T -> prefix max
+    // exact prefilter: per (segment, price bucket) max T -> prefix max. The bucket range
+    // only has to contain every item price (any non-decreasing price -> bucket map keeps
+    // the filter exact), so it comes from the price matrix on the host: a combo costs at
+    // least the cheapest offered config and at most n_max x the dearest (with margin for
+    // rounding; bucket indices are clamped, which keeps the map non-decreasing).
     const unsigned gb = (unsigned)((nmax + 255) / 256);
-    unsigned long long init[2] = {~0ull, 0ull}, range[2];
-    CUDA_TRY(cudaMemcpyAsync(h->nsel.as<unsigned long long>() + 1, init, 16, cudaMemcpyHostToDevice, st));
-    frontier_range_kernel<<<(unsigned)std::min<int64_t>(gb, (int64_t)h->num_sms * 8), 256, 0, st>>>(
-        A, h->nsel.as<unsigned long long>() + 1);
-    LAUNCH_CHECK(h);
-    CUDA_TRY(cudaMemcpyAsync(range, h->nsel.as<unsigned long long>() + 1, 16, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    unsigned long long range[2] = {~0ull, 0ull};
+    {
+      double pmin = HUGE_VAL, pmax = 0.0;
+      for (double p : pv)
+        if (!std::isnan(p)) { pmin = std::min(pmin, p); pmax = std::max(pmax, p); }
+      if (pmin <= pmax && pmax > 0.0) {
+        const double lo = pmin > 0.0 ? pmin * (1.0 - 1e-9) : 0.0, hi = pmax * h->n_max * (1.0 + 1e-9);
+        std::memcpy(&range[0], &lo, 8);
+        std::memcpy(&range[1], &hi, 8);
+      }
+    }
     int shift = 0, nb = 0;
     unsigned long long base = 0;
     const int64_t nseg = (int64_t)h->NM * h->NP * num_regions;
