@@ -113,6 +113,8 @@ struct coral_s1_handle {
   cudaStream_t side[kStreams] = {};
   cudaEvent_t side_ev[kStreams] = {};
   cudaEvent_t fork_ev = nullptr;
+  cudaEvent_t prep_ev = nullptr;  // lattice tables prepared on side[0] during enumerate
+  bool lat_ready = false, flags_ready = false;
   std::vector<unsigned char> flags_h;
   std::vector<char> model_used;
   std::vector<double> memb_h, wbytes_h;  // config memory bytes, model weight bytes
@@ -131,6 +133,7 @@ struct coral_s1_handle {
   bool census_on = false;
   DevBuf census;
   DevBuf poscnt;  // positive T-hat entries per (mp, S)
+  DevBuf prep_tmp;  // CUB scratch of lattice_prepare (side stream)
 };
 
 namespace {
@@ -961,10 +964,11 @@ int frontier_from_items(coral_s1_handle* h, int64_t n, int R) {
 }
 
 template <class T>
-int upload(coral_s1_handle* h, DevBuf& buf, const std::vector<T>& v) {
+int upload(coral_s1_handle* h, DevBuf& buf, const std::vector<T>& v, cudaStream_t st = nullptr) {
   int rc = buf.ensure(std::max<size_t>(v.size() * sizeof(T), 8));
   if (rc) return rc;
-  if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+  if (!v.empty())
+    CUDA_TRY(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st ? st : h->stream));
   return 0;
 }
 
@@ -984,6 +988,8 @@ int64_t universe_size(int K, int n_max) {
 // ================================================================================
 // C ABI
 // ================================================================================
+static int lattice_prepare(coral_s1_handle* h, cudaStream_t st);  // below: lattice state tables
+
 extern "C" {
 
 const char* coral_s1_last_error(void) { return g_err.c_str(); }
@@ -1017,6 +1023,7 @@ int coral_s1_create(int device, coral_s1_handle** out) {
     cudaEventCreateWithFlags(&h->side_ev[i], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&h->prep_ev, cudaEventDisableTiming);
   for (int i = 0; i < coral_s1_handle::kTimedMax; ++i) {
     cudaEventCreate(&h->tev[i][0]);
     cudaEventCreate(&h->tev[i][1]);
@@ -1042,7 +1049,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
                     &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
-                    &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};
+                    &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release(); h->ws_ranks[i].release();
@@ -1050,6 +1057,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
     if (h->side_ev[i]) cudaEventDestroy(h->side_ev[i]);
   }
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
+  if (h->prep_ev) cudaEventDestroy(h->prep_ev);
   for (int i = 0; i < coral_s1_handle::kTimedMax; ++i) {
     if (h->tev[i][0]) cudaEventDestroy(h->tev[i][0]);
     if (h->tev[i][1]) cudaEventDestroy(h->tev[i][1]);
@@ -1194,6 +1202,7 @@ int coral_s1_tables(coral_s1_handle* h) {
   CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
   h->have_tables = true;
   h->have_eval = false;
+  h->lat_ready = h->flags_ready = false;
   return 0;
 }
 
@@ -1263,10 +1272,27 @@ int coral_s1_enumerate(coral_s1_handle* h) {
     LAUNCH_CHECK(h);
     std::vector<unsigned long long> nv(NM);
     CUDA_TRY(cudaMemcpyAsync(nv.data(), h->nvalid.p, NM * 8, cudaMemcpyDeviceToHost, st));
+    // the evaluator's T-hat monotonicity flags ride on this round trip
+    const int NMPf = NM * h->NP;
+    h->flags_h.assign((size_t)std::max(NMPf, 1) * h->n_max * h->K, 0);
+    if (h->have_tables && NMPf && h->K)
+      CUDA_TRY(cudaMemcpyAsync(h->flags_h.data(), h->flags.p, (size_t)NMPf * h->n_max * h->K,
+                               cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    h->flags_ready = h->have_tables;
     for (int m = 0; m < NM; ++m) {
       h->counts[m] = (int64_t)nv[m];
       h->koff[m + 1] = h->koff[m] + h->counts[m];
+    }
+    // lattice state tables for every model with candidates, on side stream 0 while the
+    // rest of the enumeration (compaction, sort) runs on the main stream
+    h->model_used.assign(NM, 0);
+    for (int m = 0; m < NM; ++m) h->model_used[m] = h->counts[m] > 0;
+    h->lat_ready = false;
+    if (h->n_max >= 2 && h->have_tables) {
+      if ((rc = lattice_prepare(h, h->side[0]))) return rc;
+      CUDA_TRY(cudaEventRecord(h->prep_ev, h->side[0]));
+      h->lat_ready = true;
     }
     const int64_t nk = h->koff[NM];
     if ((rc = h->keys.ensure(std::max<int64_t>(nk, 1) * 8)) ||
@@ -1397,9 +1423,8 @@ static void timed_end(coral_s1_handle* h, cudaStream_t st, int i) {
 }
 
 // State tables shared by all models (depend on K and n_max only) + per-model maxn.
-static int lattice_prepare(coral_s1_handle* h) {
+static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
   const int K = h->K, R = h->n_max - 1;
-  cudaStream_t st = h->stream;
   h->lat_base.assign(R + 2, 0);
   for (int sz = 1; sz <= R; ++sz) {
     long double c = 1;
@@ -1408,7 +1433,7 @@ static int lattice_prepare(coral_s1_handle* h) {
   }
   h->lat_states = h->lat_base[R + 1];
   int rc;
-  if ((rc = upload(h, h->lat_base_d, h->lat_base))) return rc;
+  if ((rc = upload(h, h->lat_base_d, h->lat_base, st))) return rc;
   if (h->lat_states == 0) return 0;
   const long long ns = h->lat_states;
   if ((rc = h->lat_key.ensure(ns * 8)) || (rc = h->lat_nsub.ensure((ns + 1) * 8)) ||
@@ -1422,11 +1447,11 @@ static int lattice_prepare(coral_s1_handle* h) {
   lat_nsub_kernel<<<(unsigned)((ns + 256) / 256), 256, 0, st>>>(L, h->lat_key.as<unsigned long long>(),
                                                                 h->lat_nsub.as<long long>());
   LAUNCH_CHECK(h);
-  size_t tmp = 0;
+  size_t tmp = 0;  // own scratch: may run beside the enumeration's CUB calls
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, h->lat_nsub.as<long long>(), h->lat_off.as<long long>(),
                                 (int)(ns + 1), st);
-  if ((rc = ensure_tmp(h, tmp))) return rc;
-  CUDA_TRY(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, h->lat_nsub.as<long long>(),
+  if ((rc = h->prep_tmp.ensure(std::max<size_t>(tmp, 8)))) return rc;
+  CUDA_TRY(cub::DeviceScan::ExclusiveSum(h->prep_tmp.p, tmp, h->lat_nsub.as<long long>(),
                                          h->lat_off.as<long long>(), (int)(ns + 1), st));
   h->launches += 2;
   // upper bound (every state has at most 2^R sub-multiset codes): no host round trip
@@ -1460,7 +1485,7 @@ static int lattice_prepare(coral_s1_handle* h) {
       flat.insert(flat.end(), sums[k].begin(), sums[k].end());
     }
     soff[kmax + 1] = (int)flat.size();
-    if ((rc = upload(h, h->lat_sums, flat)) || (rc = upload(h, h->lat_soff, soff))) return rc;
+    if ((rc = upload(h, h->lat_sums, flat, st)) || (rc = upload(h, h->lat_soff, soff, st))) return rc;
     for (int m = 0; m < h->NM; ++m) {
       if (!h->counts[m] || !h->model_used[m]) continue;
       const double lo = h->wbytes_h[m], hi = h->rho * lo;
@@ -1588,21 +1613,28 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
     return rc;
   cudaStream_t st = h->stream;
   const int NMP = h->NM * h->NP;
-  h->flags_h.assign((size_t)std::max(NMP, 1) * h->n_max * h->K, 0);
-  if (NMP && h->K)
-    CUDA_TRY(cudaMemcpyAsync(h->flags_h.data(), h->flags.p, (size_t)NMP * h->n_max * h->K,
-                             cudaMemcpyDeviceToHost, st));
+  const bool flags_were_ready = h->flags_ready;
+  if (!flags_were_ready) {
+    h->flags_h.assign((size_t)std::max(NMP, 1) * h->n_max * h->K, 0);
+    if (NMP && h->K)
+      CUDA_TRY(cudaMemcpyAsync(h->flags_h.data(), h->flags.p, (size_t)NMP * h->n_max * h->K,
+                               cudaMemcpyDeviceToHost, st));
+  }
   CUDA_TRY(cudaEventRecord(h->ev[4], st));
   h->ntimed = 0;
   // records not improved by any unit read as infeasible (num_stages 0)
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), st));
   if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 8, st));
-  h->model_used.assign(h->NM, 0);  // lattice tables only for the models this call evaluates
-  for (int mp = 0; mp < NMP; ++mp)
-    for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
-      if (take(mp, S)) h->model_used[mp / h->NP] = 1;
-  if ((rc = lattice_prepare(h))) return rc;
-  CUDA_TRY(cudaStreamSynchronize(st));  // flags_h valid
+  if (h->lat_ready) {  // prepared on side[0] during enumerate (every model with candidates)
+    CUDA_TRY(cudaStreamWaitEvent(st, h->prep_ev, 0));
+  } else {
+    h->model_used.assign(h->NM, 0);  // lattice tables only for the models this call evaluates
+    for (int mp = 0; mp < NMP; ++mp)
+      for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
+        if (take(mp, S)) h->model_used[mp / h->NP] = 1;
+    if ((rc = lattice_prepare(h, st))) return rc;
+  }
+  if (!flags_were_ready) CUDA_TRY(cudaStreamSynchronize(st));  // flags_h valid
   CUDA_TRY(cudaEventRecord(h->fork_ev, st));
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) CUDA_TRY(cudaStreamWaitEvent(h->side[i], h->fork_ev, 0));
   // one chain per model (its phases back to back on one stream, sharing the model's
