@@ -134,6 +134,11 @@ struct coral_s1_handle {
   DevBuf census;
   DevBuf poscnt;  // positive T-hat entries per (mp, S)
   DevBuf prep_tmp;  // CUB scratch of lattice_prepare (side stream)
+  // memoised achievable-memory-sum table of lattice_prepare (key -> flat sums, offsets)
+  std::vector<double> sums_key_mem, sums_flat;
+  double sums_key_cap = -1.0;
+  int sums_key_kmax = -1;
+  std::vector<int> sums_off;
 };
 
 namespace {
@@ -1469,22 +1474,30 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
       if (h->model_used[m]) cap = std::max(cap, h->rho * h->wbytes_h[m]);
     cap *= 1.0 + 1e-6;
     const int kmax = h->n_max - 1;  // a state holds >= 1 config
-    std::vector<std::vector<double>> sums(kmax + 1);
-    sums[0].push_back(0.0);
-    for (int k = 1; k <= kmax; ++k) {
-      for (double prev : sums[k - 1])
-        for (double v : mem)
-          if (prev + v < cap) sums[k].push_back(prev + v);
-      std::sort(sums[k].begin(), sums[k].end());
-      sums[k].erase(std::unique(sums[k].begin(), sums[k].end()), sums[k].end());
+    // the sum table is a pure function of (memory sizes, cap, kmax): memoised per handle
+    if (!(h->sums_key_mem == mem && h->sums_key_cap == cap && h->sums_key_kmax == kmax)) {
+      std::vector<std::vector<double>> sums(kmax + 1);
+      sums[0].push_back(0.0);
+      for (int k = 1; k <= kmax; ++k) {
+        for (double prev : sums[k - 1])
+          for (double v : mem)
+            if (prev + v < cap) sums[k].push_back(prev + v);
+        std::sort(sums[k].begin(), sums[k].end());
+        sums[k].erase(std::unique(sums[k].begin(), sums[k].end()), sums[k].end());
+      }
+      h->sums_flat.clear();
+      h->sums_off.assign(kmax + 2, 0);
+      for (int k = 0; k <= kmax; ++k) {
+        h->sums_off[k] = (int)h->sums_flat.size();
+        h->sums_flat.insert(h->sums_flat.end(), sums[k].begin(), sums[k].end());
+      }
+      h->sums_off[kmax + 1] = (int)h->sums_flat.size();
+      h->sums_key_mem = mem;
+      h->sums_key_cap = cap;
+      h->sums_key_kmax = kmax;
     }
-    std::vector<double> flat;
-    std::vector<int> soff(kmax + 2, 0);
-    for (int k = 0; k <= kmax; ++k) {
-      soff[k] = (int)flat.size();
-      flat.insert(flat.end(), sums[k].begin(), sums[k].end());
-    }
-    soff[kmax + 1] = (int)flat.size();
+    const std::vector<double>& flat = h->sums_flat;
+    const std::vector<int>& soff = h->sums_off;
     if ((rc = upload(h, h->lat_sums, flat, st)) || (rc = upload(h, h->lat_soff, soff, st))) return rc;
     for (int m = 0; m < h->NM; ++m) {
       if (!h->counts[m] || !h->model_used[m]) continue;
