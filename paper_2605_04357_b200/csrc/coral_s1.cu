@@ -105,7 +105,6 @@ struct coral_s1_handle {
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
   static constexpr int kStreams = 4;
   int nstreams = kStreams;  // side streams in use (CORAL_S1_STREAMS)
-  bool top_per_S = false;   // one top-cell launch per S (CORAL_S1_TOP_PER_S)
   long long lat_states = 0;
   std::vector<long long> lat_base;     // [R + 2]
   DevBuf lat_base_d, lat_binom_d, lat_key, lat_nsub, lat_off, lat_sub, lat_maxn, lat_flags_h;
@@ -477,7 +476,6 @@ struct TopArgs {
 };
 
 __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
-  const LatModel& L = A.L;
   const int lane = threadIdx.x & 31;
   const long long ci = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= A.ncombo) return;
@@ -1034,7 +1032,6 @@ int coral_s1_create(int device, coral_s1_handle** out) {
     cudaEventCreate(&h->tev[i][1]);
   }
   if (const char* e = getenv("CORAL_S1_STREAMS")) h->nstreams = std::max(1, std::min(atoi(e), coral_s1_handle::kStreams));
-  if (const char* e = getenv("CORAL_S1_TOP_PER_S")) h->top_per_S = atoi(e) != 0;
   if (h->lat_binom_d.ensure(sizeof(tab)) == 0)
     cudaMemcpy(h->lat_binom_d.p, tab, sizeof(tab), cudaMemcpyHostToDevice);
   const size_t smem_max = dp_smem_bytes(kMaxM, CORAL_S1_MAX_LAYER_UNITS + 1, CORAL_S1_MAX_LAYER_UNITS);
@@ -1593,25 +1590,14 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   T.rec = h->rec.as<coral_s1_record>() + h->cand_off[mp];
   T.win = h->win.as<int4>() + h->cand_off[mp];
   T.ranks = ranks;
-  if (h->top_per_S) {  // one launch per S: working set value_S + f_S[S-1] stays in L2
-    for (int S = 1; S <= Smax; ++S) {
-      if (!((smask >> S) & 1u)) continue;
-      T.smask = 1u << S;
-      lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
-      LAUNCH_CHECK(h);
-      lat_decode_kernel<<<(unsigned)((ncombo + 255) / 256), 256, 0, st>>>(T);
-      LAUNCH_CHECK(h);
-    }
-  } else {
-    const int ti = timed_begin(h, st, 0);
-    lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
-    timed_end(h, st, ti);
-    LAUNCH_CHECK(h);
-    const int td = timed_begin(h, st, 3);
-    lat_decode_kernel<<<(unsigned)((ncombo + 255) / 256), 256, 0, st>>>(T);
-    timed_end(h, st, td);
-    LAUNCH_CHECK(h);
-  }
+  const int ti = timed_begin(h, st, 0);
+  lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
+  timed_end(h, st, ti);
+  LAUNCH_CHECK(h);
+  const int td = timed_begin(h, st, 3);
+  lat_decode_kernel<<<(unsigned)((ncombo + 255) / 256), 256, 0, st>>>(T);
+  timed_end(h, st, td);
+  LAUNCH_CHECK(h);
   return 0;
 }
 

@@ -108,30 +108,6 @@ __device__ __forceinline__ int lat_tokens(const int* __restrict__ inv_rank, unsi
   return C;
 }
 
-// maxn[idx] = max |combo| over the model's candidates containing state idx.
-// One thread per candidate, looping over its sub-multiset codes.
-__global__ void lat_maxn_kernel(LatModel L, const int* __restrict__ inv_rank,
-                                const unsigned long long* __restrict__ keys, long long ncombo,
-                                unsigned* __restrict__ maxn) {
-  const long long ci = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (ci >= ncombo) return;
-  int cfg[kMaxC], cnt[kMaxC];
-  const int C = lat_tokens(inv_rank, keys[ci], cfg, cnt);
-  int M = 1, n = 0;
-  for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; }
-  int d[kMaxC] = {0, 0, 0, 0, 0, 0};
-  for (int code = 1; code < M; ++code) {
-    for (int c = 0; c < C; ++c) {  // odometer increment = next mixed-radix code
-      if (++d[c] <= cnt[c]) break;
-      d[c] = 0;
-    }
-    int s;
-    const long long r = lat_rank_tokens(L, cfg, d, C, &s);
-    if (s > L.R) continue;
-    if (maxn[r] < (unsigned)n) atomicMax(maxn + r, (unsigned)n);  // popular states saturate fast
-  }
-}
-
 // Closed form of maxn (a superset of the exact one, so it can only add cells):
 // maxn(X) = |X| + max k such that some k configs E make lo <= mem(X)+mem(E) < hi
 // (templates.py:107-111 window), with a relative slack eps; sums[soff[k]..soff[k+1])

@@ -210,64 +210,6 @@ __device__ __forceinline__ void dp_pair(const double* __restrict__ gv,
   }
 }
 
-// N independent pairs of the monotone rule (kernels.py:210-239) advanced in lock
-// step: every chain performs exactly the reference's comparisons and (lo, hi)
-// updates, but the shared-/global-memory loads of all chains are issued together so
-// their latencies overlap. Chains with act[i] == false are left untouched.
-template <int N>
-__device__ __forceinline__ void dp_pair_multi(const double* const* gv, const double* const* hv,
-                                              const int* l, const int* jmax, const bool* act,
-                                              double* cand, int* cj) {
-  double g1[N], h1[N], gm[N], hm[N];
-  bool run[N];
-  int lo[N], hi[N];
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    if (!act[i]) continue;
-    g1[i] = gv[i][1];
-    h1[i] = hv[i][l[i] - 1];
-    gm[i] = gv[i][jmax[i]];
-    hm[i] = hv[i][l[i] - jmax[i]];
-  }
-  bool any = false;
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    run[i] = false;
-    if (!act[i]) continue;
-    if (g1[i] <= h1[i]) { cand[i] = g1[i]; cj[i] = 1; }
-    else if (gm[i] >= hm[i]) { cand[i] = hm[i]; cj[i] = jmax[i]; }
-    else { run[i] = true; lo[i] = 1; hi[i] = jmax[i]; any = true; }
-  }
-  while (any) {
-    double a[N], b[N];
-    int mid[N];
-    bool step[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      step[i] = run[i] && hi[i] - lo[i] > 1;
-      if (step[i]) {
-        mid[i] = (lo[i] + hi[i]) >> 1;
-        a[i] = gv[i][mid[i]];
-        b[i] = hv[i][l[i] - mid[i]];
-      }
-    }
-    any = false;
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      if (!step[i]) continue;
-      if (a[i] > b[i]) lo[i] = mid[i]; else hi[i] = mid[i];
-      any |= hi[i] - lo[i] > 1;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    if (!run[i]) continue;
-    const double vlo = hv[i][l[i] - lo[i]];
-    const double vhi = gv[i][hi[i]];
-    if (vlo >= vhi) { cand[i] = vlo; cj[i] = lo[i]; } else { cand[i] = vhi; cj[i] = hi[i]; }
-  }
-}
-
 // Run the DP for stage count S (2 <= S <= min(n, Lu)) on the value table already
 // in B.value. Leaves the answer in sh.top_val/top_u/top_j and the choices of
 // layers 2..S-1 in B.ch. All threads call.
