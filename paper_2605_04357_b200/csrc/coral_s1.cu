@@ -105,6 +105,9 @@ struct coral_s1_handle {
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
   static constexpr int kStreams = 4;
   int nstreams = kStreams;  // side streams in use (CORAL_S1_STREAMS)
+  int lat_streams = kStreams;  // streams whose lattice workspace fits in device memory
+  bool lat_ok = true;          // false: every unit runs the exact per-candidate kernel
+  size_t mem_limit = 0;        // CORAL_S1_MEM_LIMIT: cap on usable device memory (tests)
   long long lat_states = 0;
   std::vector<long long> lat_base;     // [R + 2]
   DevBuf lat_base_d, lat_binom_d, lat_key, lat_nsub, lat_off, lat_sub, lat_maxn, lat_flags_h;
@@ -1032,6 +1035,7 @@ int coral_s1_create(int device, coral_s1_handle** out) {
     cudaEventCreate(&h->tev[i][1]);
   }
   if (const char* e = getenv("CORAL_S1_STREAMS")) h->nstreams = std::max(1, std::min(atoi(e), coral_s1_handle::kStreams));
+  if (const char* e = getenv("CORAL_S1_MEM_LIMIT")) h->mem_limit = (size_t)strtoull(e, nullptr, 10);
   if (h->lat_binom_d.ensure(sizeof(tab)) == 0)
     cudaMemcpy(h->lat_binom_d.p, tab, sizeof(tab), cudaMemcpyHostToDevice);
   const size_t smem_max = dp_smem_bytes(kMaxM, CORAL_S1_MAX_LAYER_UNITS + 1, CORAL_S1_MAX_LAYER_UNITS);
@@ -1506,13 +1510,35 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
       LAUNCH_CHECK(h);
     }
   }
-  // workspaces
+  // workspaces: one chain per stream, as many streams as fit in device memory (the
+  // tables grow as C(K + n_max - 2, n_max - 1) x Lu); none fitting -> every unit takes
+  // the exact per-candidate kernel (no lattice tables needed)
   const long long LuP = lat_pitch(h->maxLu);
   const long long nS = std::max(h->n_max - 1, 1);                         // S = 2..n_max
   const long long nch = std::max((h->n_max - 2) * (h->n_max - 1) / 2, 1);  // (S, sg) choice layers
-  for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
-    if ((rc = h->ws_value[i].ensure(nS * ns * LuP * 8)) || (rc = h->ws_f0[i].ensure(2 * nS * ns * LuP * 8)) ||
-        (rc = h->ws_ch[i].ensure(nch * ns * LuP * 2)))
+  const size_t want_v = (size_t)(nS * ns * LuP * 8), want_f = 2 * want_v, want_c = (size_t)(nch * ns * LuP * 2);
+  size_t free_b = 0, total_b = 0;
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  if (h->mem_limit) {
+    size_t used = 0;  // what this handle already holds counts as used against the cap
+    for (int i = 0; i < coral_s1_handle::kStreams; ++i) used += h->ws_value[i].cap + h->ws_f0[i].cap + h->ws_ch[i].cap;
+    free_b = std::min(free_b, h->mem_limit > used ? h->mem_limit - used : (size_t)0);
+  }
+  const size_t budget = free_b / 10 * 9;  // headroom for records, frontier and rank tables
+  int fit = 0;
+  size_t extra = 0;
+  for (int i = 0; i < h->nstreams; ++i) {
+    auto more = [](const DevBuf& b, size_t w) { return b.cap >= w ? (size_t)0 : w; };
+    const size_t add = more(h->ws_value[i], want_v) + more(h->ws_f0[i], want_f) + more(h->ws_ch[i], want_c);
+    if (extra + add > budget) break;
+    extra += add;
+    ++fit;
+  }
+  h->lat_streams = std::max(fit, 1);
+  h->lat_ok = fit > 0;
+  for (int i = 0; i < fit; ++i) {
+    if ((rc = h->ws_value[i].ensure(want_v)) || (rc = h->ws_f0[i].ensure(want_f)) ||
+        (rc = h->ws_ch[i].ensure(want_c)))
       return rc;
   }
   return 0;
@@ -1534,7 +1560,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   for (int S : Ss) {
     bool mono = true;  // kernels.py:291 over every config row at (mp, S)
     for (int c = 0; c < K; ++c) mono &= (h->flags_h[((size_t)mp * h->n_max + (S - 1)) * K + c] & 1) != 0;
-    if (!mono) {  // exact per-candidate kernel for this S
+    if (!mono || !h->lat_ok) {  // exact per-candidate kernel for this S
       int rc = launch_percombo(h, st, h->cand_off[mp], h->cand_off[mp + 1], 1, S, S);
       if (rc) return rc;
       continue;
@@ -1657,7 +1683,7 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
         if (take(m * h->NP + p, S)) { per_phase[p].push_back(S); any = true; }
     if (!any) continue;
     unsigned* ranks = h->ws_ranks[slot].as<unsigned>();
-    if (h->n_max >= 2 && h->lat_states > 0) {
+    if (h->n_max >= 2 && h->lat_states > 0 && h->lat_ok) {
       LatModel L{h->K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
       const long long rb = std::min<long long>((h->counts[m] + kRanksWarps - 1) / kRanksWarps, (long long)h->num_sms * h->ranks_blocks_per_sm);
       const int tr = timed_begin(h, h->side[slot], 4);
@@ -1669,7 +1695,7 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
     for (int p = 0; p < h->NP; ++p)
       if (!per_phase[p].empty() && (rc = lattice_units(h, m * h->NP + p, per_phase[p], slot, ranks)))
         return rc;
-    slot = (slot + 1) % h->nstreams;
+    slot = (slot + 1) % (h->lat_ok ? h->lat_streams : h->nstreams);
   }
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     CUDA_TRY(cudaEventRecord(h->side_ev[i], h->side[i]));

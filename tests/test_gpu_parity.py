@@ -500,3 +500,30 @@ def test_rows_monotone_only_within_tolerance_take_the_literal_search():
     lines = [template_line(t) for t in lib.entries]
     assert lines == g["library"]["records"]
     assert lines == oracle_library_lines(oracle_problem(inputs))
+
+
+@pytest.mark.parametrize("streams", [0, 2])
+def test_lattice_workspace_beyond_device_memory(streams, monkeypatch):
+    """When the lattice tables of all four chain streams do not fit in device memory,
+    fewer streams run them; when none fits, every unit takes the exact per-candidate
+    kernel. Both give the reference's library (golden core, 30,739 templates).
+    CORAL_S1_MEM_LIMIT caps the memory a fresh handle sees."""
+    from math import comb
+    from paper_2605_04357_b200 import _native
+    configs, models, slos, caps, ctx, regions, prices = workload("core")
+    _, lsteps, _ = Stage1Problem(configs, models, slos, caps, ctx).h.table_layout()
+    K, n_max = len(configs), caps.n_max
+    ns = sum(comb(K + s - 1, s) for s in range(1, n_max))
+    pitch = (int(max(lsteps)) + 2) & ~1  # lat_pitch
+    per_stream = ns * pitch * (8 * 3 * (n_max - 1) + 2 * ((n_max - 2) * (n_max - 1) // 2))
+    limit = 1 if streams == 0 else int(per_stream * streams / 0.9) + (1 << 20)
+    monkeypatch.setenv("CORAL_S1_MEM_LIMIT", str(limit))
+    fresh = _native.Handle(0)
+    monkeypatch.setitem(_native._handles, 0, fresh)
+    lib = build_library(configs, models, slos, caps, ctx)
+    assert [template_line(t) for t in lib.entries] == golden("library_core.json.gz")["records"]
+    layers = [slot for kind, slot, _, _ in fresh.kernel_timeline() if kind == 1]
+    if streams == 0:
+        assert not layers  # no lattice: per-candidate kernel only
+    else:
+        assert layers and set(layers) <= set(range(streams))
