@@ -108,6 +108,7 @@ struct coral_s1_handle {
   int lat_streams = kStreams;  // streams whose lattice workspace fits in device memory
   bool lat_ok = true;          // false: every unit runs the exact per-candidate kernel
   size_t mem_limit = 0;        // CORAL_S1_MEM_LIMIT: cap on usable device memory (tests)
+  long long lat_fit_ns = -1, lat_fit_pitch = -1;  // table shape of the last fit decision
   long long lat_states = 0;
   std::vector<long long> lat_base;     // [R + 2]
   DevBuf lat_base_d, lat_binom_d, lat_key, lat_nsub, lat_off, lat_sub, lat_maxn, lat_flags_h;
@@ -1517,6 +1518,19 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
   const long long nS = std::max(h->n_max - 1, 1);                         // S = 2..n_max
   const long long nch = std::max((h->n_max - 2) * (h->n_max - 1) / 2, 1);  // (S, sg) choice layers
   const size_t want_v = (size_t)(nS * ns * LuP * 8), want_f = 2 * want_v, want_c = (size_t)(nch * ns * LuP * 2);
+  {  // already allocated: no memory query (cudaMemGetInfo can stall the step)
+    int have = 0;
+    while (have < h->nstreams && h->ws_value[have].cap >= want_v && h->ws_f0[have].cap >= want_f &&
+           h->ws_ch[have].cap >= want_c)
+      ++have;
+    if (have == h->nstreams) {  // every stream fits
+      h->lat_streams = have;
+      h->lat_ok = true;
+      return 0;
+    }
+    if (h->lat_ok && h->lat_fit_ns == ns && h->lat_fit_pitch == LuP && have >= h->lat_streams)
+      return 0;  // same tables as the last, memory-limited decision
+  }
   size_t free_b = 0, total_b = 0;
   CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
   if (h->mem_limit) {
@@ -1536,6 +1550,8 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
   }
   h->lat_streams = std::max(fit, 1);
   h->lat_ok = fit > 0;
+  h->lat_fit_ns = ns;
+  h->lat_fit_pitch = LuP;
   for (int i = 0; i < fit; ++i) {
     if ((rc = h->ws_value[i].ensure(want_v)) || (rc = h->ws_f0[i].ensure(want_f)) ||
         (rc = h->ws_ch[i].ensure(want_c)))
