@@ -267,7 +267,7 @@ def main():
     if world > 1:
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2605_04357_b200 import _native, build_frontier, catalog
-    from paper_2605_04357_b200.frontier import _merge_across_ranks, _price_matrix
+    from paper_2605_04357_b200.frontier import _local_frontier, _merge_across_ranks, _price_matrix
     from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem
     from paper_2605_04357_b200.shard import assign_units, table_posfrac
 
@@ -290,7 +290,7 @@ def main():
             masks = assign_units(prob.counts, lsteps, smax, NP, world,
                                  table_posfrac(h, len(prob.configs)))[rank]
             h.evaluate_units(masks)
-            n_local = h.frontier(pmat)
+            n_local = _local_frontier(prob, pmat)
             return _merge_across_ranks(prob, n_local, tdist)
         h.evaluate(0, -1)
         return h.frontier(pmat)

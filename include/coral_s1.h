@@ -183,6 +183,12 @@ int coral_s1_frontier_merge_device(coral_s1_handle* h, const void* dev_items, in
  * merged with the same skyline as coral_s1_frontier_merge_device. */
 int coral_s1_frontier_merge_parts(coral_s1_handle* h, const void* dev_base, int parts, int64_t stride_bytes,
                                   int64_t item_offset_bytes, const int64_t* counts, int64_t* num_survivors);
+/* The exact bucketed prefilter of coral_s1_frontier without the final skyline: the
+ * candidates that no strictly cheaper item of this shard dominates, ready for
+ * coral_s1_frontier_export_device (multi-GPU: the merge takes the skyline of the union,
+ * which equals the global skyline). */
+int coral_s1_frontier_candidates(coral_s1_handle* h, int num_regions, const double* prices,
+                                 int64_t* num_candidates);
 
 /* ---- operator: placement_search (kernels.py:279-295), batched ----------
  * case i: counts[i*6 .. +C_i) (int64), C_i = ncfg[i] <= 6, tput rows at

@@ -109,6 +109,7 @@ def load():
             "coral_s1_set_census": (C.c_int, [vp, C.c_int]),
             "coral_s1_table_posfrac": (C.c_int, [vp, _f64p, C.c_int64]),
             "coral_s1_frontier_merge_parts": (C.c_int, [vp, vp, C.c_int, C.c_int64, C.c_int64, _i64p, _i64p]),
+            "coral_s1_frontier_candidates": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
             "coral_s1_kernel_timeline": (C.c_int, [vp, C.c_int64, _i32p, _i32p, _f64p, _f64p, _i64p]),
             "coral_s1_census": (C.c_int, [vp, _i64p]),
             "coral_s1_write_library": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_int, _i32p,
@@ -290,6 +291,13 @@ class Handle:
         n = C.c_int64()
         _check(self._lib.coral_s1_frontier(self._h, prices.shape[0], _ptr(prices, C.c_double),
                                            C.byref(n)))
+        return n.value
+
+    def frontier_candidates(self, prices) -> int:
+        """Prefiltered frontier candidates of this shard (no skyline), for a multi-GPU merge."""
+        pm = np.ascontiguousarray(prices, dtype=np.float64)
+        n = C.c_int64()
+        _check(self._lib.coral_s1_frontier_candidates(self._h, pm.shape[0], _ptr(pm, C.c_double), C.byref(n)))
         return n.value
 
     def get_frontier(self, count: int):

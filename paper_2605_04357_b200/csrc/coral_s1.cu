@@ -1764,7 +1764,8 @@ int coral_s1_get_records(coral_s1_handle* h, int mp, coral_s1_record* out, int64
   return 0;
 }
 
-int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices, int64_t* num_survivors) {
+static int frontier_run(coral_s1_handle* h, int num_regions, const double* prices, bool skyline,
+                        int64_t* num_survivors) {
   if (!h || !h->have_eval) return fail(CORAL_S1_EINVAL, "evaluate first");
   if (num_regions < 0) return fail(CORAL_S1_EINVAL, "num_regions < 0");
   CUDA_TRY(cudaSetDevice(h->device));
@@ -1832,10 +1833,27 @@ int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices,
     CUDA_TRY(cudaStreamSynchronize(st));
     n = (int64_t)ni;
   }
-  if ((rc = frontier_from_items(h, n, num_regions))) return rc;
+  if (skyline) {
+    if ((rc = frontier_from_items(h, n, num_regions))) return rc;
+  } else {  // prefiltered candidates only (their skyline is taken after the multi-GPU merge)
+    if ((rc = h->front.ensure(std::max<int64_t>(n, 1) * sizeof(coral_s1_frontier_item)))) return rc;
+    if (n)
+      CUDA_TRY(cudaMemcpyAsync(h->front.p, h->items.p, n * sizeof(coral_s1_frontier_item),
+                               cudaMemcpyDeviceToDevice, st));
+    h->nfront = n;
+  }
   CUDA_TRY(cudaEventRecord(h->ev[7], st));
   if (num_survivors) *num_survivors = h->nfront;
   return 0;
+}
+
+int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices, int64_t* num_survivors) {
+  return frontier_run(h, num_regions, prices, true, num_survivors);
+}
+
+int coral_s1_frontier_candidates(coral_s1_handle* h, int num_regions, const double* prices,
+                                 int64_t* num_candidates) {
+  return frontier_run(h, num_regions, prices, false, num_candidates);
 }
 
 int coral_s1_get_frontier(coral_s1_handle* h, coral_s1_frontier_item* out, int64_t n) {

@@ -123,6 +123,15 @@ def _gather_partials(n_local: int, export, tdist, device, item_bytes: int):
     raise RuntimeError("partial frontier capacity did not converge")
 
 
+def _local_frontier(prob: Stage1Problem, pmat) -> int:
+    """A rank's share of the frontier for the merge: its exactly prefiltered candidates
+    (items no strictly cheaper item of the shard dominates). The skyline is taken once,
+    over the union, in the merge; the skyline of the union of prefiltered shards is the
+    global skyline, because every dropped item's dominator is itself in the union or
+    dominated by a kept, cheaper one."""
+    return prob.h.frontier_candidates(pmat)
+
+
 def _merge_across_ranks(prob: Stage1Problem, n_local: int, tdist) -> int:
     """Single all-gather of the partial frontiers, then the same skyline over their
     union on every rank (associative: all ranks end identical)."""
@@ -164,7 +173,7 @@ def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,
         masks = assign_units(prob.counts, lsteps, smax, NP, tdist.get_world_size(),
                              table_posfrac(prob.h, len(prob.configs)))
         prob.h.evaluate_units(masks[tdist.get_rank()])
-        n_local = prob.h.frontier(pmat)
+        n_local = _local_frontier(prob, pmat)
         n = _merge_across_ranks(prob, n_local, tdist)
     else:
         prob.run()

@@ -232,6 +232,21 @@ def test_sharded_evaluation_and_merge_equal_single_gpu():
     dbuf = torch.from_numpy(buf).cuda()
     n = prob.h.frontier_merge_parts(dbuf.data_ptr(), stride, item, [len(p) for p in parts])
     assert prob.h.get_frontier(n).tobytes() == full.tobytes()
+    # what the ranks actually exchange: prefiltered candidates, no local skyline
+    cands = []
+    for r in range(W):
+        prob.h.evaluate_units(masks[r])
+        n = prob.h.frontier_candidates(pm)
+        cands.append(prob.h.get_frontier(n))
+    assert sum(len(c) for c in cands) >= sum(len(p) for p in parts)
+    cap = max(len(c) for c in cands) + 1
+    stride = item + cap * item
+    buf = np.zeros(W * stride, dtype=np.uint8)
+    for r, part in enumerate(cands):
+        buf[r * stride + item: r * stride + item + len(part) * item] = part.view(np.uint8)
+    dbuf = torch.from_numpy(buf).cuda()
+    n = prob.h.frontier_merge_parts(dbuf.data_ptr(), stride, item, [len(c) for c in cands])
+    assert prob.h.get_frontier(n).tobytes() == full.tobytes()
     assert _native.FRONTIER_DTYPE.itemsize == 64
 
 
