@@ -196,11 +196,13 @@ def test_random_scenarios_match_oracle(seed):
     assert [template_line(t) for t in lib.entries] == ref
 
 
-def test_sharded_evaluation_and_merge_equal_single_gpu():
+@pytest.mark.parametrize("name,W", [("core", 3), ("core", 8), ("c1", 8)])
+def test_sharded_evaluation_and_merge_equal_single_gpu(name, W):
     """(model, phase, S) unit shards + per-shard frontier + merge == full frontier
-    (the multi-GPU protocol, emulated on one device)."""
+    (the multi-GPU protocol, emulated on one device). W=8 on c1 (2 chains of <= 6 S
+    units) leaves some ranks with no units: their empty parts must merge cleanly."""
     from paper_2605_04357_b200 import _native
-    configs, models, slos, caps, ctx, regions, prices = workload("core")
+    configs, models, slos, caps, ctx, regions, prices = workload(name)
     from tests.helpers import price_matrix
     pm = price_matrix(configs, prices, regions)
     prob = Stage1Problem(configs, models, slos, caps, ctx).run()
@@ -209,7 +211,6 @@ def test_sharded_evaluation_and_merge_equal_single_gpu():
     import torch
     from paper_2605_04357_b200.shard import assign_units
     parts = []
-    W = 3
     _, lsteps, smax = prob.h.table_layout()
     from paper_2605_04357_b200.shard import table_posfrac
     masks = assign_units(prob.counts, lsteps, smax, 2, W, table_posfrac(prob.h))

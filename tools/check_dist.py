@@ -26,7 +26,7 @@ def main():
     torch.cuda.set_device(local)
     tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ok = True
-    for name in ("extended", "c3", "core"):
+    for name in ("extended", "c3", "core", "c1"):
         w = catalog.WORKLOADS[name]()
         caps, ctx = LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf, granularity=w.granularity)
         dist = build_frontier(w.configs, w.models, w.slos, caps, w.prices, regions=w.regions, ctx=ctx)
