@@ -1291,16 +1291,6 @@ int coral_s1_enumerate(coral_s1_handle* h) {
       h->counts[m] = (int64_t)nv[m];
       h->koff[m + 1] = h->koff[m] + h->counts[m];
     }
-    // lattice state tables for every model with candidates, on side stream 0 while the
-    // rest of the enumeration (compaction, sort) runs on the main stream
-    h->model_used.assign(NM, 0);
-    for (int m = 0; m < NM; ++m) h->model_used[m] = h->counts[m] > 0;
-    h->lat_ready = false;
-    if (h->n_max >= 2 && h->have_tables) {
-      if ((rc = lattice_prepare(h, h->side[0]))) return rc;
-      CUDA_TRY(cudaEventRecord(h->prep_ev, h->side[0]));
-      h->lat_ready = true;
-    }
     const int64_t nk = h->koff[NM];
     if ((rc = h->keys.ensure(std::max<int64_t>(nk, 1) * 8)) ||
         (rc = h->keys_tmp.ensure(std::max<int64_t>(nk, 1) * 8)))
@@ -1330,6 +1320,16 @@ int coral_s1_enumerate(coral_s1_handle* h) {
     strip_model_kernel<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(h->keys.as<unsigned long long>(), nk);
     h->launches += 6;
     LAUNCH_CHECK(h);
+    }
+    // lattice state tables for every model with candidates, on side stream 0; enqueued
+    // after the compaction + sort above, so the device sorts while the host prepares
+    h->model_used.assign(NM, 0);
+    for (int m = 0; m < NM; ++m) h->model_used[m] = h->counts[m] > 0;
+    h->lat_ready = false;
+    if (h->n_max >= 2 && h->have_tables) {
+      if ((rc = lattice_prepare(h, h->side[0]))) return rc;
+      CUDA_TRY(cudaEventRecord(h->prep_ev, h->side[0]));
+      h->lat_ready = true;
     }
   }
   CUDA_TRY(cudaEventRecord(h->ev[3], st));

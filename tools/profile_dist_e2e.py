@@ -47,7 +47,7 @@ def main():
         prob.h.evaluate_units(assign_units(prob.counts, lsteps, smax, NP, tdist.get_world_size(),
                                             table_posfrac(prob.h, len(prob.configs)))[tdist.get_rank()])
         mark("evaluate")
-        n_local = prob.h.frontier(pm)
+        n_local = prob.h.frontier_candidates(pm)
         mark("local frontier")
         n = _merge_across_ranks(prob, n_local, tdist)
         mark("merge")
