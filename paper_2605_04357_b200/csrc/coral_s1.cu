@@ -193,13 +193,20 @@ __global__ void tables_kernel(DevProblem P, const int64_t* __restrict__ tab_off,
 // Enumeration: thread per (model, universe rank). Universe = multisets of 1..n_max
 // of K configs, ranked size-major, lexicographic within a size (stars and bars).
 // --------------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long binom(int N, int k) {
-  if (k < 0 || N < k) return 0ull;
-  return c_binom[N][k];
-}
+constexpr int kEnumBinomRows = 72;  // N = K + n - 1 < 63 + 7 in the GPU envelope
+
 
 __global__ void enumerate_kernel(DevProblem P, int64_t U, unsigned long long* __restrict__ keys,
                                  unsigned long long* __restrict__ nvalid) {
+  // the unranking's binomials are looked up at thread-varying N: from shared memory,
+  // not the constant bank (which serialises divergent addresses)
+  __shared__ unsigned long long s_binom[kEnumBinomRows][8];
+  const int rows = min(kEnumBinomRows, P.K + P.n_max);
+  for (int i = threadIdx.x; i < rows * 8; i += blockDim.x) s_binom[i >> 3][i & 7] = c_binom[i >> 3][i & 7];
+  __syncthreads();
+  auto binom = [&](int N, int k) -> unsigned long long {
+    return (k < 0 || N < k) ? 0ull : s_binom[N][k];
+  };
   const int m = blockIdx.y;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool pass = false;
@@ -215,7 +222,12 @@ __global__ void enumerate_kernel(DevProblem P, int64_t U, unsigned long long* __
     }
     // unrank combination b_0 < ... < b_{n-1} of [0, N), N = K + n - 1 (lexicographic)
     const int N = K + n - 1;
-    int picks[kMaxC];
+    // picks stream out in non-decreasing config order (pool sorted by name): the
+    // memory sum (templates.py:109, sequential in pick order) and the packed key's
+    // (rank, count) runs are accumulated on the fly, no per-thread pick array
+    double mem = 0.0;
+    unsigned long long k54 = 0ull;
+    int ntok = 0, prev = -1, run = 0;
     int v = 0;
     for (int i = 0; i < n; ++i) {
       for (;;) {
@@ -224,31 +236,27 @@ __global__ void enumerate_kernel(DevProblem P, int64_t U, unsigned long long* __
         rr -= c;
         ++v;
       }
-      picks[i] = v - i;  // non-decreasing config index (pool sorted by name)
+      const int pick = v - i;
       ++v;
+      mem = rn_add(mem, P.mem_bytes[pick]);
+      if (pick != prev) {
+        if (run) {
+          k54 = (k54 << kKeyTokenBits) | ((unsigned long long)P.rank1[prev] << 3) | (unsigned long long)run;
+          ++ntok;
+        }
+        prev = pick;
+        run = 0;
+      }
+      ++run;
     }
-    // templates.py:109 mem = sum(c.mem_bytes for c in pick): sequential, pick order
-    double mem = 0.0;
-    for (int i = 0; i < n; ++i) mem = rn_add(mem, P.mem_bytes[picks[i]]);
+    k54 = (k54 << kKeyTokenBits) | ((unsigned long long)P.rank1[prev] << 3) | (unsigned long long)run;
+    ++ntok;
     const double wbytes = rn_mul(rn_mul(P.ptb[m], 1e9), P.bpp[m]);
     const double lo = wbytes;
     const double hi = rn_mul(P.rho, wbytes);
     if (lo <= mem && mem < hi) {
       pass = true;
-      key = 0ull;
-      int ntok = 0;
-      int i = 0;
-      while (i < n) {
-        int j = i;
-        while (j < n && picks[j] == picks[i]) ++j;
-        const unsigned long long tok =
-            ((unsigned long long)P.rank1[picks[i]] << 3) | (unsigned long long)(j - i);
-        key = (key << kKeyTokenBits) | tok;
-        ++ntok;
-        i = j;
-      }
-      key <<= kKeyTokenBits * (kMaxC - ntok);
-      key |= (unsigned long long)m << (kKeyTokenBits * kMaxC);
+      key = (k54 << (kKeyTokenBits * (kMaxC - ntok))) | ((unsigned long long)m << (kKeyTokenBits * kMaxC));
     }
   }
   if (r < U) keys[(int64_t)m * U + r] = key;

@@ -1,0 +1,29 @@
+"""Enumeration stage timing (device, CUDA events on the handle's stream) of one workload:
+python tools/enum_time.py [workload]  (CORAL_S1_LIB selects a build for A/B runs)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2605_04357_b200 import catalog  # noqa: E402
+from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem  # noqa: E402
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "c5"
+    w = catalog.WORKLOADS[name]()
+    prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho),
+                         GenContext(perf=w.perf, granularity=w.granularity))
+    ms = []
+    for _ in range(5):
+        prob.h.tables()
+        prob.h.enumerate()
+        torch.cuda.synchronize()
+        ms.append(prob.h.stage_ms()["enumerate"])
+    print(f"{name} enumerate ms: {' '.join(f'{x:.3f}' for x in ms)}  combos {sum(prob.h.num_combos())}")
+
+
+if __name__ == "__main__":
+    main()
