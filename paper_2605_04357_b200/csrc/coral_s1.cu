@@ -50,7 +50,6 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kKeyTokenBits = 9;
-constexpr unsigned long long kNoCombo = ~0ull;
 
 __constant__ unsigned long long c_binom[160][8];  // C(N, k), N < 160, k <= 7
 
@@ -100,7 +99,7 @@ struct coral_s1_handle {
   // device buffers
   DevBuf prob, tab, flags, budget, keys_raw, keys, keys_tmp, koff_d, nvalid, cand_off_d, rec, cub_tmp;
   DevBuf items, items_sorted, sort_a, sort_b, segk, scanv, flagsel, nsel, front,
-      prices, enum_tmp;
+      prices, enum_tmp, ukey_s, umem, umem_s, blkcnt, blkoff;
   DevBuf op_in, op_out, tab_off_d, win, fbucket;
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
   static constexpr int kStreams = 4;
@@ -196,8 +195,15 @@ __global__ void tables_kernel(DevProblem P, const int64_t* __restrict__ tab_off,
 constexpr int kEnumBinomRows = 72;  // N = K + n - 1 < 63 + 7 in the GPU envelope
 
 
-__global__ void enumerate_kernel(DevProblem P, int64_t U, unsigned long long* __restrict__ keys,
-                                 unsigned long long* __restrict__ nvalid) {
+// Enumeration (templates.py:99-113) in three streaming passes. The universe of
+// multisets and its memory sums are model-independent, so it is unranked ONCE per
+// solve and sorted by packed key (= str(combo) order); each model's
+// window test (weight <= mem < rho * weight) is then a stable compaction of the sorted
+// universe: model-major, library order within a model, no per-model sort.
+
+// universe element r (lexicographic multiset unranking) -> packed key54 + memory sum
+__global__ void universe_kernel(DevProblem P, int64_t U, unsigned long long* __restrict__ ukey,
+                                double* __restrict__ umem) {
   // the unranking's binomials are looked up at thread-varying N: from shared memory,
   // not the constant bank (which serialises divergent addresses)
   __shared__ unsigned long long s_binom[kEnumBinomRows][8];
@@ -207,71 +213,131 @@ __global__ void enumerate_kernel(DevProblem P, int64_t U, unsigned long long* __
   auto binom = [&](int N, int k) -> unsigned long long {
     return (k < 0 || N < k) ? 0ull : s_binom[N][k];
   };
-  const int m = blockIdx.y;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool pass = false;
-  unsigned long long key = kNoCombo;
-  if (r < U) {
-    const int K = P.K;
-    int n = 1;
-    int64_t rr = r;
-    for (; n <= P.n_max; ++n) {
-      const int64_t cnt = (int64_t)binom(K + n - 1, n);
-      if (rr < cnt) break;
-      rr -= cnt;
-    }
-    // unrank combination b_0 < ... < b_{n-1} of [0, N), N = K + n - 1 (lexicographic)
-    const int N = K + n - 1;
-    // picks stream out in non-decreasing config order (pool sorted by name): the
-    // memory sum (templates.py:109, sequential in pick order) and the packed key's
-    // (rank, count) runs are accumulated on the fly, no per-thread pick array
-    double mem = 0.0;
-    unsigned long long k54 = 0ull;
-    int ntok = 0, prev = -1, run = 0;
-    int v = 0;
-    for (int i = 0; i < n; ++i) {
-      for (;;) {
-        const int64_t c = (int64_t)binom(N - v - 1, n - i - 1);
-        if (rr < c) break;
-        rr -= c;
-        ++v;
-      }
-      const int pick = v - i;
+  if (r >= U) return;
+  const int K = P.K;
+  int n = 1;
+  int64_t rr = r;
+  for (; n <= P.n_max; ++n) {
+    const int64_t cnt = (int64_t)binom(K + n - 1, n);
+    if (rr < cnt) break;
+    rr -= cnt;
+  }
+  // unrank combination b_0 < ... < b_{n-1} of [0, N), N = K + n - 1 (lexicographic);
+  // picks b_i - i stream out in non-decreasing config order (pool sorted by name): the
+  // memory sum (templates.py:109, sequential in pick order) and the packed key's
+  // (rank, count) runs are accumulated on the fly
+  const int N = K + n - 1;
+  double mem = 0.0;
+  unsigned long long k54 = 0ull;
+  int ntok = 0, prev = -1, run = 0;
+  int v = 0;
+  for (int i = 0; i < n; ++i) {
+    for (;;) {
+      const int64_t c = (int64_t)binom(N - v - 1, n - i - 1);
+      if (rr < c) break;
+      rr -= c;
       ++v;
-      mem = rn_add(mem, P.mem_bytes[pick]);
-      if (pick != prev) {
-        if (run) {
-          k54 = (k54 << kKeyTokenBits) | ((unsigned long long)P.rank1[prev] << 3) | (unsigned long long)run;
-          ++ntok;
-        }
-        prev = pick;
-        run = 0;
-      }
-      ++run;
     }
-    k54 = (k54 << kKeyTokenBits) | ((unsigned long long)P.rank1[prev] << 3) | (unsigned long long)run;
-    ++ntok;
-    const double wbytes = rn_mul(rn_mul(P.ptb[m], 1e9), P.bpp[m]);
-    const double lo = wbytes;
-    const double hi = rn_mul(P.rho, wbytes);
-    if (lo <= mem && mem < hi) {
-      pass = true;
-      key = (k54 << (kKeyTokenBits * (kMaxC - ntok))) | ((unsigned long long)m << (kKeyTokenBits * kMaxC));
+    const int pick = v - i;
+    ++v;
+    mem = rn_add(mem, P.mem_bytes[pick]);
+    if (pick != prev) {
+      if (run) {
+        k54 = (k54 << kKeyTokenBits) | ((unsigned long long)P.rank1[prev] << 3) | (unsigned long long)run;
+        ++ntok;
+      }
+      prev = pick;
+      run = 0;
+    }
+    ++run;
+  }
+  k54 = (k54 << kKeyTokenBits) | ((unsigned long long)P.rank1[prev] << 3) | (unsigned long long)run;
+  ++ntok;
+  ukey[r] = k54 << (kKeyTokenBits * (kMaxC - ntok));
+  umem[r] = mem;
+}
+
+constexpr int kWinThreads = 256, kWinItems = 4;  // one block = 1024 consecutive elements
+
+// templates.py:110-111 window of model m, in the reference's arithmetic
+__device__ __forceinline__ void model_window(const DevProblem& P, int m, double& lo, double& hi) {
+  const double wbytes = rn_mul(rn_mul(P.ptb[m], 1e9), P.bpp[m]);
+  lo = wbytes;
+  hi = rn_mul(P.rho, wbytes);
+}
+
+// pass 1: survivors per (model, block of the sorted universe); blkcnt is model-major
+__global__ void __launch_bounds__(kWinThreads) window_count_kernel(
+    DevProblem P, int64_t U, const double* __restrict__ umem, int nblk,
+    unsigned long long* __restrict__ blkcnt) {
+  __shared__ int ws[kWinThreads / 32];
+  const int m = blockIdx.y;
+  double lo, hi;
+  model_window(P, m, lo, hi);
+  const int64_t base = (int64_t)blockIdx.x * (kWinThreads * kWinItems);
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < kWinItems; ++k) {
+    const int64_t r = base + k * kWinThreads + threadIdx.x;
+    if (r < U) {
+      const double v = umem[r];
+      c += lo <= v && v < hi;
     }
   }
-  if (r < U) keys[(int64_t)m * U + r] = key;
-  const unsigned ballot = __ballot_sync(0xffffffffu, pass);
-  if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(nvalid + m, (unsigned long long)__popc(ballot));
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kWinThreads / 32; ++w) t += ws[w];
+    blkcnt[(int64_t)m * nblk + blockIdx.x] = (unsigned long long)t;
+  }
 }
 
-struct NotNoCombo {
-  __device__ __forceinline__ bool operator()(unsigned long long k) const { return k != kNoCombo; }
-};
-
-__global__ void strip_model_kernel(unsigned long long* keys, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) keys[i] &= (1ull << (kKeyTokenBits * kMaxC)) - 1;
+// pass 2: stable compaction at the scanned block offsets (element order k-major in a
+// block, as pass 1 counted it)
+__global__ void __launch_bounds__(kWinThreads) window_select_kernel(
+    DevProblem P, int64_t U, const unsigned long long* __restrict__ ukey,
+    const double* __restrict__ umem, int nblk, const unsigned long long* __restrict__ blkoff,
+    unsigned long long* __restrict__ keys) {
+  __shared__ int ws[kWinThreads / 32];
+  const int m = blockIdx.y;
+  double lo, hi;
+  model_window(P, m, lo, hi);
+  const int64_t base = (int64_t)blockIdx.x * (kWinThreads * kWinItems);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long out = blkoff[(int64_t)m * nblk + blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kWinItems; ++k) {
+    const int64_t r = base + k * kWinThreads + threadIdx.x;
+    bool pass = false;
+    if (r < U) {
+      const double v = umem[r];
+      pass = lo <= v && v < hi;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, pass);
+    if (lane == 0) ws[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kWinThreads / 32; ++w) {
+      before += w < warp ? ws[w] : 0;
+      total += ws[w];
+    }
+    if (pass) keys[out + before + __popc(bal & ((1u << lane) - 1u))] = ukey[r];
+    out += total;
+    __syncthreads();
+  }
 }
+
+// per-model survivor counts from the scanned block offsets (offset array has NM*nblk+1)
+__global__ void window_totals_kernel(int NM, int nblk, const unsigned long long* __restrict__ blkoff,
+                                     unsigned long long* __restrict__ nvalid) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < NM) nvalid[m] = blkoff[(int64_t)(m + 1) * nblk] - blkoff[(int64_t)m * nblk];
+}
+
 
 __device__ __forceinline__ int decode_key(const DevProblem& P, unsigned long long key,
                                           int* cfg, int* cnt) {
@@ -1062,7 +1128,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
   DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->keys_tmp, &h->koff_d,
                     &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
-                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,
+                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->ukey_s, &h->umem, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
                     &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};
   for (DevBuf* b : bufs) b->release();
@@ -1271,20 +1337,46 @@ int coral_s1_enumerate(coral_s1_handle* h) {
   CUDA_TRY(cudaSetDevice(h->device));
   const int NM = h->NM;
   const int64_t U = h->U;
-  const int64_t tot = std::max<int64_t>((int64_t)NM * U, 1);
   int rc;
-  if ((rc = h->keys_raw.ensure(tot * 8)) || (rc = h->nvalid.ensure(std::max(NM, 1) * 8 + 16)))
-    return rc;
+  if ((rc = h->nvalid.ensure(std::max(NM, 1) * 8 + 16))) return rc;
   cudaStream_t st = h->stream;
   CUDA_TRY(cudaEventRecord(h->ev[2], st));
   h->counts.assign(NM, 0);
   h->koff.assign(NM + 1, 0);
   if (NM > 0 && U > 0) {
-    CUDA_TRY(cudaMemsetAsync(h->nvalid.p, 0, NM * 8, st));
-    dim3 grid((unsigned)((U + 255) / 256), NM);
-    enumerate_kernel<<<grid, 256, 0, st>>>(h->dp, U, h->keys_raw.as<unsigned long long>(),
-                                           h->nvalid.as<unsigned long long>());
+    const int nblk = (int)((U + kWinThreads * kWinItems - 1) / (kWinThreads * kWinItems));
+    const int64_t nb = (int64_t)NM * nblk;
+    if ((rc = h->keys_raw.ensure(U * 8)) || (rc = h->ukey_s.ensure(U * 8)) || (rc = h->umem.ensure(U * 8)) ||
+        (rc = h->umem_s.ensure(U * 8)) || (rc = h->blkcnt.ensure((nb + 1) * 8)) ||
+        (rc = h->blkoff.ensure((nb + 1) * 8)))
+      return rc;
+    // the universe once: keys + memory sums, sorted by key (54 bits, unique keys)
+    universe_kernel<<<(unsigned)((U + 255) / 256), 256, 0, st>>>(h->dp, U, h->keys_raw.as<unsigned long long>(),
+                                                                 h->umem.as<double>());
     LAUNCH_CHECK(h);
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, h->keys_raw.as<unsigned long long>(),
+                                    h->ukey_s.as<unsigned long long>(), h->umem.as<double>(),
+                                    h->umem_s.as<double>(), (int)U, 0, kKeyTokenBits * kMaxC, st);
+    if ((rc = ensure_tmp(h, tmp))) return rc;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, h->keys_raw.as<unsigned long long>(),
+                                             h->ukey_s.as<unsigned long long>(), h->umem.as<double>(),
+                                             h->umem_s.as<double>(), (int)U, 0, kKeyTokenBits * kMaxC, st));
+    // per-model window counts per block, one scan -> block offsets and model totals
+    window_count_kernel<<<dim3((unsigned)nblk, NM), kWinThreads, 0, st>>>(
+        h->dp, U, h->umem_s.as<double>(), nblk, h->blkcnt.as<unsigned long long>());
+    LAUNCH_CHECK(h);
+    CUDA_TRY(cudaMemsetAsync(h->blkcnt.as<unsigned long long>() + nb, 0, 8, st));
+    tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, h->blkcnt.as<unsigned long long>(),
+                                  h->blkoff.as<unsigned long long>(), (int)(nb + 1), st);
+    if ((rc = ensure_tmp(h, tmp))) return rc;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, h->blkcnt.as<unsigned long long>(),
+                                           h->blkoff.as<unsigned long long>(), (int)(nb + 1), st));
+    window_totals_kernel<<<(NM + 127) / 128, 128, 0, st>>>(NM, nblk, h->blkoff.as<unsigned long long>(),
+                                                           h->nvalid.as<unsigned long long>());
+    LAUNCH_CHECK(h);
+    h->launches += 6;
     std::vector<unsigned long long> nv(NM);
     CUDA_TRY(cudaMemcpyAsync(nv.data(), h->nvalid.p, NM * 8, cudaMemcpyDeviceToHost, st));
     // the evaluator's T-hat monotonicity flags ride on this round trip
@@ -1300,37 +1392,16 @@ int coral_s1_enumerate(coral_s1_handle* h) {
       h->koff[m + 1] = h->koff[m] + h->counts[m];
     }
     const int64_t nk = h->koff[NM];
-    if ((rc = h->keys.ensure(std::max<int64_t>(nk, 1) * 8)) ||
-        (rc = h->keys_tmp.ensure(std::max<int64_t>(nk, 1) * 8)))
-      return rc;
-    if (nk > 0) {
-    // compact the window survivors (keys carry the model index above bit 54) ...
-    size_t tmp = 0;
-    NotNoCombo pred;
-    cub::DeviceSelect::If(nullptr, tmp, h->keys_raw.as<unsigned long long>(),
-                          h->keys_tmp.as<unsigned long long>(), h->nvalid.as<long long>() + NM,
-                          (int)(NM * U), pred, st);
-    if ((rc = ensure_tmp(h, tmp))) return rc;
-    CUDA_TRY(cub::DeviceSelect::If(h->cub_tmp.p, tmp, h->keys_raw.as<unsigned long long>(),
-                                   h->keys_tmp.as<unsigned long long>(), h->nvalid.as<long long>() + NM,
-                                   (int)(NM * U), pred, st));
-    // ... then one radix sort: model-major, str(combo) order within a model
-    int mbits = 0;
-    while ((1 << mbits) < NM) ++mbits;
-    tmp = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tmp, h->keys_tmp.as<unsigned long long>(),
-                                   h->keys.as<unsigned long long>(), (int)nk, 0,
-                                   kKeyTokenBits * kMaxC + mbits, st);
-    if ((rc = ensure_tmp(h, tmp))) return rc;
-    CUDA_TRY(cub::DeviceRadixSort::SortKeys(h->cub_tmp.p, tmp, h->keys_tmp.as<unsigned long long>(),
-                                            h->keys.as<unsigned long long>(), (int)nk, 0,
-                                            kKeyTokenBits * kMaxC + mbits, st));
-    strip_model_kernel<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(h->keys.as<unsigned long long>(), nk);
-    h->launches += 6;
-    LAUNCH_CHECK(h);
+    if ((rc = h->keys.ensure(std::max<int64_t>(nk, 1) * 8))) return rc;
+    if (nk > 0) {  // model-major, str(combo) order within a model: the library order
+      window_select_kernel<<<dim3((unsigned)nblk, NM), kWinThreads, 0, st>>>(
+          h->dp, U, h->ukey_s.as<unsigned long long>(), h->umem_s.as<double>(), nblk,
+          h->blkoff.as<unsigned long long>(), h->keys.as<unsigned long long>());
+      h->launches += 1;
+      LAUNCH_CHECK(h);
     }
     // lattice state tables for every model with candidates, on side stream 0; enqueued
-    // after the compaction + sort above, so the device sorts while the host prepares
+    // after the compaction above, so the device compacts while the host prepares
     h->model_used.assign(NM, 0);
     for (int m = 0; m < NM; ++m) h->model_used[m] = h->counts[m] > 0;
     h->lat_ready = false;

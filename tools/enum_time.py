@@ -2,6 +2,7 @@
 python tools/enum_time.py [workload]  (CORAL_S1_LIB selects a build for A/B runs)."""
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -16,13 +17,18 @@ def main():
     w = catalog.WORKLOADS[name]()
     prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho),
                          GenContext(perf=w.perf, granularity=w.granularity))
-    ms = []
-    for _ in range(5):
+    ms, wall = [], []
+    for _ in range(int(os.environ.get("ENUM_ITERS", "5"))):
         prob.h.tables()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         prob.h.enumerate()
+        t1 = time.perf_counter()
         torch.cuda.synchronize()
         ms.append(prob.h.stage_ms()["enumerate"])
-    print(f"{name} enumerate ms: {' '.join(f'{x:.3f}' for x in ms)}  combos {sum(prob.h.num_combos())}")
+        wall.append(1e3 * (t1 - t0))
+    print(f"{name} enumerate ms: {' '.join(f'{x:.3f}' for x in ms)}  host call ms: "
+          f"{' '.join(f'{x:.3f}' for x in wall)}  combos {sum(prob.h.num_combos())}")
 
 
 if __name__ == "__main__":
