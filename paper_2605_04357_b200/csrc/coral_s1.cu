@@ -761,37 +761,53 @@ struct FrontArgs {
   unsigned long long* nitems;
 };
 
-// allocation.py:91-98 _template_price of candidate ci in region r; false when the
-// candidate has no template or a config is not offered (price None).
-__device__ __forceinline__ bool frontier_item(const FrontArgs& A, int64_t ci, int r,
-                                              coral_s1_frontier_item* it) {
+// One candidate of the frontier passes: its (model, phase), packed key, tokens and
+// record, fetched once and priced per region (thread per candidate, regions in a loop).
+struct FrontCand {
+  int mp, C;
+  unsigned long long key;
+  coral_s1_record rc;
+  int cfg[kMaxC], cnt[kMaxC];
+};
+// false when ci is past the end or the candidate has no template
+__device__ __forceinline__ bool frontier_cand(const FrontArgs& A, int64_t ci, FrontCand& f) {
   if (ci >= A.ncand) return false;
-  const coral_s1_record rc = A.rec[ci];
-  if (rc.num_stages == 0) return false;
+  f.rc = A.rec[ci];
+  if (f.rc.num_stages == 0) return false;
   int lo = 0, hi = A.NMP;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
     if (A.cand_off[mid] <= ci) lo = mid; else hi = mid;
   }
+  f.mp = lo;
   const int m = lo / A.P.NP;
-  const unsigned long long key = A.keys[A.koff[m] + (ci - A.cand_off[lo])];
-  int cfg[kMaxC], cnt[kMaxC];
-  const int C = decode_key(A.P, key, cfg, cnt);
-  double total = 0.0;
-  for (int c = 0; c < C; ++c) {
-    const double p = A.prices[(int64_t)r * A.P.K + cfg[c]];
-    if (isnan(p)) return false;
-    total = rn_add(total, rn_mul((double)cnt[c], p));
+  f.key = A.keys[A.koff[m] + (ci - A.cand_off[lo])];
+  // tokens are contiguous from the top: unrolled, so cfg/cnt stay in registers
+  f.C = 0;
+#pragma unroll
+  for (int t = 0; t < kMaxC; ++t) {
+    const unsigned tok = (unsigned)(f.key >> (kKeyTokenBits * (kMaxC - 1 - t))) & 511u;
+    f.cnt[t] = (int)(tok & 7u);
+    f.cfg[t] = tok ? A.P.inv_rank[(tok >> 3) - 1] : 0;
+    f.C += tok != 0u;
   }
-  it->price_usd_h = total;
-  it->throughput_tps = rc.throughput_tps;
-  it->combo_key = key;
-  it->mp = lo;
-  it->region = r;
-  it->rec = rc;
   return true;
 }
-
+// allocation.py:91-98 _template_price of the candidate in region r (combo order,
+// sequential); false when a config is not offered there (price None)
+__device__ __forceinline__ bool frontier_price(const FrontArgs& A, const FrontCand& f, int r,
+                                               double& total) {
+  total = 0.0;
+#pragma unroll
+  for (int c = 0; c < kMaxC; ++c) {
+    if (c < f.C) {
+      const double p = A.prices[(int64_t)r * A.P.K + f.cfg[c]];
+      if (isnan(p)) return false;
+      total = rn_add(total, rn_mul((double)f.cnt[c], p));
+    }
+  }
+  return true;
+}
 __device__ __forceinline__ unsigned long long dbits(double x) {
   return (unsigned long long)__double_as_longlong(x);  // monotone for x >= 0
 }
@@ -808,15 +824,17 @@ __device__ __forceinline__ int bucket_of(double price, int shift, unsigned long 
 // pass 1: per (segment, price bucket) the max throughput (bit pattern, T > 0)
 __global__ void frontier_bucket_kernel(FrontArgs A, int shift, unsigned long long base, int nb,
                                        unsigned long long* __restrict__ bmax) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  coral_s1_frontier_item it;
-  if (!frontier_item(A, t / A.R, (int)(t % A.R), &it)) return;
-  const int b = bucket_of(it.price_usd_h, shift, base, nb);
-  unsigned long long* slot = bmax + ((int64_t)it.mp * A.R + it.region) * nb + b;
-  const unsigned long long tb = dbits(it.throughput_tps);
-  if (*slot < tb) atomicMax(slot, tb);
+  FrontCand f;
+  if (!frontier_cand(A, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, f)) return;
+  const unsigned long long tb = dbits(f.rc.throughput_tps);
+  for (int r = 0; r < A.R; ++r) {
+    double price;
+    if (!frontier_price(A, f, r, price)) continue;
+    const int b = bucket_of(price, shift, base, nb);
+    unsigned long long* slot = bmax + ((int64_t)f.mp * A.R + r) * nb + b;
+    if (*slot < tb) atomicMax(slot, tb);
+  }
 }
-
 // pass 2: exclusive prefix max over the buckets of each segment (block per segment)
 __global__ void frontier_prefix_kernel(int nb, unsigned long long* __restrict__ bmax) {
   typedef cub::BlockScan<unsigned long long, 256> Scan;
@@ -842,22 +860,33 @@ __global__ void frontier_prefix_kernel(int nb, unsigned long long* __restrict__ 
 // (SURVEY.md 8c keep rule: T > running max of the earlier items).
 __global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long base, int nb,
                                       const unsigned long long* __restrict__ pmax) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  coral_s1_frontier_item it;
-  bool keep = frontier_item(A, t / A.R, (int)(t % A.R), &it);
-  if (keep && nb > 0) {
-    const int b = bucket_of(it.price_usd_h, shift, base, nb);
-    keep = dbits(it.throughput_tps) > pmax[((int64_t)it.mp * A.R + it.region) * nb + b];
-  }
-  const unsigned ballot = __ballot_sync(0xffffffffu, keep);
-  if (!ballot) return;
+  FrontCand f;
+  const bool valid = frontier_cand(A, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, f);
   const int lane = threadIdx.x & 31;
-  unsigned long long pos = 0;
-  if (lane == __ffs(ballot) - 1) pos = atomicAdd(A.nitems, (unsigned long long)__popc(ballot));
-  pos = __shfl_sync(0xffffffffu, pos, __ffs(ballot) - 1);
-  if (keep) A.items[pos + __popc(ballot & ((1u << lane) - 1u))] = it;
+  for (int r = 0; r < A.R; ++r) {  // uniform over the warp: ballots stay converged
+    double price = 0.0;
+    bool keep = valid && frontier_price(A, f, r, price);
+    if (keep && nb > 0) {
+      const int b = bucket_of(price, shift, base, nb);
+      keep = dbits(f.rc.throughput_tps) > pmax[((int64_t)f.mp * A.R + r) * nb + b];
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+    if (!ballot) continue;
+    unsigned long long pos = 0;
+    if (lane == __ffs(ballot) - 1) pos = atomicAdd(A.nitems, (unsigned long long)__popc(ballot));
+    pos = __shfl_sync(0xffffffffu, pos, __ffs(ballot) - 1);
+    if (keep) {
+      coral_s1_frontier_item it;
+      it.price_usd_h = price;
+      it.throughput_tps = f.rc.throughput_tps;
+      it.combo_key = f.key;
+      it.mp = f.mp;
+      it.region = r;
+      it.rec = f.rc;
+      A.items[pos + __popc(ballot & ((1u << lane) - 1u))] = it;
+    }
+  }
 }
-
 // cmd_sweep statistics (cli.py:233-272) for several LibraryCaps at once from one
 // solve at the widest caps: DP records do not depend on the caps, only the
 // enumeration window does (templates.py:107-111). Per candidate: window test per caps
@@ -1878,7 +1907,7 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
     // the filter exact), so it comes from the price matrix on the host: a combo costs at
     // least the cheapest offered config and at most n_max x the dearest (with margin for
     // rounding; bucket indices are clamped, which keeps the map non-decreasing).
-    const unsigned gb = (unsigned)((nmax + 255) / 256);
+    const unsigned gb = (unsigned)((h->ncand + 255) / 256);  // thread per candidate, regions looped
     unsigned long long range[2] = {~0ull, 0ull};
     {
       double pmin = HUGE_VAL, pmax = 0.0;
