@@ -1,12 +1,17 @@
 // coral_s1.cu — B200-native stage-1 Serving-Template generator: kernels + C ABI.
 //
-// Pipeline (one stream):
-//   tables_kernel      T-hat rows per (model, phase, S, config)      templates.py:83-96
-//   enumerate_kernel   unrank multiset -> memory window -> key        templates.py:99-113
-//   segmented radix sort of keys per model (str(combo) order)         templates.py:112, 340
-//   evaluate_kernel    per candidate: DP for every S, best S, decode  templates.py:308-326
-//   frontier           price -> 4 stable radix passes -> segmented
-//                      running max -> compaction
+// Pipeline:
+//   tables_kernel        T-hat rows per (model, phase, S, config)      templates.py:83-96
+//   universe_kernel      unrank every multiset once: key + memory sum templates.py:99-109
+//   pair radix sort      universe in str(combo) order                 templates.py:112, 340
+//   window_count/select  per-model memory window, stable compaction   templates.py:110-111
+//   lattice kernels      (lattice.cuh) per (model, phase, S) chains on 4 streams: the
+//                        DP of every candidate over shared sub-multiset tables,
+//                        best S, decode                               templates.py:308-326
+//   evaluate_kernel      exact per-candidate DP (memory-limited route) kernels.py:143-276
+//   frontier             price per (candidate, region) -> bucketed exact prefilter ->
+//                        stable merge sort -> segmented running max -> compaction
+//                                                                     SURVEY.md 8c
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -97,7 +102,7 @@ struct coral_s1_handle {
   int num_regions = 0;
   DevProblem dp{};
   // device buffers
-  DevBuf prob, tab, flags, budget, keys_raw, keys, keys_tmp, koff_d, nvalid, cand_off_d, rec, cub_tmp;
+  DevBuf prob, tab, flags, budget, keys_raw, keys, koff_d, nvalid, cand_off_d, rec, cub_tmp;
   DevBuf items, items_sorted, sort_a, sort_b, segk, scanv, flagsel, nsel, front,
       prices, enum_tmp, ukey_s, umem, umem_s, blkcnt, blkoff;
   DevBuf op_in, op_out, tab_off_d, win, fbucket;
@@ -1154,7 +1159,7 @@ int coral_s1_create(int device, coral_s1_handle** out) {
 int coral_s1_destroy(coral_s1_handle* h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
-  DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->keys_tmp, &h->koff_d,
+  DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->koff_d,
                     &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
                     &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->ukey_s, &h->umem, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,

@@ -1,5 +1,6 @@
 """Enumeration stage timing (device, CUDA events on the handle's stream) of one workload:
 python tools/enum_time.py [workload]  (CORAL_S1_LIB selects a build for A/B runs)."""
+import hashlib
 import os
 import sys
 import time
@@ -27,8 +28,12 @@ def main():
         torch.cuda.synchronize()
         ms.append(prob.h.stage_ms()["enumerate"])
         wall.append(1e3 * (t1 - t0))
+    prob.counts = prob.h.num_combos()
+    sha = hashlib.sha256()
+    for m in range(len(w.models)):
+        sha.update(prob.keys(m).tobytes())
     print(f"{name} enumerate ms: {' '.join(f'{x:.3f}' for x in ms)}  host call ms: "
-          f"{' '.join(f'{x:.3f}' for x in wall)}  combos {sum(prob.h.num_combos())}")
+          f"{' '.join(f'{x:.3f}' for x in wall)}  combos {sum(prob.h.num_combos())} digest {sha.hexdigest()[:16]}")
 
 
 if __name__ == "__main__":
