@@ -124,6 +124,8 @@ struct coral_s1_handle {
   bool lat_ready = false, flags_ready = false;
   std::vector<unsigned char> flags_h;
   std::vector<char> model_used;
+  std::vector<char> own_mp;  // (model, phase) chains with records from the last evaluate
+  DevBuf run_off_d, run_mp_d;
   std::vector<double> memb_h, wbytes_h;  // config memory bytes, model weight bytes
   std::vector<int> inv_rank_h;           // str rank -> config index
   double rho = 0;
@@ -764,6 +766,12 @@ struct FrontArgs {
   int R;
   coral_s1_frontier_item* items;
   unsigned long long* nitems;
+  // the prefilter passes run over the (model, phase) chains this device evaluated:
+  // thread t -> run k (run_off[k] <= t < run_off[k+1]) -> mp = run_mp[k]
+  const int64_t* run_off = nullptr;
+  const int* run_mp = nullptr;
+  int nrun = 0;
+  int64_t ntot = 0;
 };
 
 // One candidate of the frontier passes: its (model, phase), packed key, tokens and
@@ -774,19 +782,21 @@ struct FrontCand {
   coral_s1_record rc;
   int cfg[kMaxC], cnt[kMaxC];
 };
-// false when ci is past the end or the candidate has no template
-__device__ __forceinline__ bool frontier_cand(const FrontArgs& A, int64_t ci, FrontCand& f) {
-  if (ci >= A.ncand) return false;
-  f.rc = A.rec[ci];
-  if (f.rc.num_stages == 0) return false;
-  int lo = 0, hi = A.NMP;
+// false when t is past the end or the candidate has no template
+__device__ __forceinline__ bool frontier_cand(const FrontArgs& A, int64_t t, FrontCand& f) {
+  if (t >= A.ntot) return false;
+  int lo = 0, hi = A.nrun;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (A.cand_off[mid] <= ci) lo = mid; else hi = mid;
+    if (A.run_off[mid] <= t) lo = mid; else hi = mid;
   }
-  f.mp = lo;
-  const int m = lo / A.P.NP;
-  f.key = A.keys[A.koff[m] + (ci - A.cand_off[lo])];
+  const int mp = A.run_mp[lo];
+  const int64_t idx = t - A.run_off[lo];  // candidate index within its (model, phase)
+  f.rc = A.rec[A.cand_off[mp] + idx];
+  if (f.rc.num_stages == 0) return false;
+  f.mp = mp;
+  const int m = mp / A.P.NP;
+  f.key = A.keys[A.koff[m] + idx];
   // tokens are contiguous from the top: unrolled, so cfg/cnt stay in registers
   f.C = 0;
 #pragma unroll
@@ -1164,7 +1174,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
                     &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->ukey_s, &h->umem, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
-                    &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff};
+                    &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff, &h->run_off_d, &h->run_mp_d};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release(); h->ws_ranks[i].release();
@@ -1767,6 +1777,10 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
     return rc;
   cudaStream_t st = h->stream;
   const int NMP = h->NM * h->NP;
+  h->own_mp.assign(NMP, 0);
+  for (int mp = 0; mp < NMP; ++mp)
+    for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
+      if (take(mp, S)) h->own_mp[mp] = 1;
   const bool flags_were_ready = h->flags_ready;
   if (!flags_were_ready) {
     h->flags_h.assign((size_t)std::max(NMP, 1) * h->n_max * h->K, 0);
@@ -1846,6 +1860,7 @@ int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi) {
   CUDA_TRY(cudaSetDevice(h->device));
   int rc;
   if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record)))) return rc;
+  h->own_mp.assign((size_t)h->NM * h->NP, 1);
   CUDA_TRY(cudaEventRecord(h->ev[4], h->stream));
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), h->stream));
   if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 8, h->stream));
@@ -1907,12 +1922,28 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
     A.R = num_regions;
     A.items = h->items.as<coral_s1_frontier_item>();
     A.nitems = h->nsel.as<unsigned long long>();
+    {  // only the chains this device evaluated (all of them on one GPU)
+      std::vector<int64_t> roff(1, 0);
+      std::vector<int> rmp;
+      for (int mp = 0; mp < A.NMP; ++mp) {
+        const int64_t c = h->cand_off[mp + 1] - h->cand_off[mp];
+        if (!c || (mp < (int)h->own_mp.size() && !h->own_mp[mp])) continue;
+        rmp.push_back(mp);
+        roff.push_back(roff.back() + c);
+      }
+      if (rmp.empty()) rmp.push_back(0);  // keeps the device arrays non-empty (ntot = 0)
+      if ((rc = upload(h, h->run_off_d, roff)) || (rc = upload(h, h->run_mp_d, rmp))) return rc;
+      A.run_off = h->run_off_d.as<int64_t>();
+      A.run_mp = h->run_mp_d.as<int>();
+      A.nrun = (int)roff.size() - 1;
+      A.ntot = roff.back();
+    }
     // exact prefilter: per (segment, price bucket) max T -> prefix max. The bucket range
     // only has to contain every item price (any non-decreasing price -> bucket map keeps
     // the filter exact), so it comes from the price matrix on the host: a combo costs at
     // least the cheapest offered config and at most n_max x the dearest (with margin for
     // rounding; bucket indices are clamped, which keeps the map non-decreasing).
-    const unsigned gb = (unsigned)((h->ncand + 255) / 256);  // thread per candidate, regions looped
+    const unsigned gb = (unsigned)((std::max<int64_t>(A.ntot, 1) + 255) / 256);  // thread per candidate, regions looped
     unsigned long long range[2] = {~0ull, 0ull};
     {
       double pmin = HUGE_VAL, pmax = 0.0;

@@ -1,0 +1,61 @@
+"""Per-phase wall time of the multi-GPU merge (torchrun): after a barrier (so waiting
+for the slowest rank is excluded) time the candidates export, the all-gather and the
+merge on every rank. python -m torch.distributed.run --nproc-per-node N tools/profile_merge.py"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as tdist  # noqa: E402
+
+from paper_2605_04357_b200 import _native, catalog  # noqa: E402
+from paper_2605_04357_b200.frontier import _gather_partials, _price_matrix  # noqa: E402
+from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem  # noqa: E402
+from paper_2605_04357_b200.shard import assign_units, table_posfrac  # noqa: E402
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = catalog.extended_workload()
+    caps, ctx = LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf)
+    prob = Stage1Problem(w.configs, w.models, w.slos, caps, ctx)
+    _, pm = _price_matrix(prob.configs, w.prices, w.regions)
+    dev = torch.device("cuda", local)
+    item = _native.FRONTIER_DTYPE.itemsize
+    for it in range(6):
+        prob.h.tables()
+        prob.h.enumerate()
+        prob.counts = prob.h.num_combos()
+        _, lsteps, smax = prob.h.table_layout()
+        masks = assign_units(prob.counts, lsteps, smax, 2, tdist.get_world_size(),
+                             table_posfrac(prob.h, len(prob.configs)))
+        prob.h.evaluate_units(masks[tdist.get_rank()])
+        torch.cuda.synchronize()
+        tdist.barrier()
+        torch.cuda.synchronize()
+        t = [time.perf_counter()]
+        n_local = prob.h.frontier_candidates(pm)
+        t.append(time.perf_counter())
+
+        def export(buf, offset, cap):
+            prob.h.frontier_export_device(buf.data_ptr() + offset, cap)
+
+        recv, stride, counts = _gather_partials(n_local, export, tdist, dev, item)
+        t.append(time.perf_counter())
+        n = prob.h.frontier_merge_parts(recv.data_ptr(), stride, item, counts)
+        torch.cuda.synchronize()
+        t.append(time.perf_counter())
+        if it == 5:
+            d = np.diff(t) * 1e3
+            print(f"rank {tdist.get_rank()}: n_local {n_local} gathered {sum(counts)} survivors {n} | "
+                  f"candidates {d[0]:.3f} ms gather {d[1]:.3f} ms merge {d[2]:.3f} ms", flush=True)
+    tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
