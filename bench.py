@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--workload", default=WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--c5", action="store_true", help="also time BASELINE config 5 (seconds)")
+    ap.add_argument("--c5", action="store_true", help="(default) also time BASELINE config 5")
+    ap.add_argument("--no-c5", action="store_true", help="skip the BASELINE config 5 solve (seconds)")
     return ap.parse_args()
 
 
@@ -171,7 +172,7 @@ def top_kernel_bytes(counts, lsteps, smax, masks, K, n_max):
 
 
 def other_configs(args, h_main):
-    """Device time of one stage-1 solve of BASELINE configs 3 (and 5 with --c5), and of
+    """Device time of one stage-1 solve of BASELINE configs 3 and 5 (not with --no-c5), and of
     a config-4 epoch re-pricing from cached records (frontier only). Parity cases, not
     the headline."""
     import torch
@@ -179,7 +180,7 @@ def other_configs(args, h_main):
     from paper_2605_04357_b200.frontier import _price_matrix
     from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem
     out = {}
-    names = ["c3"] + (["c5"] if args.c5 else [])
+    names = ["c3"] + (["c5"] if not args.no_c5 and args.workload not in ("c5",) else [])
     for name in names:
         w = catalog.WORKLOADS[name]()
         prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho),
