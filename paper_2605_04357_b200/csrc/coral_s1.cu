@@ -779,7 +779,8 @@ struct FrontArgs {
 struct FrontCand {
   int mp, C;
   unsigned long long key;
-  coral_s1_record rc;
+  double T;      // the record's throughput (the full record is re-read for survivors only)
+  int64_t ri;    // record index
   int cfg[kMaxC], cnt[kMaxC];
 };
 // false when t is past the end or the candidate has no template
@@ -792,8 +793,11 @@ __device__ __forceinline__ bool frontier_cand(const FrontArgs& A, int64_t t, Fro
   }
   const int mp = A.run_mp[lo];
   const int64_t idx = t - A.run_off[lo];  // candidate index within its (model, phase)
-  f.rc = A.rec[A.cand_off[mp] + idx];
-  if (f.rc.num_stages == 0) return false;
+  f.ri = A.cand_off[mp] + idx;
+  // throughput + num_stages: the record's first 16 bytes (one sector either way)
+  const double2 head = *reinterpret_cast<const double2*>(A.rec + f.ri);
+  if ((__double2loint(head.y) & 0xFF) == 0) return false;  // num_stages == 0: no template
+  f.T = head.x;
   f.mp = mp;
   const int m = mp / A.P.NP;
   f.key = A.keys[A.koff[m] + idx];
@@ -841,7 +845,7 @@ __global__ void frontier_bucket_kernel(FrontArgs A, int shift, unsigned long lon
                                        unsigned long long* __restrict__ bmax) {
   FrontCand f;
   if (!frontier_cand(A, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, f)) return;
-  const unsigned long long tb = dbits(f.rc.throughput_tps);
+  const unsigned long long tb = dbits(f.T);
   for (int r = 0; r < A.R; ++r) {
     double price;
     if (!frontier_price(A, f, r, price)) continue;
@@ -883,7 +887,7 @@ __global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long
     bool keep = valid && frontier_price(A, f, r, price);
     if (keep && nb > 0) {
       const int b = bucket_of(price, shift, base, nb);
-      keep = dbits(f.rc.throughput_tps) > pmax[((int64_t)f.mp * A.R + r) * nb + b];
+      keep = dbits(f.T) > pmax[((int64_t)f.mp * A.R + r) * nb + b];
     }
     const unsigned ballot = __ballot_sync(0xffffffffu, keep);
     if (!ballot) continue;
@@ -893,11 +897,11 @@ __global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long
     if (keep) {
       coral_s1_frontier_item it;
       it.price_usd_h = price;
-      it.throughput_tps = f.rc.throughput_tps;
+      it.throughput_tps = f.T;
       it.combo_key = f.key;
       it.mp = f.mp;
       it.region = r;
-      it.rec = f.rc;
+      it.rec = A.rec[f.ri];
       A.items[pos + __popc(ballot & ((1u << lane) - 1u))] = it;
     }
   }
