@@ -198,6 +198,15 @@ def other_configs(args, h_main):
             times.append(e0.elapsed_time(e1))
         out[name] = {"candidates": prob.num_candidates, "frontier_survivors": int(n),
                      "stage1_ms": times[-1], "candidates_per_s": prob.num_candidates / (times[-1] / 1e3)}
+        # streaming-path roofline: the per-model window compaction of the
+        # last solve, CUDA events around its launch, algorithmic bytes from the library
+        ws_ms, ws_bytes = prob.h.window_select_stats()
+        if ws_ms > 0:
+            hbm = measured_peaks()[0].get("hbm_gbs", 6650.0)
+            gbs = ws_bytes / (ws_ms / 1e3) / 1e9
+            out[name]["roofline_window_select"] = {
+                "bound": "hbm", "kernel": "window_select_kernel", "achieved": gbs, "peak": hbm,
+                "unit": "GB/s", "frac": gbs / hbm, "launch_ms": ws_ms, "alg_bytes": ws_bytes}
     w = catalog.extended_workload()
     sess = FrontierSession(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf))
     ts = []

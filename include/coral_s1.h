@@ -236,6 +236,10 @@ int coral_s1_format_double(double v, char* out, int cap);
 /* device time of the last evaluate's lattice kernels of one kind (0 top cells,
  * 1 layers, 2 value tables, 3 decode, 4 sub-multiset ranks): summed CUDA-event time of each launch on its stream */
 int coral_s1_kernel_stats(const coral_s1_handle* h, int kind, double* total_ms, int64_t* launches);
+/* device time (CUDA events on the handle's stream) and algorithmic bytes of the last
+ * enumerate's window_select_kernel, the per-model memory-window compaction of
+ * templates.py:110-111 (bench roofline of the streaming path); ms = -1 if none ran */
+int coral_s1_window_select_stats(const coral_s1_handle* h, double* ms, int64_t* alg_bytes);
 /* per-launch timeline of the last evaluate's lattice kernels (kinds as above plus
  * 3 decode, 4 sub-multiset ranks): side-stream slot and begin/end in ms from the
  * evaluate's start event; up to cap launches, count in *n (diagnostics) */

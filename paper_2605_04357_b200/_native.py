@@ -106,6 +106,7 @@ def load():
                                                     _f64p, C.c_int64, _i32p, _f64p, _i64p, _i64p]),
             "coral_s1_stage_ms": (C.c_int, [vp, _f64p, _f64p, _f64p, _f64p]),
             "coral_s1_kernel_stats": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
+            "coral_s1_window_select_stats": (C.c_int, [vp, _f64p, _i64p]),
             "coral_s1_set_census": (C.c_int, [vp, C.c_int]),
             "coral_s1_table_posfrac": (C.c_int, [vp, _f64p, C.c_int64]),
             "coral_s1_frontier_merge_parts": (C.c_int, [vp, vp, C.c_int, C.c_int64, C.c_int64, _i64p, _i64p]),
@@ -367,6 +368,12 @@ class Handle:
         t, n = C.c_double(), C.c_int64()
         _check(self._lib.coral_s1_kernel_stats(self._h, kind, C.byref(t), C.byref(n)))
         return t.value, n.value
+
+    def window_select_stats(self):
+        """(ms, algorithmic bytes) of the last enumerate's window_select_kernel."""
+        t, b = C.c_double(), C.c_int64()
+        _check(self._lib.coral_s1_window_select_stats(self._h, C.byref(t), C.byref(b)))
+        return t.value, b.value
 
     def write_library(self, path: str, header: str, mp_order, model_json, phase_json, slo_json,
                       cfg_json) -> int:

@@ -137,6 +137,9 @@ struct coral_s1_handle {
   int tslot[kTimedMax] = {};
   int ntimed = 0;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t ev_ws[2] = {};  // around the last window_select_kernel launch (bench roofline)
+  bool ws_timed = false;
+  int64_t ws_bytes = 0;
   float ms[4] = {0, 0, 0, 0};
   // layer-kernel census (coral_s1_set_census): algorithmic bytes of the last evaluate
   bool census_on = false;
@@ -1147,6 +1150,7 @@ int coral_s1_create(int device, coral_s1_handle** out) {
   cudaError_t e = cudaMemcpyToSymbol(c_binom, tab, sizeof(tab));
   if (e != cudaSuccess) { delete h; return fail(CORAL_S1_ECUDA, cudaGetErrorString(e)); }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
+  for (auto& ev : h->ev_ws) cudaEventCreate(&ev);
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     cudaStreamCreateWithFlags(&h->side[i], cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&h->side_ev[i], cudaEventDisableTiming);
@@ -1186,6 +1190,8 @@ int coral_s1_destroy(coral_s1_handle* h) {
     if (h->side_ev[i]) cudaEventDestroy(h->side_ev[i]);
   }
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
+  for (auto& ev : h->ev_ws)
+    if (ev) cudaEventDestroy(ev);
   if (h->prep_ev) cudaEventDestroy(h->prep_ev);
   for (int i = 0; i < coral_s1_handle::kTimedMax; ++i) {
     if (h->tev[i][0]) cudaEventDestroy(h->tev[i][0]);
@@ -1441,12 +1447,19 @@ int coral_s1_enumerate(coral_s1_handle* h) {
     }
     const int64_t nk = h->koff[NM];
     if ((rc = h->keys.ensure(std::max<int64_t>(nk, 1) * 8))) return rc;
+    h->ws_timed = false;
     if (nk > 0) {  // model-major, str(combo) order within a model: the library order
+      CUDA_TRY(cudaEventRecord(h->ev_ws[0], st));
       window_select_kernel<<<dim3((unsigned)nblk, NM), kWinThreads, 0, st>>>(
           h->dp, U, h->ukey_s.as<unsigned long long>(), h->umem_s.as<double>(), nblk,
           h->blkoff.as<unsigned long long>(), h->keys.as<unsigned long long>());
       h->launches += 1;
       LAUNCH_CHECK(h);
+      CUDA_TRY(cudaEventRecord(h->ev_ws[1], st));
+      // its algorithmic bytes: each model reads every memory sum (8 B), each survivor's
+      // key (8 B) and writes it (8 B)
+      h->ws_bytes = (int64_t)NM * U * 8 + nk * 16;
+      h->ws_timed = true;
     }
     // lattice state tables for every model with candidates, on side stream 0; enqueued
     // after the compaction above, so the device compacts while the host prepares
@@ -2357,6 +2370,18 @@ int coral_s1_kernel_timeline(const coral_s1_handle* h, int64_t cap, int32_t* kin
     end_ms[i] = e;
   }
   if (n) *n = m;
+  return 0;
+}
+
+int coral_s1_window_select_stats(const coral_s1_handle* h, double* ms, int64_t* alg_bytes) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  float t = 0;
+  if (h->ws_timed) {
+    CUDA_TRY(cudaEventSynchronize(h->ev_ws[1]));
+    CUDA_TRY(cudaEventElapsedTime(&t, h->ev_ws[0], h->ev_ws[1]));
+  }
+  if (ms) *ms = h->ws_timed ? t : -1.0;
+  if (alg_bytes) *alg_bytes = h->ws_timed ? h->ws_bytes : 0;
   return 0;
 }
 
