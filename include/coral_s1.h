@@ -222,7 +222,16 @@ int coral_s1_write_library(coral_s1_handle* h, const char* path, const char* hea
  * over phases in phase_mask (bit = phase slot), from ONE evaluated solve. */
 int coral_s1_sweep(coral_s1_handle* h, int ncaps, const int32_t* n_max, const double* rho,
                    int num_regions, const double* prices, uint32_t phase_mask, int64_t* counts,
-                   double* best);
+                   double* best, int64_t* unpriced, int64_t* mp_counts);
+/* unpriced[k] (may be NULL): counted templates with a config unpriced in some region (the
+ * reference's cmd_sweep raises KeyError on those, cli.py:255); mp_counts[k * NM*NP + mp]
+ * (may be NULL): templates per (model, phase) slot at caps entry k (build_library raises
+ * LibraryGenError when one is zero, templates.py:499-502). */
+/* ---- feasibility check of build_library (templates.py:499-502): feasible templates per
+ * (model, phase) slot of the last evaluate into counts[NM*NP]; returns
+ * CORAL_S1_ENOTEMPLATE (slots listed in coral_s1_last_error) when an evaluated slot has
+ * none. */
+int coral_s1_feasible_counts(coral_s1_handle* h, int64_t* counts, int64_t n);
 /* ---- T-hat queries (simulator reuse): node_max_throughput
  * (perf.py:159-175, use_profile != 0) or planned_batch_and_tput (perf.py:186-230) for
  * n (config, model, phase code, j layers, budget s) against the current problem's

@@ -120,7 +120,8 @@ def load():
             "coral_s1_node_queries": (C.c_int, [vp, C.c_int64, _i32p, _i32p, _i32p, _i32p, _f64p, C.c_int,
                                                 _f64p, _i64p]),
             "coral_s1_sweep": (C.c_int, [vp, C.c_int, _i32p, _f64p, C.c_int, _f64p, C.c_uint32, _i64p,
-                                         _f64p]),
+                                         _f64p, _i64p, _i64p]),
+            "coral_s1_feasible_counts": (C.c_int, [vp, _i64p, C.c_int64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -390,15 +391,31 @@ class Handle:
         return n.value
 
     def sweep(self, n_max, rho, prices, phase_mask: int):
+        """-> (counts[k], best[k], unpriced[k], mp_counts[k, NM*NP])."""
         n_max = np.ascontiguousarray(n_max, dtype=np.int32)
         rho = np.ascontiguousarray(rho, dtype=np.float64)
         prices = np.ascontiguousarray(prices, dtype=np.float64)
-        counts = np.zeros(max(len(n_max), 1), dtype=np.int64)
-        best = np.zeros(max(len(n_max), 1))
+        k = max(len(n_max), 1)
+        counts = np.zeros(k, dtype=np.int64)
+        best = np.zeros(k)
+        unpriced = np.zeros(k, dtype=np.int64)
+        mpc = np.zeros(k * max(self.NM * self.NP, 1), dtype=np.int64)
         _check(self._lib.coral_s1_sweep(self._h, len(n_max), _ptr(n_max, C.c_int32), _ptr(rho, C.c_double),
                                         prices.shape[0], _ptr(prices, C.c_double), phase_mask,
-                                        _ptr(counts, C.c_int64), _ptr(best, C.c_double)))
-        return counts[:len(n_max)], best[:len(n_max)]
+                                        _ptr(counts, C.c_int64), _ptr(best, C.c_double),
+                                        _ptr(unpriced, C.c_int64), _ptr(mpc, C.c_int64)))
+        n = len(n_max)
+        return (counts[:n], best[:n], unpriced[:n],
+                mpc[:n * self.NM * self.NP].reshape(n, self.NM * self.NP))
+
+    def feasible_counts(self):
+        """Feasible templates per (model, phase) slot; raises LibraryGenErrorNative when an
+        evaluated slot has none (templates.py:499-502)."""
+        out = np.zeros(max(self.NM * self.NP, 1), dtype=np.int64)
+        rc = self._lib.coral_s1_feasible_counts(self._h, _ptr(out, C.c_int64), out.size)
+        if rc not in (OK, ENOTEMPLATE):
+            _check(rc)
+        return out[:self.NM * self.NP], rc == ENOTEMPLATE
 
     def node_queries(self, cfg, model, phase, j, budget, use_profile: bool):
         a = [np.ascontiguousarray(x, dtype=np.int32) for x in (cfg, model, phase, j)]
@@ -417,19 +434,57 @@ class Handle:
         return dict(zip(("tables", "enumerate", "evaluate", "frontier"), [v.value for v in vals]))
 
 
-_handles: dict = {}
+# Free handles per device. A handle carries one problem's device state (spec blob,
+# tables, keys, records, frontier), so every live Stage1Problem leases its OWN handle
+# and gives it back when it is closed or collected; stateless users (placement_search,
+# T-hat queries) lease one for the duration of the call. Released handles keep their
+# device buffers (lattice workspaces, CUB scratch) warm for the next lease.
+_pool: dict = {}
+_POOL_KEEP = 2
 
 
-def handle(device: int | None = None) -> Handle:
-    """Process-wide handle per CUDA device, bound to torch's current stream."""
+def _cuda_device(device):
     import torch
     if not torch.cuda.is_available():
         raise NativeError("no CUDA device: the stage-1 generator runs only on the GPU")
-    if device is None:
-        device = torch.cuda.current_device()
-    h = _handles.get(device)
-    if h is None:
-        h = Handle(device)
-        _handles[device] = h
+    return torch.cuda.current_device() if device is None else int(device)
+
+
+def acquire(device: int | None = None) -> Handle:
+    """Lease a handle on `device` (default: torch's current device), bound to torch's
+    current stream. The caller owns it exclusively until release()."""
+    import torch
+    device = _cuda_device(device)
+    free = _pool.setdefault(device, [])
+    h = free.pop() if free else Handle(device)
     h.set_stream(torch.cuda.current_stream(device).cuda_stream)
     return h
+
+
+def release(h: Handle) -> None:
+    """Return a leased handle; beyond _POOL_KEEP free handles per device it is destroyed."""
+    if h is None or not h._h:
+        return
+    free = _pool.setdefault(h.device, [])
+    if any(x is h for x in free):
+        return
+    if len(free) < _POOL_KEEP:
+        free.append(h)
+    else:
+        h.close()
+
+
+class lease:
+    """Context manager over acquire/release for call-scoped (stateless) users."""
+
+    def __init__(self, device: int | None = None):
+        self.device = device
+        self.h = None
+
+    def __enter__(self) -> Handle:
+        self.h = acquire(self.device)
+        return self.h
+
+    def __exit__(self, *exc):
+        release(self.h)
+        self.h = None

@@ -61,6 +61,10 @@ __constant__ unsigned long long c_binom[160][8];  // C(N, k), N < 160, k <= 7
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }  // locals free on every early return
   int ensure(size_t bytes) {
     if (bytes <= cap) return 0;
     if (p) cudaFree(p);
@@ -105,7 +109,7 @@ struct coral_s1_handle {
   DevBuf prob, tab, flags, budget, keys_raw, keys, koff_d, nvalid, cand_off_d, rec, cub_tmp;
   DevBuf items, items_sorted, sort_a, sort_b, segk, scanv, flagsel, nsel, front,
       prices, enum_tmp, ukey_s, umem, umem_s, blkcnt, blkoff;
-  DevBuf op_in, op_out, tab_off_d, win, fbucket;
+  DevBuf op_in, op_out, tab_off_d, fbucket;
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
   static constexpr int kStreams = 4;
   int nstreams = kStreams;  // side streams in use (CORAL_S1_STREAMS)
@@ -116,7 +120,7 @@ struct coral_s1_handle {
   long long lat_states = 0;
   std::vector<long long> lat_base;     // [R + 2]
   DevBuf lat_base_d, lat_binom_d, lat_key, lat_nsub, lat_off, lat_sub, lat_maxn, lat_flags_h;
-  DevBuf ws_value[kStreams], ws_f0[kStreams], ws_ch[kStreams], ws_ranks[kStreams];
+  DevBuf ws_value[kStreams], ws_f0[kStreams], ws_ch[kStreams], ws_ranks[kStreams], ws_win[kStreams];
   cudaStream_t side[kStreams] = {};
   cudaEvent_t side_ev[kStreams] = {};
   cudaEvent_t fork_ev = nullptr;
@@ -769,6 +773,7 @@ struct FrontArgs {
   int R;
   coral_s1_frontier_item* items;
   unsigned long long* nitems;
+  unsigned long long cap = 0;      // items capacity (frontier_items_kernel counts past it)
   // the prefilter passes run over the (model, phase) chains this device evaluated:
   // thread t -> run k (run_off[k] <= t < run_off[k+1]) -> mp = run_mp[k]
   const int64_t* run_off = nullptr;
@@ -897,7 +902,7 @@ __global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long
     unsigned long long pos = 0;
     if (lane == __ffs(ballot) - 1) pos = atomicAdd(A.nitems, (unsigned long long)__popc(ballot));
     pos = __shfl_sync(0xffffffffu, pos, __ffs(ballot) - 1);
-    if (keep) {
+    if (keep && pos + __popc(ballot & ((1u << lane) - 1u)) < A.cap) {  // bounded buffer: count the rest
       coral_s1_frontier_item it;
       it.price_usd_h = price;
       it.throughput_tps = f.T;
@@ -917,7 +922,9 @@ __global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long
 __global__ void sweep_kernel(FrontArgs A, int ncaps, const int* __restrict__ cap_n,
                              const double* __restrict__ cap_rho, unsigned phase_mask,
                              unsigned long long* __restrict__ counts,
-                             unsigned long long* __restrict__ best_bits) {
+                             unsigned long long* __restrict__ best_bits,
+                             unsigned long long* __restrict__ unpriced,
+                             unsigned long long* __restrict__ mp_counts) {
   const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (ci >= A.ncand) return;
   const coral_s1_record rc = A.rec[ci];
@@ -938,7 +945,10 @@ __global__ void sweep_kernel(FrontArgs A, int ncaps, const int* __restrict__ cap
     n += cnt[c];
     for (int k = 0; k < cnt[c]; ++k) mem = rn_add(mem, A.P.mem_bytes[cfg[c]]);
   }
+  // cli.py:253-258: min over every region of the combo-order sum; the reference indexes
+  // scenario.prices[(region, config)] directly, so an unpriced config is an error there
   double price = __longlong_as_double(0x7ff0000000000000ll);
+  bool all_priced = A.R > 0;
   for (int r = 0; r < A.R; ++r) {
     double total = 0.0;
     bool ok = true;
@@ -947,6 +957,7 @@ __global__ void sweep_kernel(FrontArgs A, int ncaps, const int* __restrict__ cap
       if (isnan(p)) { ok = false; break; }
       total = rn_add(total, rn_mul((double)cnt[c], p));
     }
+    all_priced &= ok;
     if (ok && total < price) price = total;
   }
   const bool priced = isfinite(price);
@@ -955,8 +966,29 @@ __global__ void sweep_kernel(FrontArgs A, int ncaps, const int* __restrict__ cap
   for (int k = 0; k < ncaps; ++k) {
     if (n > cap_n[k] || !(w <= mem && mem < rn_mul(cap_rho[k], w))) continue;
     atomicAdd(counts + k, 1ull);
+    atomicAdd(mp_counts + (int64_t)k * A.NMP + lo, 1ull);
+    if (!all_priced) atomicAdd(unpriced + k, 1ull);
     if (priced) atomicMax(best_bits + k, (unsigned long long)__double_as_longlong(eff));
   }
+}
+
+// feasible templates per (model, phase) of the last evaluate (templates.py:499-502 check)
+__global__ void feasible_count_kernel(const coral_s1_record* __restrict__ rec, const int64_t* __restrict__ cand_off,
+                                      int NMP, int64_t ncand, unsigned long long* __restrict__ out) {
+  const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool f = ci < ncand && rec[ci].num_stages != 0;
+  int mp = 0;
+  if (ci < ncand) {
+    int lo = 0, hi = NMP;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (cand_off[mid] <= ci) lo = mid; else hi = mid;
+    }
+    mp = lo;
+  }
+  // one atomic per run of equal mp in the warp
+  const unsigned peers = __match_any_sync(0xffffffffu, f ? mp : -1);
+  if (f && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(out + mp, (unsigned long long)__popc(peers));
 }
 
 // Batched T-hat queries (perf.py:159-230) against the current spec tables: the
@@ -1180,12 +1212,13 @@ int coral_s1_destroy(coral_s1_handle* h) {
   DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->koff_d,
                     &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
-                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->ukey_s, &h->umem, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->win, &h->fbucket,
+                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->ukey_s, &h->umem, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->fbucket,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
                     &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff, &h->run_off_d, &h->run_mp_d};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release(); h->ws_ranks[i].release();
+    h->ws_win[i].release();
     if (h->side[i]) cudaStreamDestroy(h->side[i]);
     if (h->side_ev[i]) cudaEventDestroy(h->side_ev[i]);
   }
@@ -1678,7 +1711,22 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
     for (int i = 0; i < coral_s1_handle::kStreams; ++i) used += h->ws_value[i].cap + h->ws_f0[i].cap + h->ws_ch[i].cap;
     free_b = std::min(free_b, h->mem_limit > used ? h->mem_limit - used : (size_t)0);
   }
-  const size_t budget = free_b / 10 * 9;  // headroom for records, frontier and rank tables
+  // the evaluate's own buffers come after the lattice workspaces: records (32 B per
+  // candidate), and per chain stream the rank table (256 B) and winners (16 B) per
+  // candidate of the largest model; plus the bounded frontier item buffer (64 MiB)
+  size_t reserve = (size_t)64 << 20;
+  {
+    int64_t nc = 0, maxc = 1;
+    for (int m = 0; m < h->NM; ++m) { nc += h->counts[m] * h->NP; maxc = std::max<int64_t>(maxc, h->counts[m]); }
+    const size_t have_rec = h->rec.cap, want_rec = (size_t)nc * sizeof(coral_s1_record);
+    reserve += want_rec > have_rec ? want_rec - have_rec : 0;
+    for (int i = 0; i < h->nstreams; ++i) {
+      const size_t want = (size_t)maxc * (64 * sizeof(unsigned) + sizeof(int4)), have = h->ws_ranks[i].cap + h->ws_win[i].cap;
+      reserve += want > have ? want - have : 0;
+    }
+  }
+  const size_t avail = free_b / 10 * 9;  // 10% headroom for CUB scratch and the frontier sort
+  const size_t budget = avail > reserve ? avail - reserve : 0;
   int fit = 0;
   size_t extra = 0;
   for (int i = 0; i < h->nstreams; ++i) {
@@ -1770,7 +1818,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   T.off = h->lat_off.as<long long>();
   T.subtab = h->lat_sub.as<uint2>();
   T.rec = h->rec.as<coral_s1_record>() + h->cand_off[mp];
-  T.win = h->win.as<int4>() + h->cand_off[mp];
+  T.win = h->ws_win[slot].as<int4>();
   T.ranks = ranks;
   const int ti = timed_begin(h, st, 0);
   lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
@@ -1789,9 +1837,7 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   if (!h || !h->have_tables || !h->have_enum) return fail(CORAL_S1_EINVAL, "tables and enumerate first");
   CUDA_TRY(cudaSetDevice(h->device));
   int rc;
-  if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record))) ||
-      (rc = h->win.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(int4))))
-    return rc;
+  if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record)))) return rc;
   cudaStream_t st = h->stream;
   const int NMP = h->NM * h->NP;
   h->own_mp.assign(NMP, 0);
@@ -1831,8 +1877,11 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   });
   int64_t maxc = 1;
   for (int m = 0; m < h->NM; ++m) maxc = std::max<int64_t>(maxc, h->counts[m]);
+  // per chain stream: the model's sub-multiset rank table and the top cells' winners
+  // (both stream-ordered within a model's chains, so one buffer per stream suffices)
   for (int i = 0; i < h->nstreams; ++i)
-    if ((rc = h->ws_ranks[i].ensure(maxc * 64 * sizeof(unsigned)))) return rc;
+    if ((rc = h->ws_ranks[i].ensure(maxc * 64 * sizeof(unsigned))) || (rc = h->ws_win[i].ensure(maxc * sizeof(int4))))
+      return rc;
   int slot = 0;
   for (int m : order) {
     if (!h->counts[m]) continue;
@@ -1920,8 +1969,12 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
   const int64_t nmax = h->ncand * num_regions;
   int rc;
   std::vector<double> pv(prices, prices + (size_t)num_regions * h->K);
+  // the prefilter keeps a few thousand items per solve (c5: ~1e5 of 1.4e9), so the item
+  // buffer is bounded: it starts at 1 Mi items, the items pass counts past its end, and
+  // only an overflow grows it (to the exact count) and re-runs that pass
+  const int64_t icap0 = std::max<int64_t>(std::min<int64_t>(nmax, 1 << 20), (int64_t)(h->items.cap / sizeof(coral_s1_frontier_item)));
   if ((rc = upload(h, h->prices, pv)) ||
-      (rc = h->items.ensure(std::max<int64_t>(nmax, 1) * sizeof(coral_s1_frontier_item))) ||
+      (rc = h->items.ensure(std::max<int64_t>(icap0, 1) * sizeof(coral_s1_frontier_item))) ||
       (rc = h->nsel.ensure(32)))
     return rc;
   int64_t n = 0;
@@ -1987,11 +2040,18 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
       frontier_prefix_kernel<<<(unsigned)nseg, 256, 0, st>>>(nb, h->fbucket.as<unsigned long long>());
       LAUNCH_CHECK(h);
     }
-    frontier_items_kernel<<<gb, 256, 0, st>>>(A, shift, base, nb, h->fbucket.as<unsigned long long>());
-    LAUNCH_CHECK(h);
     unsigned long long ni = 0;
-    CUDA_TRY(cudaMemcpyAsync(&ni, h->nsel.p, 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int pass = 0; pass < 2; ++pass) {
+      A.items = h->items.as<coral_s1_frontier_item>();
+      A.cap = h->items.cap / sizeof(coral_s1_frontier_item);
+      frontier_items_kernel<<<gb, 256, 0, st>>>(A, shift, base, nb, h->fbucket.as<unsigned long long>());
+      LAUNCH_CHECK(h);
+      CUDA_TRY(cudaMemcpyAsync(&ni, h->nsel.p, 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      if (ni <= A.cap) break;
+      if ((rc = h->items.ensure(ni * sizeof(coral_s1_frontier_item)))) return rc;  // overflow: exact size
+      CUDA_TRY(cudaMemsetAsync(h->nsel.p, 0, 8, st));
+    }
     n = (int64_t)ni;
   }
   if (skyline) {
@@ -2092,6 +2152,10 @@ int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t*
       M *= counts[i * kMaxC + c] + 1;
     }
     if (M > kMaxM) return fail(CORAL_S1_EUNSUPPORTED, "placement_search: prod(counts+1) must be <= 64");
+    long long nodes = 0;
+    for (int c = 0; c < ncfg[i]; ++c) nodes += counts[i * kMaxC + c];
+    if (nodes > CORAL_S1_MAX_NODES)  // the DP's per-size tables hold <= 6 nodes
+      return fail(CORAL_S1_EUNSUPPORTED, "placement_search: at most 6 nodes per multiset");
     if (lsteps[i] < 1 || lsteps[i] > CORAL_S1_MAX_LAYER_UNITS)
       return fail(CORAL_S1_EUNSUPPORTED, "placement_search: 1..128 layer units");
     if (tput_off[i] < 0 || tput_off[i] + (int64_t)ncfg[i] * lsteps[i] > tput_len)
@@ -2147,7 +2211,7 @@ int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t*
 
 int coral_s1_sweep(coral_s1_handle* h, int ncaps, const int32_t* n_max, const double* rho,
                    int num_regions, const double* prices, uint32_t phase_mask, int64_t* counts,
-                   double* best) {
+                   double* best, int64_t* unpriced, int64_t* mp_counts) {
   if (!h || !h->have_eval) return fail(CORAL_S1_EINVAL, "evaluate first");
   if (ncaps < 0 || num_regions < 0) return fail(CORAL_S1_EINVAL, "bad sizes");
   for (int k = 0; k < ncaps; ++k)
@@ -2155,45 +2219,77 @@ int coral_s1_sweep(coral_s1_handle* h, int ncaps, const int32_t* n_max, const do
   CUDA_TRY(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
   int rc;
+  const int NMP = h->NM * h->NP;
   std::vector<double> pv(prices, prices + (size_t)num_regions * h->K);
   std::vector<int> nv(n_max, n_max + ncaps);
   std::vector<double> rv(rho, rho + ncaps);
   DevBuf capn, caprho, out;
+  const size_t nout = (size_t)std::max(ncaps, 1) * (3 + NMP);  // counts | best | unpriced | [caps][mp]
   if ((rc = upload(h, h->prices, pv)) || (rc = upload(h, capn, nv)) || (rc = upload(h, caprho, rv)) ||
-      (rc = out.ensure(std::max(ncaps, 1) * 16)))
+      (rc = out.ensure(nout * 8)))
     return rc;
-  CUDA_TRY(cudaMemsetAsync(out.p, 0, std::max(ncaps, 1) * 16, st));
+  CUDA_TRY(cudaMemsetAsync(out.p, 0, nout * 8, st));
   FrontArgs A;
   A.P = h->dp;
   A.keys = h->keys.as<unsigned long long>();
   A.koff = h->koff_d.as<int64_t>();
   A.cand_off = h->cand_off_d.as<int64_t>();
-  A.NMP = h->NM * h->NP;
+  A.NMP = NMP;
   A.rec = h->rec.as<coral_s1_record>();
   A.ncand = h->ncand;
   A.prices = h->prices.as<double>();
   A.R = num_regions;
   A.items = nullptr;
   A.nitems = nullptr;
+  unsigned long long* o = out.as<unsigned long long>();
+  const int nc = std::max(ncaps, 1);
   if (h->ncand > 0 && ncaps > 0) {
-    unsigned long long* o = out.as<unsigned long long>();
     sweep_kernel<<<(unsigned)((h->ncand + 255) / 256), 256, 0, st>>>(A, ncaps, capn.as<int>(), caprho.as<double>(),
-                                                                    phase_mask, o, o + ncaps);
+                                                                    phase_mask, o, o + nc, o + 2 * nc, o + 3 * nc);
     LAUNCH_CHECK(h);
   }
-  std::vector<unsigned long long> hv(2 * std::max(ncaps, 1));
-  CUDA_TRY(cudaMemcpyAsync(hv.data(), out.p, hv.size() * 8, cudaMemcpyDeviceToHost, st));
+  std::vector<unsigned long long> hv(nout);
+  CUDA_TRY(cudaMemcpyAsync(hv.data(), out.p, nout * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   for (int k = 0; k < ncaps; ++k) {
     counts[k] = (int64_t)hv[k];
-    unsigned long long b = hv[ncaps + k];
+    unsigned long long b = hv[nc + k];
     double d;
     memcpy(&d, &b, 8);
     best[k] = d;
+    if (unpriced) unpriced[k] = (int64_t)hv[2 * nc + k];
+    if (mp_counts)
+      for (int mp = 0; mp < NMP; ++mp) mp_counts[(size_t)k * NMP + mp] = (int64_t)hv[3 * nc + (size_t)k * NMP + mp];
   }
-  capn.release();
-  caprho.release();
-  out.release();
+  return 0;
+}
+
+int coral_s1_feasible_counts(coral_s1_handle* h, int64_t* counts, int64_t n) {
+  if (!h || !h->have_eval) return fail(CORAL_S1_EINVAL, "evaluate first");
+  const int NMP = h->NM * h->NP;
+  if (n < NMP) return fail(CORAL_S1_EINVAL, "output too small");
+  CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  DevBuf out;
+  int rc;
+  if ((rc = out.ensure((size_t)std::max(NMP, 1) * 8))) return rc;
+  CUDA_TRY(cudaMemsetAsync(out.p, 0, (size_t)std::max(NMP, 1) * 8, st));
+  if (h->ncand > 0) {
+    feasible_count_kernel<<<(unsigned)((h->ncand + 255) / 256), 256, 0, st>>>(
+        h->rec.as<coral_s1_record>(), h->cand_off_d.as<int64_t>(), NMP, h->ncand, out.as<unsigned long long>());
+    LAUNCH_CHECK(h);
+  }
+  std::vector<unsigned long long> hv(std::max(NMP, 1));
+  CUDA_TRY(cudaMemcpyAsync(hv.data(), out.p, hv.size() * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::string missing;
+  for (int mp = 0; mp < NMP; ++mp) {
+    counts[mp] = (int64_t)hv[mp];
+    const bool owned = mp >= (int)h->own_mp.size() || h->own_mp[mp];
+    if (!hv[mp] && owned) missing += (missing.empty() ? "" : ",") + std::to_string(mp);
+  }
+  // templates.py:499-502: a (model, phase) with no feasible template at all
+  if (!missing.empty()) return fail(CORAL_S1_ENOTEMPLATE, "no feasible template for (model, phase) slots " + missing);
   return 0;
 }
 

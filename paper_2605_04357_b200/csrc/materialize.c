@@ -465,7 +465,9 @@ static PyObject* load_library(PyObject* self, PyObject* args) {
     seta(pl, s_layers, layers);
     seta(pl, s_son, son);
     PyObject* key3 = PyTuple_Pack(3, model, phase, combo_str);
-    if (prev_key && sorted && PyObject_RichCompareBool(prev_key, key3, Py_GT) == 1) sorted = 0;
+    /* equal keys (a duplicate template) also clear `sorted`, so the loader re-indexes and
+       raises the reference's duplicate-template DomainError (templates.py:339-347) */
+    if (prev_key && sorted && PyObject_RichCompareBool(prev_key, key3, Py_GE) == 1) sorted = 0;
     Py_XDECREF(prev_key);
     prev_key = key3;
     Py_DECREF(combo_str);

@@ -10,8 +10,8 @@ asks for, defined exactly as the oracle in SURVEY.md 8c:
   unpriced configs drop the template) exists, sort by (p asc, T desc, str(combo) asc)
   and keep t iff T > the running max of T over the earlier ones.
 
-Everything runs on the device (pricing, 4 stable radix passes, segmented running max,
-compaction); with torch.distributed initialised the candidates are interleaved over
+Everything runs on the device (pricing, an exact bucketed prefilter, one stable sort,
+segmented running max, compaction); with torch.distributed initialised the candidates are interleaved over
 ranks and the per-rank frontiers are merged after ONE NCCL all-gather.
 """
 
@@ -280,13 +280,24 @@ def sweep(configs, models, slos, caps_list, prices, regions=None, ctx=None, phas
     """
     import time
 
-    from .library import LibraryCaps
+    from .library import LibraryCaps, LibraryGenError
     t0 = time.monotonic()
     widest = LibraryCaps(max(c.n_max for c in caps_list), max(c.rho for c in caps_list))
     prob = Stage1Problem(configs, models, slos, widest, ctx or GenContext(), phases).run()
     _, pmat = _price_matrix(prob.configs, prices, regions)
-    counts, best = prob.h.sweep([c.n_max for c in caps_list], [c.rho for c in caps_list], pmat,
-                                (1 << len(prob.phases)) - 1)
+    counts, best, unpriced, mp_counts = prob.h.sweep([c.n_max for c in caps_list], [c.rho for c in caps_list],
+                                                     pmat, (1 << len(prob.phases)) - 1)
+    NP = len(prob.phases)
+    for k, c in enumerate(caps_list):
+        # build_library at these caps raises first (templates.py:499-502) ...
+        missing = [(prob.models[mp // NP].name, prob.phases[mp % NP])
+                   for mp in range(mp_counts.shape[1]) if mp_counts[k, mp] == 0]
+        if missing:
+            raise LibraryGenError(f"no feasible template for: {sorted(missing)}")
+        # ... then cli.py:255 indexes scenario.prices[(region, config)] for every template
+        if unpriced[k]:
+            raise KeyError(f"{int(unpriced[k])} templates at caps ({c.n_max}, {c.rho}) use a config "
+                           "without a price in some region")
     wall = time.monotonic() - t0
     return [(c.n_max, c.rho, int(n), wall, float(b)) for c, n, b in zip(caps_list, counts, best)]
 

@@ -11,6 +11,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
+from .specs import DomainError
 
 NEG_INF = _native.NEG_INF
 
@@ -31,6 +32,9 @@ def placement_search_batch(cases):
         if np.any(tput < 0):
             raise ValueError("throughput table must be non-negative")
         C = cnt.shape[0]
+        if C > _native.MAX_NODES or int(cnt.sum()) > _native.MAX_NODES:
+            raise DomainError(f"placement_search on the GPU covers <= {_native.MAX_NODES} nodes "
+                              f"(got {C} configs, {int(cnt.sum())} nodes)")
         row = np.zeros(_native.MAX_NODES, dtype=np.int64)
         row[:C] = cnt
         ncfg.append(C)
@@ -40,9 +44,9 @@ def placement_search_batch(cases):
         S_arr.append(int(S))
         flat.append(tput.ravel())
         off += tput.size
-    best, sj, sc = _native.handle().placement_search(
-        np.array(ncfg), np.stack(counts), np.array(lsteps), np.array(offs),
-        np.concatenate(flat), np.array(S_arr))
+    with _native.lease() as h:
+        best, sj, sc = h.placement_search(np.array(ncfg), np.stack(counts), np.array(lsteps), np.array(offs),
+                                          np.concatenate(flat), np.array(S_arr))
     out = []
     for i, (cnt, _, S) in enumerate(cases):
         C = len(cnt)

@@ -156,7 +156,12 @@ def decode_key(key: int):
 
 
 class Stage1Problem:
-    """One stage-1 solve on one device: spec tables in, device records out."""
+    """One stage-1 solve on one device: spec tables in, device records out.
+
+    The problem leases its own device handle (_native.acquire) for its lifetime, so
+    other solves or T-hat queries issued while it is alive (a FrontierSession between
+    epochs, a lazy library before save) never touch its device state. close() (or
+    garbage collection) returns the handle to the per-device pool."""
 
     def __init__(self, configs, models, slos, caps, ctx=None, phases=PHASES, device=None):
         self.ctx = ctx or GenContext()
@@ -171,10 +176,22 @@ class Stage1Problem:
         self.cfg_by_rank = [None] * len(self.configs)
         for i, r in enumerate(rank):
             self.cfg_by_rank[r] = self.configs[i]
-        self.h = _native.handle(device)
+        self.h = None
+        self.h = _native.acquire(device)
         self.h.set_problem(self.arrays, self.scalars)
         self.counts = None
         self.cand_off = None
+
+    def close(self) -> None:
+        h, self.h = self.h, None
+        if h is not None:
+            _native.release(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
 
     # -- device stages ------------------------------------------------------------
     def run(self, shard=None):
@@ -201,6 +218,17 @@ class Stage1Problem:
 
     def records(self, mp: int) -> np.ndarray:
         return self.h.get_records(mp, int(self.counts[mp // len(self.phases)]))
+
+    def check_feasible(self):
+        """templates.py:499-502: LibraryGenError when a (model, phase) has no feasible
+        template (counted on the device; CORAL_S1_ENOTEMPLATE)."""
+        counts, bad = self.h.feasible_counts()
+        if bad:
+            NP = len(self.phases)
+            missing = [(self.models[mp // NP].name, self.phases[mp % NP])
+                       for mp in range(len(counts)) if counts[mp] == 0]
+            raise LibraryGenError(f"no feasible template for: {sorted(missing)}")
+        return counts
 
     # -- host materialisation -------------------------------------------------------
     def combo_objects(self, keys: np.ndarray) -> list:
@@ -241,11 +269,8 @@ class Stage1Problem:
         from ._lib import _materialize
         NP = len(self.phases)
         nmp = len(self.models) * NP
+        self.check_feasible()
         recs_by_mp = [self.records(mp) for mp in range(nmp)]
-        missing = [(self.models[mp // NP].name, self.phases[mp % NP]) for mp in range(nmp)
-                   if not np.any(recs_by_mp[mp]["num_stages"] > 0)]
-        if missing:
-            raise LibraryGenError(f"no feasible template for: {sorted(missing)}")
         order = sorted(range(nmp), key=lambda mp: (self.models[mp // NP].name, self.phases[mp % NP]))
         caches, keys = {}, {}
         entries = []
@@ -378,27 +403,6 @@ class TemplateLibrary:
                                                              NodeComboKey, SloSpec)
         return cls(entries=entries, meta=header, _presorted=bool(in_order))
 
-    @classmethod
-    def load_py(cls, path: str) -> "TemplateLibrary":
-        """Pure-Python twin of load (the reference's loop), kept for the tests."""
-        with open(path) as fh:
-            header = json.loads(fh.readline())
-            if header.get("format") != LIBRARY_FORMAT:
-                raise DomainError(f"{path} is not a template library file")
-            configs = {name: _config_from_meta(spec) for name, spec in header["configs"].items()}
-            entries = []
-            for line in fh:
-                if not line.strip():
-                    continue
-                rec = json.loads(line)
-                combo = NodeComboKey(tuple((configs[name], int(n)) for name, n in rec["combo"]))
-                entries.append(ServingTemplate(
-                    model=rec["model"], phase=rec["phase"], slo=SloSpec(*rec["slo"]), combo=combo,
-                    placement=Placement(rec["num_stages"], tuple(rec["layers_per_stage"]),
-                                        tuple(rec["stage_of_node"])),
-                    throughput_tps=float(rec["throughput_tps"])))
-        return cls(entries=entries, meta=header)
-
 
 # ---------------------------------------------------------------------------------
 # public operators
@@ -442,13 +446,11 @@ def enumerate_combos(configs, model, caps) -> list:
     return prob.combo_objects(keys)
 
 
-def _tables_for(configs, model, slo, phase, S, ctx):
+def _tables_for(h, configs, model, slo, phase, S, ctx):
     caps = LibraryCaps(n_max=max(1, S), rho=2.0)
-    h = _native.handle()
     arrays, scalars = _pack_problem(list(configs), [model], {model.name: slo}, (phase,), caps, ctx)
     h.set_problem(arrays, scalars)
     h.tables()
-    return h
 
 
 def throughput_table(configs, model, slo, phase, S, ctx) -> np.ndarray:
@@ -460,8 +462,9 @@ def throughput_table(configs, model, slo, phase, S, ctx) -> np.ndarray:
         raise DomainError("S must be >= 1")
     if S > min(6, model.num_layers):
         raise DomainError("GPU T-hat tables cover S <= min(6, num_layers)")
-    h = _tables_for(configs, model, slo, phase, S, ctx)
-    tab, offs, ls = h.get_tables()
+    with _native.lease() as h:
+        _tables_for(h, configs, model, slo, phase, S, ctx)
+        tab, offs, ls = h.get_tables()
     K = len(configs)
     block = tab[offs[0]:offs[1]].reshape(-1, K, lsteps)
     return block[S - 1].copy()
@@ -472,8 +475,9 @@ def stage_budget_s(model, slo, phase, S, ctx) -> float:
     if not 1 <= S <= min(6, model.num_layers):
         raise DomainError("GPU stage budgets cover 1 <= S <= min(6, num_layers)")
     cfg = NodeConfig(GpuSpec("probe", 1.0, 1.0, 1.0, 1.0), 1)
-    h = _tables_for([cfg], model, slo, phase, S, ctx)
-    return float(h.get_budgets()[0, S - 1])
+    with _native.lease() as h:
+        _tables_for(h, [cfg], model, slo, phase, S, ctx)
+        return float(h.get_budgets()[0, S - 1])
 
 
 class LazyTemplateLibrary:
@@ -492,11 +496,9 @@ class LazyTemplateLibrary:
         NP = len(prob.phases)
         self._mp_of = {(m.name, ph): mi * NP + pi for mi, m in enumerate(prob.models)
                        for pi, ph in enumerate(prob.phases)}
+        prob.check_feasible()
         self._recs = {mp: prob.records(mp) for mp in self._mp_of.values()}
         self._feas = {mp: np.nonzero(r["num_stages"] > 0)[0] for mp, r in self._recs.items()}
-        missing = [k for k, mp in self._mp_of.items() if len(self._feas[mp]) == 0]
-        if missing:
-            raise LibraryGenError(f"no feasible template for: {sorted(missing)}")
         for (mname, ph), mp in self._mp_of.items():
             model = prob.models[mp // NP]
             g = prob.ctx.layer_granularity(model)

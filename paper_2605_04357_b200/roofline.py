@@ -15,8 +15,9 @@ from .library import GenContext, LibraryCaps, _pack_problem, stage_budget_s
 from .specs import PREFILL, SloSpec
 
 
-def _problem(nodes, models, params, profile):
-    """A throw-away problem holding exactly the configs and models being queried."""
+def _problem(h, nodes, models, params, profile):
+    """A throw-away problem (on a leased handle) holding exactly the configs and models
+    being queried."""
     cfgs, seen = [], {}
     for n in nodes:
         if n.name not in seen:
@@ -30,9 +31,8 @@ def _problem(nodes, models, params, profile):
     ctx = GenContext(perf=params, profile=profile)
     arrays, scalars = _pack_problem(cfgs, mdls, {m.name: SloSpec(1.0, 1.0) for m in mdls},
                                     (PREFILL,), LibraryCaps(1, 2.0), ctx)
-    h = _native.handle()
     h.set_problem(arrays, scalars)
-    return h, seen, mseen
+    return seen, mseen
 
 
 def node_queries(queries, params, profile=None, use_profile=True):
@@ -43,10 +43,11 @@ def node_queries(queries, params, profile=None, use_profile=True):
     for _, _, phase, j, budget in queries:
         if not (budget > 0 and j >= 1):  # perf.py:189 assert
             raise AssertionError("stage_budget_s > 0 and j >= 1 required")
-    h, cidx, midx = _problem([q[0] for q in queries], [q[1] for q in queries], params, profile)
-    tput, batch = h.node_queries([cidx[q[0].name] for q in queries], [midx[q[1].name] for q in queries],
-                                 [_native.PHASE_CODE[q[2]] for q in queries], [q[3] for q in queries],
-                                 [q[4] for q in queries], use_profile and profile is not None)
+    with _native.lease() as h:
+        cidx, midx = _problem(h, [q[0] for q in queries], [q[1] for q in queries], params, profile)
+        tput, batch = h.node_queries([cidx[q[0].name] for q in queries], [midx[q[1].name] for q in queries],
+                                     [_native.PHASE_CODE[q[2]] for q in queries], [q[3] for q in queries],
+                                     [q[4] for q in queries], use_profile and profile is not None)
     return tput.tolist(), batch.tolist()
 
 

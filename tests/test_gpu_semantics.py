@@ -147,3 +147,58 @@ def test_reference_objects_are_accepted_duck_typed():
     lib = build_library([N(gpu, 2)], [M8], {"m8": SLO}, LibraryCaps(2, 12.0), CTX)
     ref = build_library([FAST], [M8], {"m8": SLO}, LibraryCaps(2, 12.0), CTX)
     assert [template_line(t) for t in lib.entries] == [template_line(t) for t in ref.entries]
+
+
+def test_live_problems_keep_their_own_device_state(tmp_path):
+    """a FrontierSession and a lazy library keep reading their own device
+    records while other solves and T-hat queries run in between."""
+    import hashlib
+    from paper_2605_04357_b200 import FrontierSession, build_frontier, node_max_throughput
+    from tests.helpers import golden, workload
+    configs, models, slos, caps, ctx, regions, prices = workload("core")
+    sess = FrontierSession(configs, models, slos, caps, ctx)
+    first = sess.frontier(prices, regions=regions)
+    lazy = build_library(configs, models, slos, caps, ctx, lazy=True)
+    c1 = workload("c1")
+    build_frontier(c1[0], c1[1], c1[2], c1[3], c1[6], regions=c1[5], ctx=c1[4])
+    build_library(*c1[:5])
+    node_max_throughput(c1[0][0], c1[1][0], "decode", 8, 0.05, c1[4].perf)
+    again = sess.frontier(prices, regions=regions)
+
+    def rows(f):
+        return sorted((k, str(e.template.combo), e.price_usd_h, e.throughput_tps)
+                      for k, v in f.segments.items() for e in v)
+    assert rows(again) == rows(first)
+    path = str(tmp_path / "core.jsonl")
+    lazy.save(path)
+    ref = golden("saved_libraries.json.gz")["core"]
+    assert hashlib.sha256(open(path, "rb").read()).hexdigest() == ref["sha256"]
+
+
+def test_placement_search_beyond_six_nodes_is_rejected():
+    """more than 6 nodes would overrun the DP's per-size tables; the GPU
+    operator raises DomainError instead (reference accepts them on the CPU)."""
+    with pytest.raises(DomainError):
+        placement_search(np.array([7]), np.ones((1, 8)), 2)
+    with pytest.raises(DomainError):
+        placement_search(np.array([4, 3]), np.ones((2, 8)), 7)
+    # S above the node count stays the reference's infeasible answer (kernels.py:174-175)
+    best, sj, sc = placement_search(np.array([2, 1]), np.ones((2, 8)), 5)
+    assert best == -1e300
+
+
+def test_sweep_raises_like_build_library_and_cmd_sweep():
+    """the one-solve sweep raises LibraryGenError when a caps entry leaves a
+    (model, phase) without templates (templates.py:499-502), and KeyError when a
+    template uses a config unpriced in some region (cli.py:255)."""
+    from paper_2605_04357_b200.frontier import sweep
+    big = ModelSpec("big", num_layers=8, params_total_b=60, params_active_b=60, hidden_size=5120)
+    p = {("r", FAST.name): 2.0, ("r", SLOW.name): 1.0}
+    rows = sweep([FAST, SLOW], [big], {"big": SLO}, [LibraryCaps(3, 12.0)], p, regions=["r"], ctx=CTX)
+    assert rows[0][2] > 0
+    with pytest.raises(LibraryGenError):  # one node of <= 160 GB cannot hold 120 GB x rho window... caps n_max=1
+        sweep([SLOW], [big], {"big": SLO}, [LibraryCaps(1, 1.5), LibraryCaps(3, 12.0)],
+              {("r", SLOW.name): 1.0}, regions=["r"], ctx=CTX)
+    with pytest.raises(KeyError):
+        sweep([FAST, SLOW], [big], {"big": SLO}, [LibraryCaps(3, 12.0)], {("r", FAST.name): 2.0},
+              regions=["r"], ctx=CTX)

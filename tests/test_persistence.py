@@ -40,3 +40,19 @@ def test_python_save_is_byte_identical_to_reference(name):
         back = TemplateLibrary.load(path)
         assert [t.template_id for t in back.entries] == [t.template_id for t in lib.entries]
         assert [t.throughput_tps for t in back.entries] == [t.throughput_tps for t in lib.entries]
+
+
+def test_load_rejects_duplicate_templates(tmp_path):
+    """A saved file with the same template twice: load raises the reference's
+    DomainError('duplicate template ...') (templates.py:339-347), even though the
+    duplicate lines are adjacent (in order)."""
+    from paper_2605_04357_b200.specs import DomainError
+    lib = library_from_lines("c1", golden("library_c1.json.gz")["records"])
+    path = str(tmp_path / "lib.jsonl")
+    lib.save(path)
+    lines = open(path).read().splitlines(keepends=True)
+    dup = str(tmp_path / "dup.jsonl")
+    with open(dup, "w") as fh:
+        fh.writelines(lines[:3] + [lines[2]] + lines[3:])
+    with pytest.raises(DomainError, match="duplicate template"):
+        TemplateLibrary.load(dup)
