@@ -115,6 +115,16 @@ typedef struct coral_s1_frontier_item {
   coral_s1_record rec;
 } coral_s1_frontier_item; /* 64 bytes */
 
+/* One stage-2 allocation variable nu[region][template] (allocation.py:154-163). */
+typedef struct coral_s1_alloc_var {
+  uint64_t combo_key;             /* template's packed combo key */
+  int32_t mp;                     /* model * num_phases + phase slot */
+  int32_t region;                 /* index into the caller's region list */
+  int64_t ub;                     /* min(availability cap, ceil(demand / T)) >= 1 */
+  double price_usd_h;             /* allocation.py:91-98 */
+  double throughput_tps;
+} coral_s1_alloc_var; /* 40 bytes */
+
 /* ---- lifecycle -------------------------------------------------------- */
 int coral_s1_create(int device, coral_s1_handle** out);
 int coral_s1_destroy(coral_s1_handle* h);
@@ -239,6 +249,20 @@ int coral_s1_feasible_counts(coral_s1_handle* h, int64_t* counts, int64_t n);
 int coral_s1_node_queries(coral_s1_handle* h, int64_t n, const int32_t* cfg, const int32_t* model,
                           const int32_t* phase, const int32_t* j, const double* budget, int use_profile,
                           double* tput, int64_t* batch);
+/* ---- stage-2 model construction: build_allocation_model
+ * (allocation.py:108-195) over the evaluated records. prices / avail are [R*K] (NaN =
+ * unpriced), demand[NM*NP] (<= 0: the slot is skipped), mp_order lists the (model,
+ * phase) slots in library order, prune_ratio 0 disables the prune, running (mp, region,
+ * combo key) triples are exempt from it. Variables (*num_vars, reference insertion
+ * order: slot, template, region) stay on the device for coral_s1_get_allocation_vars;
+ * *num_pruned is the reference's meta["pruned_vars"]; best_eff[NM*NP] (may be NULL) the
+ * slot's best USD-h per token/s, +inf when it has no priced template (no demand row). */
+int coral_s1_allocation_model(coral_s1_handle* h, int num_regions, const double* prices, const int64_t* avail,
+                              const double* demand, int n_mp, const int32_t* mp_order, double prune_ratio,
+                              int64_t n_running, const int32_t* run_mp, const int32_t* run_region,
+                              const uint64_t* run_key, int64_t* num_vars, int64_t* num_pruned,
+                              double* best_eff);
+int coral_s1_get_allocation_vars(coral_s1_handle* h, coral_s1_alloc_var* out, int64_t n);
 /* CPython repr(float) of v into out (cap >= 40); host-only helper, no device needed */
 int coral_s1_format_double(double v, char* out, int cap);
 

@@ -54,7 +54,9 @@ RECORD_DTYPE = np.dtype([("throughput_tps", "<f8"), ("num_stages", "u1"), ("num_
 FRONTIER_DTYPE = np.dtype([("price_usd_h", "<f8"), ("throughput_tps", "<f8"),
                            ("combo_key", "<u8"), ("mp", "<i4"), ("region", "<i4"),
                            ("rec", RECORD_DTYPE)], align=True)
-assert RECORD_DTYPE.itemsize == 32 and FRONTIER_DTYPE.itemsize == 64
+ALLOC_VAR_DTYPE = np.dtype([("combo_key", "<u8"), ("mp", "<i4"), ("region", "<i4"), ("ub", "<i8"),
+                            ("price_usd_h", "<f8"), ("throughput_tps", "<f8")], align=True)
+assert RECORD_DTYPE.itemsize == 32 and FRONTIER_DTYPE.itemsize == 64 and ALLOC_VAR_DTYPE.itemsize == 40
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -122,6 +124,9 @@ def load():
             "coral_s1_sweep": (C.c_int, [vp, C.c_int, _i32p, _f64p, C.c_int, _f64p, C.c_uint32, _i64p,
                                          _f64p, _i64p, _i64p]),
             "coral_s1_feasible_counts": (C.c_int, [vp, _i64p, C.c_int64]),
+            "coral_s1_allocation_model": (C.c_int, [vp, C.c_int, _f64p, _i64p, _f64p, C.c_int, _i32p, C.c_double,
+                                                    C.c_int64, _i32p, _i32p, _u64p, _i64p, _i64p, _f64p]),
+            "coral_s1_get_allocation_vars": (C.c_int, [vp, vp, C.c_int64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -407,6 +412,25 @@ class Handle:
         n = len(n_max)
         return (counts[:n], best[:n], unpriced[:n],
                 mpc[:n * self.NM * self.NP].reshape(n, self.NM * self.NP))
+
+    def allocation_model(self, prices, avail, demand, mp_order, prune_ratio, run_mp, run_region, run_key):
+        """-> (vars ALLOC_VAR_DTYPE[n], pruned, best_eff[NM*NP]) of build_allocation_model."""
+        pm = np.ascontiguousarray(prices, dtype=np.float64)
+        av = np.ascontiguousarray(avail, dtype=np.int64)
+        dm = np.ascontiguousarray(demand, dtype=np.float64)
+        order = np.ascontiguousarray(mp_order, dtype=np.int32)
+        rm = np.ascontiguousarray(run_mp if len(run_mp) else [0], dtype=np.int32)
+        rr = np.ascontiguousarray(run_region if len(run_region) else [0], dtype=np.int32)
+        rk = np.ascontiguousarray(run_key if len(run_key) else [0], dtype=np.uint64)
+        best = np.zeros(max(self.NM * self.NP, 1))
+        nv, npr = C.c_int64(), C.c_int64()
+        _check(self._lib.coral_s1_allocation_model(
+            self._h, pm.shape[0], _ptr(pm, C.c_double), _ptr(av, C.c_int64), _ptr(dm, C.c_double), len(order),
+            _ptr(order, C.c_int32), float(prune_ratio), len(run_mp), _ptr(rm, C.c_int32), _ptr(rr, C.c_int32),
+            _ptr(rk, C.c_uint64), C.byref(nv), C.byref(npr), _ptr(best, C.c_double)))
+        out = np.zeros(max(nv.value, 1), dtype=ALLOC_VAR_DTYPE)
+        _check(self._lib.coral_s1_get_allocation_vars(self._h, out.ctypes.data_as(C.c_void_p), out.size))
+        return out[:nv.value], npr.value, best[:self.NM * self.NP]
 
     def feasible_counts(self):
         """Feasible templates per (model, phase) slot; raises LibraryGenErrorNative when an

@@ -2,9 +2,9 @@
 //
 // Pipeline:
 //   tables_kernel        T-hat rows per (model, phase, S, config)      templates.py:83-96
-//   universe_kernel      unrank every multiset once: key + memory sum templates.py:99-109
-//   pair radix sort      universe in str(combo) order                 templates.py:112, 340
-//   window_count/select  per-model memory window, stable compaction   templates.py:110-111
+//   enum_count_kernel    unrank every multiset once, directly in str(combo) order: key +
+//                        memory sum + per-model window counts         templates.py:99-112, 340
+//   window_select        per-model memory window, stable compaction   templates.py:110-111
 //   lattice kernels      (lattice.cuh) per (model, phase, S) chains on 4 streams: the
 //                        DP of every candidate over shared sub-multiset tables,
 //                        best S, decode                               templates.py:308-326
@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -106,10 +107,11 @@ struct coral_s1_handle {
   int num_regions = 0;
   DevProblem dp{};
   // device buffers
-  DevBuf prob, tab, flags, budget, keys_raw, keys, koff_d, nvalid, cand_off_d, rec, cub_tmp;
+  DevBuf prob, tab, flags, budget, keys, koff_d, nvalid, cand_off_d, rec, cub_tmp;
   DevBuf items, items_sorted, sort_a, sort_b, segk, scanv, flagsel, nsel, front,
-      prices, enum_tmp, ukey_s, umem, umem_s, blkcnt, blkoff;
-  DevBuf op_in, op_out, tab_off_d, fbucket;
+      prices, ukey_s, umem_s, blkcnt, blkoff;
+  DevBuf op_in, op_out, tab_off_d, fbucket, segbuf, avars;
+  int64_t navars = 0;
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
   static constexpr int kStreams = 4;
   int nstreams = kStreams;  // side streams in use (CORAL_S1_STREAMS)
@@ -209,70 +211,68 @@ __global__ void tables_kernel(DevProblem P, const int64_t* __restrict__ tab_off,
 constexpr int kEnumBinomRows = 72;  // N = K + n - 1 < 63 + 7 in the GPU envelope
 
 
-// Enumeration (templates.py:99-113) in three streaming passes. The universe of
-// multisets and its memory sums are model-independent, so it is unranked ONCE per
-// solve and sorted by packed key (= str(combo) order); each model's
-// window test (weight <= mem < rho * weight) is then a stable compaction of the sorted
-// universe: model-major, library order within a model, no per-model sort.
+// Enumeration (templates.py:99-113) in two streaming passes, with no sort. The universe
+// of node multisets is model-independent, and it is unranked DIRECTLY in packed-key order
+// (= str(combo) order): each model's window test (weight <= mem <
+// rho * weight) is then a stable compaction of that order -- model-major, library order
+// within a model.
+//
+// Key order: tokens ((r + 1) << 3 | count) with strictly increasing str rank r, first token
+// most significant, zero padded. Rest(r0, m) = token sequences over ranks >= r0 with total
+// count <= m, the empty one first; |Rest(r0, m)| = C(K - r0 + m, m) (multisets of size
+// <= m from K - r0 types). The sequences whose first rank is >= r number C(K - r + m, m) - 1,
+// and those with first token (r, c) number C(K - r - 1 + m - c, m - c).
 
-// universe element r (lexicographic multiset unranking) -> packed key54 + memory sum
-__global__ void universe_kernel(DevProblem P, int64_t U, unsigned long long* __restrict__ ukey,
-                                double* __restrict__ umem) {
-  // the unranking's binomials are looked up at thread-varying N: from shared memory,
-  // not the constant bank (which serialises divergent addresses)
-  __shared__ unsigned long long s_binom[kEnumBinomRows][8];
-  const int rows = min(kEnumBinomRows, P.K + P.n_max);
-  for (int i = threadIdx.x; i < rows * 8; i += blockDim.x) s_binom[i >> 3][i & 7] = c_binom[i >> 3][i & 7];
-  __syncthreads();
-  auto binom = [&](int N, int k) -> unsigned long long {
-    return (k < 0 || N < k) ? 0ull : s_binom[N][k];
-  };
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= U) return;
+constexpr int kEnumThreads = 256, kEnumItems = 4;  // one block = 1024 consecutive ranks
+constexpr int kEnumBlock = kEnumThreads * kEnumItems;
+
+// universe element `idx` (0-based among the non-empty sequences, key order) -> packed key
+// and memory sum, summed over the picks in config (name) order (templates.py:103-109)
+__device__ __forceinline__ void unrank_key(const unsigned long long (*B)[8], const DevProblem& P,
+                                           unsigned long long idx, unsigned long long& key, double& mem) {
   const int K = P.K;
-  int n = 1;
-  int64_t rr = r;
-  for (; n <= P.n_max; ++n) {
-    const int64_t cnt = (int64_t)binom(K + n - 1, n);
-    if (rr < cnt) break;
-    rr -= cnt;
-  }
-  // unrank combination b_0 < ... < b_{n-1} of [0, N), N = K + n - 1 (lexicographic);
-  // picks b_i - i stream out in non-decreasing config order (pool sorted by name): the
-  // memory sum (templates.py:109, sequential in pick order) and the packed key's
-  // (rank, count) runs are accumulated on the fly
-  const int N = K + n - 1;
-  double mem = 0.0;
-  unsigned long long k54 = 0ull;
-  int ntok = 0, prev = -1, run = 0;
-  int v = 0;
-  for (int i = 0; i < n; ++i) {
-    for (;;) {
-      const int64_t c = (int64_t)binom(N - v - 1, n - i - 1);
-      if (rr < c) break;
-      rr -= c;
-      ++v;
+  int m = P.n_max, r0 = 0, ntok = 0;
+  int tcfg[kMaxC], tcnt[kMaxC];
+  key = 0ull;
+  for (;;) {
+    // first rank r: the largest r with #(first rank < r) <= idx
+    const unsigned long long tot0 = B[K - r0 + m][m] - 1ull;
+    int lo = r0, hi = K - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tot0 - (B[K - mid + m][m] - 1ull) <= idx) lo = mid; else hi = mid - 1;
     }
-    const int pick = v - i;
-    ++v;
-    mem = rn_add(mem, P.mem_bytes[pick]);
-    if (pick != prev) {
-      if (run) {
-        k54 = (k54 << kKeyTokenBits) | ((unsigned long long)P.rank1[prev] << 3) | (unsigned long long)run;
-        ++ntok;
-      }
-      prev = pick;
-      run = 0;
+    const int r = lo;
+    idx -= tot0 - (B[K - r + m][m] - 1ull);
+    int c = 1;
+    for (;; ++c) {  // first token (r, c): blocks of C(K - r - 1 + m - c, m - c)
+      const unsigned long long blk = B[K - r - 1 + m - c][m - c];
+      if (idx < blk) break;
+      idx -= blk;
     }
-    ++run;
+    key = (key << kKeyTokenBits) | ((unsigned long long)(r + 1) << 3) | (unsigned long long)c;
+    tcfg[ntok] = P.inv_rank[r];
+    tcnt[ntok] = c;
+    ++ntok;
+    if (idx == 0ull) break;  // the empty rest
+    --idx;
+    r0 = r + 1;
+    m -= c;
   }
-  k54 = (k54 << kKeyTokenBits) | ((unsigned long long)P.rank1[prev] << 3) | (unsigned long long)run;
-  ++ntok;
-  ukey[r] = k54 << (kKeyTokenBits * (kMaxC - ntok));
-  umem[r] = mem;
+  key <<= kKeyTokenBits * (kMaxC - ntok);
+  // picks in config-index (name) order: sort the <= 6 tokens by config
+  for (int a = 1; a < ntok; ++a)
+    for (int b = a; b > 0 && tcfg[b - 1] > tcfg[b]; --b) {
+      const int t0 = tcfg[b], t1 = tcnt[b];
+      tcfg[b] = tcfg[b - 1];
+      tcnt[b] = tcnt[b - 1];
+      tcfg[b - 1] = t0;
+      tcnt[b - 1] = t1;
+    }
+  mem = 0.0;
+  for (int t = 0; t < ntok; ++t)
+    for (int k = 0; k < tcnt[t]; ++k) mem = rn_add(mem, P.mem_bytes[tcfg[t]]);
 }
-
-constexpr int kWinThreads = 256, kWinItems = 4;  // one block = 1024 consecutive elements
 
 // templates.py:110-111 window of model m, in the reference's arithmetic
 __device__ __forceinline__ void model_window(const DevProblem& P, int m, double& lo, double& hi) {
@@ -281,67 +281,104 @@ __device__ __forceinline__ void model_window(const DevProblem& P, int m, double&
   hi = rn_mul(P.rho, wbytes);
 }
 
-// pass 1: survivors per (model, block of the sorted universe); blkcnt is model-major
-__global__ void __launch_bounds__(kWinThreads) window_count_kernel(
-    DevProblem P, int64_t U, const double* __restrict__ umem, int nblk,
+// pass 1: thread t of block b unranks elements b * 1024 + 4t .. +3 (key order), stores
+// their keys and memory sums (16 B each, read once by pass 2) and counts each model's
+// window survivors per block: blkcnt[m * nblk + b] (model-major)
+__global__ void __launch_bounds__(kEnumThreads) enum_count_kernel(
+    DevProblem P, int64_t U, int nblk, unsigned long long* __restrict__ ukey, double* __restrict__ umem,
     unsigned long long* __restrict__ blkcnt) {
-  __shared__ int ws[kWinThreads / 32];
-  const int m = blockIdx.y;
-  double lo, hi;
-  model_window(P, m, lo, hi);
-  const int64_t base = (int64_t)blockIdx.x * (kWinThreads * kWinItems);
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < kWinItems; ++k) {
-    const int64_t r = base + k * kWinThreads + threadIdx.x;
-    if (r < U) {
-      const double v = umem[r];
-      c += lo <= v && v < hi;
-    }
-  }
-  c = __reduce_add_sync(0xffffffffu, c);
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __shared__ unsigned long long s_binom[kEnumBinomRows][8];
+  extern __shared__ unsigned s_wcnt[];  // [NM] window counts of this block
+  const int rows = min(kEnumBinomRows, P.K + P.n_max + 1);
+  for (int i = threadIdx.x; i < rows * 8; i += blockDim.x) s_binom[i >> 3][i & 7] = c_binom[i >> 3][i & 7];
+  for (int m = threadIdx.x; m < P.NM; m += blockDim.x) s_wcnt[m] = 0u;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < kWinThreads / 32; ++w) t += ws[w];
-    blkcnt[(int64_t)m * nblk + blockIdx.x] = (unsigned long long)t;
+  const int64_t e0 = (int64_t)blockIdx.x * kEnumBlock + (int64_t)threadIdx.x * kEnumItems;
+  unsigned long long k4[kEnumItems];
+  double m4[kEnumItems];
+#pragma unroll
+  for (int k = 0; k < kEnumItems; ++k) {
+    k4[k] = 0ull;
+    m4[k] = -1.0;  // past the end: in no window (weights are > 0)
+    if (e0 + k < U) unrank_key(s_binom, P, (unsigned long long)(e0 + k), k4[k], m4[k]);
   }
+  if (e0 + kEnumItems <= U) {  // 32-byte aligned: vector stores
+    reinterpret_cast<ulonglong2*>(ukey + e0)[0] = make_ulonglong2(k4[0], k4[1]);
+    reinterpret_cast<ulonglong2*>(ukey + e0)[1] = make_ulonglong2(k4[2], k4[3]);
+    reinterpret_cast<double2*>(umem + e0)[0] = make_double2(m4[0], m4[1]);
+    reinterpret_cast<double2*>(umem + e0)[1] = make_double2(m4[2], m4[3]);
+  } else {
+    for (int k = 0; k < kEnumItems; ++k)
+      if (e0 + k < U) {
+        ukey[e0 + k] = k4[k];
+        umem[e0 + k] = m4[k];
+      }
+  }
+  for (int m = 0; m < P.NM; ++m) {
+    double lo, hi;
+    model_window(P, m, lo, hi);
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < kEnumItems; ++k) c += lo <= m4[k] && m4[k] < hi;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_wcnt[m], (unsigned)c);
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < P.NM; m += blockDim.x) blkcnt[(int64_t)m * nblk + blockIdx.x] = s_wcnt[m];
 }
 
-// pass 2: stable compaction at the scanned block offsets (element order k-major in a
-// block, as pass 1 counted it)
-__global__ void __launch_bounds__(kWinThreads) window_select_kernel(
-    DevProblem P, int64_t U, const unsigned long long* __restrict__ ukey,
-    const double* __restrict__ umem, int nblk, const unsigned long long* __restrict__ blkoff,
-    unsigned long long* __restrict__ keys) {
-  __shared__ int ws[kWinThreads / 32];
-  const int m = blockIdx.y;
-  double lo, hi;
-  model_window(P, m, lo, hi);
-  const int64_t base = (int64_t)blockIdx.x * (kWinThreads * kWinItems);
+// pass 2: ONE read of the block's keys and memory sums, then every model's stable
+// compaction at its scanned block offset (element order = thread-major, as pass 1)
+__global__ void __launch_bounds__(kEnumThreads) window_select_kernel(
+    DevProblem P, int64_t U, const unsigned long long* __restrict__ ukey, const double* __restrict__ umem,
+    int nblk, const unsigned long long* __restrict__ blkoff, unsigned long long* __restrict__ keys) {
+  __shared__ int s_warp[2][kEnumThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long out = blkoff[(int64_t)m * nblk + blockIdx.x];
+  const int64_t e0 = (int64_t)blockIdx.x * kEnumBlock + (int64_t)threadIdx.x * kEnumItems;
+  unsigned long long k4[kEnumItems];
+  double m4[kEnumItems];
+  if (e0 + kEnumItems <= U) {
+    const ulonglong2 a = reinterpret_cast<const ulonglong2*>(ukey + e0)[0];
+    const ulonglong2 b = reinterpret_cast<const ulonglong2*>(ukey + e0)[1];
+    const double2 c = reinterpret_cast<const double2*>(umem + e0)[0];
+    const double2 d = reinterpret_cast<const double2*>(umem + e0)[1];
+    k4[0] = a.x; k4[1] = a.y; k4[2] = b.x; k4[3] = b.y;
+    m4[0] = c.x; m4[1] = c.y; m4[2] = d.x; m4[3] = d.y;
+  } else {
 #pragma unroll
-  for (int k = 0; k < kWinItems; ++k) {
-    const int64_t r = base + k * kWinThreads + threadIdx.x;
-    bool pass = false;
-    if (r < U) {
-      const double v = umem[r];
-      pass = lo <= v && v < hi;
+    for (int k = 0; k < kEnumItems; ++k) {
+      k4[k] = e0 + k < U ? ukey[e0 + k] : 0ull;
+      m4[k] = e0 + k < U ? umem[e0 + k] : -1.0;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, pass);
-    if (lane == 0) ws[warp] = __popc(bal);
-    __syncthreads();
-    int before = 0, total = 0;
+  }
+  for (int m = 0; m < P.NM; ++m) {
+    double lo, hi;
+    model_window(P, m, lo, hi);
+    unsigned pass = 0u;
+    int c = 0;
 #pragma unroll
-    for (int w = 0; w < kWinThreads / 32; ++w) {
-      before += w < warp ? ws[w] : 0;
-      total += ws[w];
+    for (int k = 0; k < kEnumItems; ++k) {
+      const bool in = lo <= m4[k] && m4[k] < hi;
+      pass |= (unsigned)in << k;
+      c += in;
     }
-    if (pass) keys[out + before + __popc(bal & ((1u << lane) - 1u))] = ukey[r];
-    out += total;
+    int incl = c;  // inclusive scan of the per-thread counts over the warp
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int buf = m & 1;  // double-buffered warp totals: one barrier per model
+    if (lane == 31) s_warp[buf][warp] = incl;
     __syncthreads();
+    if (!pass) continue;
+    int before = 0;
+#pragma unroll
+    for (int w = 0; w < kEnumThreads / 32; ++w) before += w < warp ? s_warp[buf][w] : 0;
+    unsigned long long out = blkoff[(int64_t)m * nblk + blockIdx.x] + (unsigned long long)(before + incl - c);
+#pragma unroll
+    for (int k = 0; k < kEnumItems; ++k)
+      if ((pass >> k) & 1u) keys[out++] = k4[k];
   }
 }
 
@@ -991,6 +1028,178 @@ __global__ void feasible_count_kernel(const coral_s1_record* __restrict__ rec, c
   if (f && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(out + mp, (unsigned long long)__popc(peers));
 }
 
+// --------------------------------------------------------------------------------
+// Stage-2 model construction: build_allocation_model
+// (allocation.py:108-195) over the device records. Per (model, phase) slot with demand
+// > 0, every (template, region) with a price is a candidate variable: eff = p / T, the
+// slot's best eff, the prune rule (eff > ratio x best unless already running), the
+// availability cap min over the combo of avail // n, and ub = min(cap, ceil(demand / T));
+// ub <= 0 drops it. Variables come out in the reference's insertion order: slots in
+// library order, templates in library (str) order, regions in market order.
+// --------------------------------------------------------------------------------
+struct AllocArgs {
+  DevProblem P;
+  const unsigned long long* keys;
+  const int64_t* koff;
+  const int64_t* cand_off;
+  const coral_s1_record* rec;
+  const double* prices;           // [R][K], NaN = unpriced (allocation.py:91-98 None)
+  const long long* avail;         // [R][K] MarketState.available
+  const double* demand;           // [NMP]
+  int R;
+  double prune_ratio;
+  // running (region, template) pairs, sorted by (mp, key, region)
+  const int* run_mp;
+  const int* run_region;
+  const unsigned long long* run_key;
+  long long nrunning;
+  // slots in library order with their candidates: thread t -> run k -> mp = runs_mp[k]
+  const int64_t* runs_off;
+  const int* runs_mp;
+  int nruns;
+  int64_t ntot;
+  unsigned long long* best_bits;  // [NMP] min eff (bit pattern; eff >= 0)
+  unsigned* flags;                // [ntot] region bit mask of kept variables
+  unsigned long long* blkcnt;     // per block kept count
+  unsigned long long* npruned;    // meta["pruned_vars"] (allocation.py:146-148)
+  coral_s1_alloc_var* out;
+  const unsigned long long* blkoff;
+};
+
+struct AllocCand {
+  int mp, C;
+  unsigned long long key;
+  double T;
+  int cfg[kMaxC], cnt[kMaxC];
+};
+
+__device__ __forceinline__ bool alloc_cand(const AllocArgs& A, int64_t t, AllocCand& f) {
+  if (t >= A.ntot) return false;
+  int lo = 0, hi = A.nruns;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (A.runs_off[mid] <= t) lo = mid; else hi = mid;
+  }
+  f.mp = A.runs_mp[lo];
+  const int64_t idx = t - A.runs_off[lo];
+  const coral_s1_record& r = A.rec[A.cand_off[f.mp] + idx];
+  if (r.num_stages == 0) return false;  // not a template
+  f.T = r.throughput_tps;
+  f.key = A.keys[A.koff[f.mp / A.P.NP] + idx];
+  f.C = decode_key(A.P, f.key, f.cfg, f.cnt);
+  return true;
+}
+
+__device__ __forceinline__ bool alloc_price(const AllocArgs& A, const AllocCand& f, int r, double& p) {
+  p = 0.0;
+  for (int c = 0; c < f.C; ++c) {
+    const double x = A.prices[(int64_t)r * A.P.K + f.cfg[c]];
+    if (isnan(x)) return false;
+    p = rn_add(p, rn_mul((double)f.cnt[c], x));
+  }
+  return true;
+}
+
+__global__ void alloc_best_kernel(AllocArgs A) {
+  AllocCand f;
+  if (!alloc_cand(A, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, f)) return;
+  for (int r = 0; r < A.R; ++r) {
+    double p;
+    if (!alloc_price(A, f, r, p)) continue;
+    const unsigned long long e = (unsigned long long)__double_as_longlong(rn_div(p, f.T));
+    if (e < A.best_bits[f.mp]) atomicMin(A.best_bits + f.mp, e);
+  }
+}
+
+__device__ __forceinline__ bool alloc_running(const AllocArgs& A, int mp, unsigned long long key, int r) {
+  long long lo = 0, hi = A.nrunning;  // first entry >= (mp, key, r)
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    const bool less = A.run_mp[mid] != mp ? A.run_mp[mid] < mp
+                    : A.run_key[mid] != key ? A.run_key[mid] < key : A.run_region[mid] < r;
+    if (less) lo = mid + 1; else hi = mid;
+  }
+  return lo < A.nrunning && A.run_mp[lo] == mp && A.run_key[lo] == key && A.run_region[lo] == r;
+}
+
+// the variable (f, r) if it is kept: its ub
+// -1: pruned (allocation.py:143-148)
+__device__ __forceinline__ long long alloc_ub(const AllocArgs& A, const AllocCand& f, int r, double p) {
+  const double eff = rn_div(p, f.T);
+  const double best = __longlong_as_double((long long)A.best_bits[f.mp]);
+  if (A.prune_ratio != 0.0 && eff > rn_mul(A.prune_ratio, best) && !alloc_running(A, f.mp, f.key, r)) return -1;
+  long long cap = LLONG_MAX;
+  for (int c = 0; c < f.C; ++c) {
+    const long long a = A.avail[(int64_t)r * A.P.K + f.cfg[c]];
+    const long long q = a >= 0 ? a / f.cnt[c] : -((-a + f.cnt[c] - 1) / f.cnt[c]);  // Python //
+    cap = q < cap ? q : cap;
+  }
+  const double need = ceil(rn_div(A.demand[f.mp], f.T));
+  const long long ub = (double)cap < need ? cap : (long long)need;
+  return ub;
+}
+
+constexpr int kAllocThreads = 256;
+
+__global__ void __launch_bounds__(kAllocThreads) alloc_count_kernel(AllocArgs A) {
+  __shared__ int ws[kAllocThreads / 32];
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  AllocCand f;
+  unsigned mask = 0u;
+  if (alloc_cand(A, t, f))
+    for (int r = 0; r < A.R; ++r) {
+      double p;
+      if (!alloc_price(A, f, r, p)) continue;
+      const long long ub = alloc_ub(A, f, r, p);
+      if (ub > 0) mask |= 1u << r;
+      else if (ub < 0) atomicAdd(A.npruned, 1ull);
+    }
+  if (t < A.ntot) A.flags[t] = mask;
+  int c = __reduce_add_sync(0xffffffffu, __popc(mask));
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < kAllocThreads / 32; ++w) s += ws[w];
+    A.blkcnt[blockIdx.x] = (unsigned long long)s;
+  }
+}
+
+__global__ void __launch_bounds__(kAllocThreads) alloc_emit_kernel(AllocArgs A) {
+  __shared__ int ws[kAllocThreads / 32];
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned mask = t < A.ntot ? A.flags[t] : 0u;
+  const int c = __popc(mask);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) ws[warp] = incl;
+  __syncthreads();
+  if (!mask) return;
+  int before = 0;
+  for (int w = 0; w < warp; ++w) before += ws[w];
+  unsigned long long o = A.blkoff[blockIdx.x] + (unsigned long long)(before + incl - c);
+  AllocCand f;
+  alloc_cand(A, t, f);
+  for (int r = 0; r < A.R; ++r) {
+    if (!((mask >> r) & 1u)) continue;
+    double p;
+    alloc_price(A, f, r, p);
+    coral_s1_alloc_var v;
+    v.combo_key = f.key;
+    v.mp = f.mp;
+    v.region = r;
+    v.ub = alloc_ub(A, f, r, p);
+    v.price_usd_h = p;
+    v.throughput_tps = f.T;
+    A.out[o++] = v;
+  }
+}
+
 // Batched T-hat queries (perf.py:159-230) against the current spec tables: the
 // simulator-side reuse of the roofline model.
 __global__ void node_query_kernel(DevProblem P, int64_t n, const int* __restrict__ cfg,
@@ -1068,10 +1277,183 @@ __global__ void skyline_flags_kernel(const unsigned long long* __restrict__ seg,
   flag[i] = (i == 0 || seg[i] != seg[i - 1] || tv[i] > incl[i - 1]) ? 1 : 0;
 }
 
+// ---- Frontier skyline, hand-written: one CTA per segment -----------------
+// The CTA of segment s collects its items from every part (one part on one GPU; the
+// gathered per-rank partial frontiers in the multi-GPU merge) into shared memory, sorts
+// them (bitonic) by (price asc, T desc, combo key asc, stages asc), keeps an item iff its
+// T exceeds the running max of the items before it (block max-scan), and stages the
+// survivors' ordinals; front_emit_kernel writes them compacted, segment by segment.
+// Segments larger than kSegCap items take the general path (frontier_from_items_general).
+constexpr int kSegThreads = 1024, kSegCap = 4096, kMaxParts = 32;
+
+struct SegKey {
+  unsigned long long price;  // bit pattern of price >= 0 (orders like the value)
+  unsigned long long neg_t;  // ~bits(T), T > 0: ascending = T descending
+  unsigned long long key;    // packed combo key
+  unsigned long long s_ord;  // num_stages << 32 | item ordinal (fewer stages first)
+};
+
+__device__ __forceinline__ bool seg_less(const SegKey& a, const SegKey& b) {
+  if (a.price != b.price) return a.price < b.price;
+  if (a.neg_t != b.neg_t) return a.neg_t < b.neg_t;
+  if (a.key != b.key) return a.key < b.key;
+  return a.s_ord < b.s_ord;
+}
+
+struct FrontParts {
+  const unsigned char* base;  // part p's items at base + p * stride + offset
+  long long stride, offset;
+  int nparts, R;
+  long long n[kMaxParts];     // items per part
+  long long first[kMaxParts + 1];  // ordinal of each part's first item
+  __device__ __forceinline__ const coral_s1_frontier_item& item(int p, long long i) const {
+    return reinterpret_cast<const coral_s1_frontier_item*>(base + p * stride + offset)[i];
+  }
+  __device__ __forceinline__ const coral_s1_frontier_item& by_ord(long long o) const {
+    int p = 0;
+    while (p + 1 < nparts && first[p + 1] <= o) ++p;
+    return item(p, o - first[p]);
+  }
+};
+
+// block-wide exclusive scan (sum or max) of one value per thread; 1024 threads
+template <bool kMax>
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* s_warp,
+                                                             unsigned long long* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = kMax ? (t > incl ? t : incl) : incl + t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = s_warp[lane], wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi = kMax ? (t > wi ? t : wi) : wi + t;
+    }
+    s_warp[lane] = wi;  // inclusive over warps
+  }
+  __syncthreads();
+  const unsigned long long before = warp ? s_warp[warp - 1] : 0ull;
+  unsigned long long ex;
+  if (kMax) {  // exclusive max: the previous lane's inclusive value, then the earlier warps
+    const unsigned long long up = __shfl_up_sync(0xffffffffu, incl, 1);
+    const unsigned long long lanepre = lane ? up : 0ull;
+    ex = lanepre > before ? lanepre : before;
+  } else {
+    ex = before + incl - v;
+  }
+  if (total) *total = s_warp[31];
+  __syncthreads();
+  return ex;
+}
+
+__global__ void __launch_bounds__(kSegThreads) front_segment_kernel(FrontParts F, int nseg,
+                                                                    unsigned* __restrict__ staged,
+                                                                    unsigned* __restrict__ surv,
+                                                                    unsigned* __restrict__ overflow) {
+  extern __shared__ SegKey s_keys[];  // [kSegCap]
+  __shared__ unsigned s_cnt;
+  __shared__ unsigned long long s_warp[32];
+  const int seg = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_cnt = 0u;
+  __syncthreads();
+  for (int p = 0; p < F.nparts; ++p) {
+    for (long long i = tid; i < F.n[p]; i += kSegThreads) {
+      const coral_s1_frontier_item& it = F.item(p, i);
+      const int2 mr = *reinterpret_cast<const int2*>(&it.mp);  // (mp, region)
+      if (mr.x * F.R + mr.y != seg) continue;
+      const unsigned pos = atomicAdd(&s_cnt, 1u);
+      if (pos < kSegCap) {
+        SegKey k;
+        k.price = (unsigned long long)__double_as_longlong(it.price_usd_h);
+        k.neg_t = ~(unsigned long long)__double_as_longlong(it.throughput_tps);
+        k.key = it.combo_key;
+        k.s_ord = ((unsigned long long)it.rec.num_stages << 32) | (unsigned long long)(F.first[p] + i);
+        s_keys[pos] = k;
+      }
+    }
+  }
+  __syncthreads();
+  const int cnt = (int)s_cnt;
+  if (cnt > kSegCap) {
+    if (tid == 0) { atomicOr(overflow, 1u); surv[seg] = 0u; }
+    return;
+  }
+  int np2 = 1;
+  while (np2 < cnt) np2 <<= 1;
+  for (int i = cnt + tid; i < np2; i += kSegThreads) {
+    SegKey k;
+    k.price = k.neg_t = k.key = k.s_ord = ~0ull;  // sentinel: sorts last
+    s_keys[i] = k;
+  }
+  __syncthreads();
+  // bitonic sort of np2 keys
+  for (int size = 2; size <= np2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = tid; t < (np2 >> 1); t += kSegThreads) {
+        const int i = 2 * t - (t & (stride - 1));  // lower index of the pair
+        const int j = i + stride;
+        const bool up = (i & size) == 0;
+        SegKey a = s_keys[i], b = s_keys[j];
+        if (seg_less(b, a) == up) { s_keys[i] = b; s_keys[j] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  // skyline: thread t owns sorted positions [t*per, t*per + per)
+  const int per = (cnt + kSegThreads - 1) / kSegThreads;
+  const int b0 = min(tid * per, cnt), b1 = min(b0 + per, cnt);
+  unsigned long long lmax = 0ull;  // T bits; every T > 0
+  for (int i = b0; i < b1; ++i) {
+    const unsigned long long tb = ~s_keys[i].neg_t;
+    lmax = tb > lmax ? tb : lmax;
+  }
+  unsigned long long run = block_excl_scan<true>(lmax, s_warp, nullptr);
+  unsigned keep = 0u;  // bit k: position b0 + k survives (per <= 4)
+  for (int i = b0; i < b1; ++i) {
+    const unsigned long long tb = ~s_keys[i].neg_t;
+    if (tb > run) { keep |= 1u << (i - b0); run = tb; }
+  }
+  unsigned long long total = 0ull;
+  const unsigned long long at = block_excl_scan<false>((unsigned long long)__popc(keep), s_warp, &total);
+  unsigned o = (unsigned)at;
+  for (int i = b0; i < b1; ++i)
+    if ((keep >> (i - b0)) & 1u) staged[(long long)seg * kSegCap + o++] = (unsigned)(s_keys[i].s_ord & 0xFFFFFFFFull);
+  if (tid == 0) surv[seg] = (unsigned)total;
+}
+
+// survivors of segment s -> out at the sum of the earlier segments' survivor counts
+__global__ void __launch_bounds__(256) front_emit_kernel(FrontParts F, int nseg, const unsigned* __restrict__ staged,
+                                                         const unsigned* __restrict__ surv,
+                                                         coral_s1_frontier_item* __restrict__ out,
+                                                         long long* __restrict__ ntotal) {
+  __shared__ unsigned long long s_part[8];
+  const int seg = blockIdx.x;
+  unsigned long long pre = 0ull;
+  for (int s = threadIdx.x; s < seg; s += blockDim.x) pre += surv[s];
+  pre = __reduce_add_sync(0xffffffffu, (unsigned)pre);  // < 2^32 survivors
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = pre;
+  __syncthreads();
+  unsigned long long base = 0ull;
+  for (int w = 0; w < 8; ++w) base += s_part[w];
+  const unsigned ns = surv[seg];
+  for (unsigned k = threadIdx.x; k < ns; k += blockDim.x)
+    out[base + k] = F.by_ord(staged[(long long)seg * kSegCap + k]);
+  if (seg == nseg - 1 && threadIdx.x == 0) *ntotal = (long long)(base + ns);
+}
+
 int ensure_tmp(coral_s1_handle* h, size_t bytes) { return h->cub_tmp.ensure(bytes); }
 
-// Frontier over n items already in h->items; survivors -> h->front, count -> h->nfront.
-int frontier_from_items(coral_s1_handle* h, int64_t n, int R) {
+// General frontier over n items already in h->items (any segment size: stable merge sort
+// + segmented max scan + compaction); survivors -> h->front, count -> h->nfront.
+int frontier_from_items_general(coral_s1_handle* h, int64_t n, int R) {
   cudaStream_t st = h->stream;
   h->nfront = 0;
   if (n == 0) return 0;
@@ -1125,6 +1507,57 @@ int frontier_from_items(coral_s1_handle* h, int64_t n, int R) {
   CUDA_TRY(cudaStreamSynchronize(st));
   h->nfront = ns;
   return 0;
+}
+
+// Frontier over the items of `F` (nseg = mp x region segments): the per-segment CTA path;
+// if some segment holds more than kSegCap items, the items are made contiguous in
+// h->items (when they are not already) and the general path runs instead.
+int frontier_segments(coral_s1_handle* h, const FrontParts& F, int64_t ntot, bool items_are_contiguous) {
+  cudaStream_t st = h->stream;
+  h->nfront = 0;
+  if (ntot == 0) return 0;
+  const int nseg = h->NM * h->NP * F.R;
+  int rc;
+  const size_t o_surv = (size_t)nseg * kSegCap * 4, o_flag = o_surv + (size_t)nseg * 4 + 16;
+  if ((rc = h->segbuf.ensure(o_flag + 16)) || (rc = h->front.ensure(ntot * sizeof(coral_s1_frontier_item))))
+    return rc;
+  unsigned char* sb = h->segbuf.as<unsigned char>();
+  CUDA_TRY(cudaMemsetAsync(sb + o_flag, 0, 16, st));
+  front_segment_kernel<<<(unsigned)nseg, kSegThreads, kSegCap * sizeof(SegKey), st>>>(
+      F, nseg, (unsigned*)sb, (unsigned*)(sb + o_surv), (unsigned*)(sb + o_flag));
+  LAUNCH_CHECK(h);
+  front_emit_kernel<<<(unsigned)nseg, 256, 0, st>>>(F, nseg, (const unsigned*)sb, (const unsigned*)(sb + o_surv),
+                                                    h->front.as<coral_s1_frontier_item>(), (long long*)(sb + o_flag + 8));
+  LAUNCH_CHECK(h);
+  long long res[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(res, sb + o_flag, 16, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if ((res[0] & 0xFFFFFFFFll) == 0) {
+    h->nfront = res[1];
+    return 0;
+  }
+  // a segment beyond kSegCap items: the general path over contiguous items
+  if (!items_are_contiguous) {
+    if ((rc = h->items.ensure(ntot * sizeof(coral_s1_frontier_item)))) return rc;
+    for (int p = 0; p < F.nparts; ++p)
+      if (F.n[p])
+        CUDA_TRY(cudaMemcpyAsync(h->items.as<coral_s1_frontier_item>() + F.first[p], F.base + p * F.stride + F.offset,
+                                 F.n[p] * sizeof(coral_s1_frontier_item), cudaMemcpyDeviceToDevice, st));
+  }
+  return frontier_from_items_general(h, ntot, F.R);
+}
+
+FrontParts one_part(const void* items, int64_t n, int R) {
+  FrontParts F{};
+  F.base = static_cast<const unsigned char*>(items);
+  F.stride = 0;
+  F.offset = 0;
+  F.nparts = 1;
+  F.R = R;
+  F.n[0] = n;
+  F.first[0] = 0;
+  F.first[1] = n;
+  return F;
 }
 
 template <class T>
@@ -1200,6 +1633,7 @@ int coral_s1_create(int device, coral_s1_handle** out) {
   const size_t smem_max = dp_smem_bytes(kMaxM, CORAL_S1_MAX_LAYER_UNITS + 1, CORAL_S1_MAX_LAYER_UNITS);
   cudaFuncSetAttribute(evaluate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
   cudaFuncSetAttribute(placement_op_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+  cudaFuncSetAttribute(front_segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSegCap * sizeof(SegKey)));
   e = cudaGetLastError();
   if (e != cudaSuccess) { delete h; return fail(CORAL_S1_ECUDA, cudaGetErrorString(e)); }
   *out = h;
@@ -1209,10 +1643,10 @@ int coral_s1_create(int device, coral_s1_handle** out) {
 int coral_s1_destroy(coral_s1_handle* h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
-  DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys_raw, &h->keys, &h->koff_d,
+  DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys, &h->koff_d,
                     &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
-                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->enum_tmp, &h->ukey_s, &h->umem, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->fbucket,
+                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->ukey_s, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->fbucket, &h->segbuf, &h->avars,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
                     &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff, &h->run_off_d, &h->run_mp_d};
   for (DevBuf* b : bufs) b->release();
@@ -1431,30 +1865,19 @@ int coral_s1_enumerate(coral_s1_handle* h) {
   h->counts.assign(NM, 0);
   h->koff.assign(NM + 1, 0);
   if (NM > 0 && U > 0) {
-    const int nblk = (int)((U + kWinThreads * kWinItems - 1) / (kWinThreads * kWinItems));
+    const int nblk = (int)((U + kEnumBlock - 1) / kEnumBlock);
     const int64_t nb = (int64_t)NM * nblk;
-    if ((rc = h->keys_raw.ensure(U * 8)) || (rc = h->ukey_s.ensure(U * 8)) || (rc = h->umem.ensure(U * 8)) ||
-        (rc = h->umem_s.ensure(U * 8)) || (rc = h->blkcnt.ensure((nb + 1) * 8)) ||
-        (rc = h->blkoff.ensure((nb + 1) * 8)))
+    if ((rc = h->ukey_s.ensure(U * 8)) || (rc = h->umem_s.ensure(U * 8)) ||
+        (rc = h->blkcnt.ensure((nb + 1) * 8)) || (rc = h->blkoff.ensure((nb + 1) * 8)))
       return rc;
-    // the universe once: keys + memory sums, sorted by key (54 bits, unique keys)
-    universe_kernel<<<(unsigned)((U + 255) / 256), 256, 0, st>>>(h->dp, U, h->keys_raw.as<unsigned long long>(),
-                                                                 h->umem.as<double>());
-    LAUNCH_CHECK(h);
-    size_t tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, h->keys_raw.as<unsigned long long>(),
-                                    h->ukey_s.as<unsigned long long>(), h->umem.as<double>(),
-                                    h->umem_s.as<double>(), (int)U, 0, kKeyTokenBits * kMaxC, st);
-    if ((rc = ensure_tmp(h, tmp))) return rc;
-    CUDA_TRY(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, h->keys_raw.as<unsigned long long>(),
-                                             h->ukey_s.as<unsigned long long>(), h->umem.as<double>(),
-                                             h->umem_s.as<double>(), (int)U, 0, kKeyTokenBits * kMaxC, st));
-    // per-model window counts per block, one scan -> block offsets and model totals
-    window_count_kernel<<<dim3((unsigned)nblk, NM), kWinThreads, 0, st>>>(
-        h->dp, U, h->umem_s.as<double>(), nblk, h->blkcnt.as<unsigned long long>());
+    // the universe once, unranked in key order: keys + memory sums + per-model window
+    // counts per block; one scan -> block offsets and model totals
+    enum_count_kernel<<<(unsigned)nblk, kEnumThreads, (size_t)NM * sizeof(unsigned), st>>>(
+        h->dp, U, nblk, h->ukey_s.as<unsigned long long>(), h->umem_s.as<double>(),
+        h->blkcnt.as<unsigned long long>());
     LAUNCH_CHECK(h);
     CUDA_TRY(cudaMemsetAsync(h->blkcnt.as<unsigned long long>() + nb, 0, 8, st));
-    tmp = 0;
+    size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, h->blkcnt.as<unsigned long long>(),
                                   h->blkoff.as<unsigned long long>(), (int)(nb + 1), st);
     if ((rc = ensure_tmp(h, tmp))) return rc;
@@ -1463,7 +1886,7 @@ int coral_s1_enumerate(coral_s1_handle* h) {
     window_totals_kernel<<<(NM + 127) / 128, 128, 0, st>>>(NM, nblk, h->blkoff.as<unsigned long long>(),
                                                            h->nvalid.as<unsigned long long>());
     LAUNCH_CHECK(h);
-    h->launches += 6;
+    h->launches += 2;
     std::vector<unsigned long long> nv(NM);
     CUDA_TRY(cudaMemcpyAsync(nv.data(), h->nvalid.p, NM * 8, cudaMemcpyDeviceToHost, st));
     // the evaluator's T-hat monotonicity flags ride on this round trip
@@ -1483,15 +1906,14 @@ int coral_s1_enumerate(coral_s1_handle* h) {
     h->ws_timed = false;
     if (nk > 0) {  // model-major, str(combo) order within a model: the library order
       CUDA_TRY(cudaEventRecord(h->ev_ws[0], st));
-      window_select_kernel<<<dim3((unsigned)nblk, NM), kWinThreads, 0, st>>>(
+      window_select_kernel<<<(unsigned)nblk, kEnumThreads, 0, st>>>(
           h->dp, U, h->ukey_s.as<unsigned long long>(), h->umem_s.as<double>(), nblk,
           h->blkoff.as<unsigned long long>(), h->keys.as<unsigned long long>());
-      h->launches += 1;
       LAUNCH_CHECK(h);
       CUDA_TRY(cudaEventRecord(h->ev_ws[1], st));
-      // its algorithmic bytes: each model reads every memory sum (8 B), each survivor's
-      // key (8 B) and writes it (8 B)
-      h->ws_bytes = (int64_t)NM * U * 8 + nk * 16;
+      // its algorithmic bytes: one read of every universe key and memory sum (16 B) and
+      // one write of each model's survivor keys (8 B)
+      h->ws_bytes = U * 16 + nk * 8;
       h->ws_timed = true;
     }
     // lattice state tables for every model with candidates, on side stream 0; enqueued
@@ -2055,7 +2477,7 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
     n = (int64_t)ni;
   }
   if (skyline) {
-    if ((rc = frontier_from_items(h, n, num_regions))) return rc;
+    if ((rc = frontier_segments(h, one_part(h->items.p, n, num_regions), n, true))) return rc;
   } else {  // prefiltered candidates only (their skyline is taken after the multi-GPU merge)
     if ((rc = h->front.ensure(std::max<int64_t>(n, 1) * sizeof(coral_s1_frontier_item)))) return rc;
     if (n)
@@ -2100,13 +2522,10 @@ int coral_s1_frontier_export_device(coral_s1_handle* h, void* dev_items, int64_t
 int coral_s1_frontier_merge_device(coral_s1_handle* h, const void* dev_items, int64_t n,
                                    int64_t* num_survivors) {
   if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  if (n < 0 || (n && !dev_items)) return fail(CORAL_S1_EINVAL, "bad items");
   CUDA_TRY(cudaSetDevice(h->device));
   int rc;
-  if ((rc = h->items.ensure(std::max<int64_t>(n, 1) * sizeof(coral_s1_frontier_item)))) return rc;
-  if (n)
-    CUDA_TRY(cudaMemcpyAsync(h->items.p, dev_items, n * sizeof(coral_s1_frontier_item),
-                             cudaMemcpyDeviceToDevice, h->stream));
-  if ((rc = frontier_from_items(h, n, h->num_regions))) return rc;
+  if ((rc = frontier_segments(h, one_part(dev_items, n, h->num_regions), n, dev_items == h->items.p))) return rc;
   if (num_survivors) *num_survivors = h->nfront;
   return 0;
 }
@@ -2122,16 +2541,28 @@ int coral_s1_frontier_merge_parts(coral_s1_handle* h, const void* dev_base, int 
     n += counts[p];
   }
   int rc;
-  if ((rc = h->items.ensure(std::max<int64_t>(n, 1) * sizeof(coral_s1_frontier_item)))) return rc;
-  int64_t at = 0;
-  for (int p = 0; p < parts; ++p) {
-    if (!counts[p]) continue;
-    const char* src = static_cast<const char*>(dev_base) + p * stride_bytes + item_offset_bytes;
-    CUDA_TRY(cudaMemcpyAsync(h->items.as<coral_s1_frontier_item>() + at, src,
-                             counts[p] * sizeof(coral_s1_frontier_item), cudaMemcpyDeviceToDevice, h->stream));
-    at += counts[p];
+  if (parts <= kMaxParts) {  // the gathered buffer is read in place
+    FrontParts F{};
+    F.base = static_cast<const unsigned char*>(dev_base);
+    F.stride = stride_bytes;
+    F.offset = item_offset_bytes;
+    F.nparts = parts;
+    F.R = h->num_regions;
+    F.first[0] = 0;
+    for (int p = 0; p < parts; ++p) { F.n[p] = counts[p]; F.first[p + 1] = F.first[p] + counts[p]; }
+    if ((rc = frontier_segments(h, F, n, false))) return rc;
+  } else {
+    if ((rc = h->items.ensure(std::max<int64_t>(n, 1) * sizeof(coral_s1_frontier_item)))) return rc;
+    int64_t at = 0;
+    for (int p = 0; p < parts; ++p) {
+      if (!counts[p]) continue;
+      const char* src = static_cast<const char*>(dev_base) + p * stride_bytes + item_offset_bytes;
+      CUDA_TRY(cudaMemcpyAsync(h->items.as<coral_s1_frontier_item>() + at, src,
+                               counts[p] * sizeof(coral_s1_frontier_item), cudaMemcpyDeviceToDevice, h->stream));
+      at += counts[p];
+    }
+    if ((rc = frontier_segments(h, one_part(h->items.p, n, h->num_regions), n, true))) return rc;
   }
-  if ((rc = frontier_from_items(h, n, h->num_regions))) return rc;
   if (num_survivors) *num_survivors = h->nfront;
   return 0;
 }
@@ -2290,6 +2721,134 @@ int coral_s1_feasible_counts(coral_s1_handle* h, int64_t* counts, int64_t n) {
   }
   // templates.py:499-502: a (model, phase) with no feasible template at all
   if (!missing.empty()) return fail(CORAL_S1_ENOTEMPLATE, "no feasible template for (model, phase) slots " + missing);
+  return 0;
+}
+
+int coral_s1_allocation_model(coral_s1_handle* h, int num_regions, const double* prices, const int64_t* avail,
+                              const double* demand, int n_mp, const int32_t* mp_order, double prune_ratio,
+                              int64_t n_running, const int32_t* run_mp, const int32_t* run_region,
+                              const uint64_t* run_key, int64_t* num_vars, int64_t* num_pruned,
+                              double* best_eff) {
+  if (!h || !h->have_eval) return fail(CORAL_S1_EINVAL, "evaluate first");
+  if (num_regions < 0 || num_regions > 32) return fail(CORAL_S1_EUNSUPPORTED, "allocation model: 0..32 regions");
+  if (n_mp < 0 || n_running < 0 || (n_running && (!run_mp || !run_region || !run_key)))
+    return fail(CORAL_S1_EINVAL, "bad allocation inputs");
+  const int NMP = h->NM * h->NP;
+  CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const int K = h->K;
+  for (int64_t i = 0; i < (int64_t)num_regions * K; ++i)
+    if (avail[i] < 0) return fail(CORAL_S1_EINVAL, "negative availability");
+  // slots with demand > 0, library order (allocation.py:128-130)
+  std::vector<int64_t> roff(1, 0);
+  std::vector<int> rmp;
+  for (int i = 0; i < n_mp; ++i) {
+    const int mp = mp_order[i];
+    if (mp < 0 || mp >= NMP) return fail(CORAL_S1_EINVAL, "bad mp in order");
+    if (!(demand[mp] > 0.0)) continue;
+    rmp.push_back(mp);
+    roff.push_back(roff.back() + (h->cand_off[mp + 1] - h->cand_off[mp]));
+  }
+  if (rmp.empty()) rmp.push_back(0);
+  const int64_t ntot = roff.back();
+  // running pairs sorted by (mp, key, region) for the device lookup
+  std::vector<int64_t> ord((size_t)n_running);
+  for (int64_t i = 0; i < n_running; ++i) ord[i] = i;
+  std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+    if (run_mp[a] != run_mp[b]) return run_mp[a] < run_mp[b];
+    if (run_key[a] != run_key[b]) return run_key[a] < run_key[b];
+    return run_region[a] < run_region[b];
+  });
+  std::vector<int> rm(std::max<int64_t>(n_running, 1)), rr(std::max<int64_t>(n_running, 1));
+  std::vector<unsigned long long> rk(std::max<int64_t>(n_running, 1));
+  for (int64_t i = 0; i < n_running; ++i) { rm[i] = run_mp[ord[i]]; rr[i] = run_region[ord[i]]; rk[i] = run_key[ord[i]]; }
+  std::vector<double> pv(prices, prices + (size_t)num_regions * K), dv(demand, demand + NMP);
+  std::vector<long long> av(avail, avail + (size_t)num_regions * K);
+  const int64_t nblk = (std::max<int64_t>(ntot, 1) + kAllocThreads - 1) / kAllocThreads;
+  DevBuf d_av, d_dem, d_rm, d_rr, d_rk, d_roff, d_rmp, d_best, d_flags, d_cnt, d_off, d_np;
+  int rc;
+  if ((rc = upload(h, h->prices, pv)) || (rc = upload(h, d_av, av)) || (rc = upload(h, d_dem, dv)) ||
+      (rc = upload(h, d_rm, rm)) || (rc = upload(h, d_rr, rr)) || (rc = upload(h, d_rk, rk)) ||
+      (rc = upload(h, d_roff, roff)) || (rc = upload(h, d_rmp, rmp)) ||
+      (rc = d_best.ensure((size_t)std::max(NMP, 1) * 8)) || (rc = d_flags.ensure((size_t)std::max<int64_t>(ntot, 1) * 4)) ||
+      (rc = d_cnt.ensure((size_t)(nblk + 1) * 8)) || (rc = d_off.ensure((size_t)(nblk + 1) * 8)) || (rc = d_np.ensure(8)))
+    return rc;
+  CUDA_TRY(cudaMemsetAsync(d_best.p, 0xFF, (size_t)std::max(NMP, 1) * 8, st));
+  CUDA_TRY(cudaMemsetAsync(d_np.p, 0, 8, st));
+  CUDA_TRY(cudaMemsetAsync(d_cnt.as<unsigned long long>() + nblk, 0, 8, st));
+  AllocArgs A;
+  A.P = h->dp;
+  A.keys = h->keys.as<unsigned long long>();
+  A.koff = h->koff_d.as<int64_t>();
+  A.cand_off = h->cand_off_d.as<int64_t>();
+  A.rec = h->rec.as<coral_s1_record>();
+  A.prices = h->prices.as<double>();
+  A.avail = d_av.as<long long>();
+  A.demand = d_dem.as<double>();
+  A.R = num_regions;
+  A.prune_ratio = prune_ratio;
+  A.run_mp = d_rm.as<int>();
+  A.run_region = d_rr.as<int>();
+  A.run_key = d_rk.as<unsigned long long>();
+  A.nrunning = n_running;
+  A.runs_off = d_roff.as<int64_t>();
+  A.runs_mp = d_rmp.as<int>();
+  A.nruns = (int)roff.size() - 1;
+  A.ntot = ntot;
+  A.best_bits = d_best.as<unsigned long long>();
+  A.flags = d_flags.as<unsigned>();
+  A.blkcnt = d_cnt.as<unsigned long long>();
+  A.npruned = d_np.as<unsigned long long>();
+  A.out = nullptr;
+  A.blkoff = d_off.as<unsigned long long>();
+  if (ntot > 0) {
+    alloc_best_kernel<<<(unsigned)nblk, kAllocThreads, 0, st>>>(A);
+    LAUNCH_CHECK(h);
+    alloc_count_kernel<<<(unsigned)nblk, kAllocThreads, 0, st>>>(A);
+    LAUNCH_CHECK(h);
+  } else {
+    CUDA_TRY(cudaMemsetAsync(d_cnt.p, 0, (size_t)(nblk + 1) * 8, st));
+  }
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, d_cnt.as<unsigned long long>(), d_off.as<unsigned long long>(),
+                                (int)(nblk + 1), st);
+  if ((rc = ensure_tmp(h, tmp))) return rc;
+  CUDA_TRY(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, d_cnt.as<unsigned long long>(),
+                                         d_off.as<unsigned long long>(), (int)(nblk + 1), st));
+  unsigned long long res[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(&res[0], d_off.as<unsigned long long>() + nblk, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&res[1], d_np.p, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t nv = (int64_t)res[0];
+  if ((rc = h->avars.ensure((size_t)std::max<int64_t>(nv, 1) * sizeof(coral_s1_alloc_var)))) return rc;
+  A.out = h->avars.as<coral_s1_alloc_var>();
+  if (nv > 0) {
+    alloc_emit_kernel<<<(unsigned)nblk, kAllocThreads, 0, st>>>(A);
+    LAUNCH_CHECK(h);
+  }
+  if (best_eff) {  // per slot min eff; +inf when the slot had no priced template
+    std::vector<unsigned long long> bb((size_t)std::max(NMP, 1));
+    CUDA_TRY(cudaMemcpyAsync(bb.data(), d_best.p, bb.size() * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int mp = 0; mp < NMP; ++mp) {
+      double v = HUGE_VAL;
+      if (bb[mp] != ~0ull) memcpy(&v, &bb[mp], 8);
+      best_eff[mp] = v;
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  h->navars = nv;
+  if (num_vars) *num_vars = nv;
+  if (num_pruned) *num_pruned = (int64_t)res[1];
+  return 0;
+}
+
+int coral_s1_get_allocation_vars(coral_s1_handle* h, coral_s1_alloc_var* out, int64_t n) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  if (n < h->navars) return fail(CORAL_S1_EINVAL, "output too small");
+  if (h->navars)
+    CUDA_TRY(cudaMemcpyAsync(out, h->avars.p, h->navars * sizeof(coral_s1_alloc_var), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }
 

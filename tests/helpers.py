@@ -103,3 +103,42 @@ def price_matrix(configs, prices, regions):
             if p is not None:
                 mat[i, k] = p
     return mat
+
+
+def alloc_inputs(config_names, region_names, library):
+    """Deterministic stage-2 inputs for the allocation-model parity tests
+    (tests/golden/make_alloc_golden.py): prices of the core workload with two configs
+    unpriced in the last region, seeded availability per (region, config), a demand per
+    (model, phase) with one zero, three running templates and an init penalty."""
+    w = catalog.WORKLOADS["core"]()
+    cfgs = sorted(config_names)
+    regs = sorted(region_names)
+    prices = {k: v for k, v in w.prices.items() if k[0] in regs}
+    for c in cfgs[:2]:
+        prices.pop((regs[-1], c), None)
+    rng = np.random.default_rng(7)
+    avail = {(r, c): int(rng.integers(0, 40)) for r in regs for c in cfgs}
+    mps = library.model_phases()
+    demand = {(m, ph): (20000.0 if ph == "prefill" else 6000.0) for m, ph in mps}
+    demand[mps[-1]] = 0.0
+    running = []
+    for m, ph in mps[:3]:
+        ts = library.templates_for(m, ph)
+        running.append((regs[0], ts[-1].template_id))
+    return prices, avail, demand, running, 0.25
+
+
+def milp_digest(milp) -> dict:
+    """Canonical text digests of a MilpModel (milp/model.py:55-120): variables in
+    insertion order, objective, constraints with their coefficient dicts in order."""
+    def sha(lines):
+        return digest(lines)
+    return {
+        "n_vars": len(milp.variables), "n_cons": len(milp.constraints), "sense": milp.sense,
+        "vars_sha": sha(f"{v.vid}|{v.kind}|{v.ub!r}" for v in milp.variables.values()),
+        "obj_sha": sha(f"{k}|{c!r}" for k, c in milp.objective.items()),
+        "cons_sha": sha(f"{c.name}|{c.sense}|{c.rhs!r}|" + ";".join(f"{v}:{x!r}" for v, x in c.coeffs.items())
+                        for c in milp.constraints),
+        "first_vars": [f"{v.vid}|{v.kind}|{v.ub!r}" for v in list(milp.variables.values())[:40]],
+        "first_cons": [f"{c.name}|{c.sense}|{c.rhs!r}|{len(c.coeffs)}" for c in milp.constraints[:40]],
+    }
