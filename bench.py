@@ -150,6 +150,34 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+BASELINE_CONFIG = {"c1": "BASELINE config 1: Llama-3-8B x {A100, L4} x {1,2,4,8}, small pool",
+                   "extended": "BASELINE config 2: 6 models x 20 node configs x 3 regions",
+                   "c2": "BASELINE config 2: 6 models x 20 node configs x 3 regions",
+                   "c3": "BASELINE config 3: llama3-70b, 20 configs, granularity 1 (Lu = 80)",
+                   "c5": "BASELINE config 5: 50 synthetic models x 40 node configs x 3 regions",
+                   "core": "reference core scenario: 3 models x 12 configs x 2 regions"}
+
+
+def workload_label(name: str) -> str:
+    from paper_2605_04357_b200 import catalog
+    w = catalog.WORKLOADS[name]()
+    return f"{w.name} ({BASELINE_CONFIG.get(name, name)})"
+
+
+def onchip_calibration():
+    """Per-pair instruction / L1-wavefront costs of the two lattice search kernels from
+    the committed ncu capture (tools/onchip_calib.py -> profiles/r02_onchip_calib.json),
+    and the measured on-chip peaks (tools/onchip_peaks.cu -> profiles/r01_onchip_peaks.json)."""
+    out = {}
+    for name in ("r02_onchip_calib.json", "r01_onchip_peaks.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                out[name] = json.load(fh)
+        except (OSError, ValueError):
+            out[name] = {}
+    return out["r02_onchip_calib.json"], out["r01_onchip_peaks.json"]
+
+
 def lattice_states(K: int, n_max: int) -> int:
     """Multisets of 1..n_max-1 of K configs: the lattice table rows (csrc/lattice.cuh)."""
     from math import comb
@@ -254,7 +282,7 @@ def run_reference(args, world, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic spec tables (reference catalog)",
-        "config": {"workload": catalog.WORKLOADS[args.workload]().name + " (BASELINE config 2)",
+        "config": {"workload": workload_label(args.workload),
                    "sample": f"every {CPU_SAMPLE_STRIDE}th candidate per (model, phase)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{n_all // args.steps} candidates/step (stride {CPU_SAMPLE_STRIDE}), "
@@ -309,8 +337,7 @@ def main():
         step()
     torch.cuda.synchronize()
     ncand = h.num_candidates()
-    top_ms, top_n, total_ms = 0.0, 0, 0.0
-    kstat = {1: [0.0, 0], 2: [0.0, 0]}  # lat_layer_kernel, lat_value_kernel: (ms, launches)
+    total_ms = 0.0
     launches0 = h.launches
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -324,13 +351,6 @@ def main():
             ev1.record()
             torch.cuda.synchronize()
             total_ms += ev0.elapsed_time(ev1)
-            t_ms, t_n = h.kernel_stats(0)
-            top_ms += t_ms
-            top_n += t_n
-            for kind in kstat:
-                k_ms, k_n = h.kernel_stats(kind)
-                kstat[kind][0] += k_ms
-                kstat[kind][1] += k_n
     launches = h.launches - launches0
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -347,48 +367,62 @@ def main():
 
     # e2e: the public API, host spec objects in -> frontier ServingTemplates out
     e2e_times = []
-    h2d = d2h = 0
+    front, p2 = build_frontier(w.configs, w.models, w.slos, caps, w.prices, regions=w.regions, ctx=ctx,
+                               return_problem=True)
+    h2d = sum(a.nbytes for a in p2.h._keep) + pmat.nbytes
+    d2h = len(front) * _native.FRONTIER_DTYPE.itemsize + 8 * (len(w.models) + 2)
+    del front, p2  # its handle returns to the pool: every timed call below reuses it warm
     for i in range(args.e2e_steps + 1):
         if world > 1:
             tdist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        front, p2 = build_frontier(w.configs, w.models, w.slos, caps, w.prices, regions=w.regions,
-                                   ctx=ctx, return_problem=True)
+        front = build_frontier(w.configs, w.models, w.slos, caps, w.prices, regions=w.regions, ctx=ctx)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if i > 0:
             e2e_times.append(dt)
-        h2d = sum(a.nbytes for a in p2.h._keep) + pmat.nbytes
-        d2h = len(front) * _native.FRONTIER_DTYPE.itemsize + 8 * (len(w.models) + 2)
+        del front
     et = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device="cuda")
     if world > 1:
         tdist.all_reduce(et, op=tdist.ReduceOp.MAX)
     e2e_s = float(et.item())
 
-    # roofline of the dominant kernel (lat_layer_kernel, 46% of a serialised solve in
-    # profiles/r01_launches_solve.txt; lat_top_kernel 37%), timed live per launch with
-    # CUDA events on its stream. Algorithmic bytes per launch from one census solve
-    # outside the timed region (csrc/lattice.cuh: 10 B per f/choice cell written + one
-    # read of each computed state's value_S and f_{sg-1} rows + its sub-table entries).
+    # roofline of the dominant kernel (lat_layer_kernel) and of lat_top_kernel, from ONE
+    # extra serialised pass (one chain stream: no launch overlaps another, so launches x
+    # mean duration adds up within the pass, as in ncu's serialised launch list) after a
+    # census pass that counts each kernel's algorithmic bytes and (u, l) / (u, S) pairs
+    # (csrc/lattice.cuh: 10 B per f/choice cell written + one read of each computed
+    # state's value_S and f_{sg-1} rows + its sub-table entries)
     peaks, peak_kind = measured_peaks()
+    h.set_streams(1)
     h.set_census(True)
     step()
-    layer_alg = h.census()
+    census = h.census_all()
     h.set_census(False)
-    layer_ms, layer_n = kstat[1]
-    per_step = max(layer_n // max(args.steps, 1), 1)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l2_flush.fill_(1)
+    ev0.record()
+    step()
+    ev1.record()
+    torch.cuda.synchronize()
+    serial_ms = ev0.elapsed_time(ev1)
+    layer_ms, layer_n = h.kernel_stats(1)
+    top_ms, top_n = h.kernel_stats(0)
+    sk = {k: h.kernel_stats(k) for k in (2, 3, 4)}
+    h.set_streams(4)
+    layer_alg, layer_pairs, top_pairs = census[0], census[1], census[2]
     layer_launch_s = (layer_ms / max(layer_n, 1)) / 1e3
-    alg_per_launch = layer_alg / per_step
+    alg_per_launch = layer_alg / max(layer_n, 1)
     achieved = alg_per_launch / layer_launch_s / 1e9 if layer_n else 0.0
     counts = h.num_combos()
     _, lsteps, smax = h.table_layout()
     if masks is None:
         masks = [sum(1 << S for S in range(1, 7))] * (len(w.models) * NP)
     top_alg = top_kernel_bytes(counts, lsteps, smax, masks, len(w.configs), w.n_max)
-    top_per_step = max(top_n // max(args.steps, 1), 1)
     top_launch_s = (top_ms / max(top_n, 1)) / 1e3
-    top_achieved = (top_alg / top_per_step) / top_launch_s / 1e9 if top_n else 0.0
+    top_achieved = (top_alg / max(top_n, 1)) / top_launch_s / 1e9 if top_n else 0.0
     traffic, top_traffic = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -397,7 +431,30 @@ def main():
         top_traffic = tj.get("lat_top_kernel_dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
-    lattice_ms = layer_ms + top_ms + kstat[2][0]
+    # on-chip roofline (the bound that actually applies): instruction issue
+    # for the layer kernel, L1 wavefronts for the top kernel; per-pair costs from the
+    # committed ncu capture x the live pair counts / the live serialised durations
+    calib, onchip = onchip_calibration()
+    clk_mhz = (clk.summary().get("sm_mhz") or onchip.get("sm_clock_mhz_nominal") or 1965.0)
+    sms = onchip.get("sms", 148)
+    roofline_onchip = {"sm_mhz": clk_mhz, "calibration": "profiles/r02_onchip_calib.json",
+                       "peaks": "profiles/r01_onchip_peaks.json"}
+    if calib.get("lat_layer_kernel", {}).get("inst_per_pair") and layer_n:
+        ipp = calib["lat_layer_kernel"]["inst_per_pair"]
+        rate = ipp * layer_pairs / (layer_ms / 1e3)
+        peak = 4.0 * sms * clk_mhz * 1e6
+        roofline_onchip["lat_layer_kernel"] = {
+            "bound": "issue", "unit": "warp-instructions/s", "achieved": rate, "peak": peak,
+            "frac": rate / peak, "inst_per_pair": ipp, "pairs": layer_pairs,
+            "ncu_issue_slots_busy": calib["lat_layer_kernel"].get("issue_slots_busy")}
+    if calib.get("lat_top_kernel", {}).get("wavefronts_per_pair") and top_n:
+        wpp = calib["lat_top_kernel"]["wavefronts_per_pair"]
+        rate = wpp * top_pairs / (top_ms / 1e3)
+        peak = onchip.get("l1_gather_lanes_per_sm_clk", 0.985) * sms * clk_mhz * 1e6
+        roofline_onchip["lat_top_kernel"] = {
+            "bound": "l1_wavefronts", "unit": "wavefronts/s", "achieved": rate, "peak": peak,
+            "frac": rate / peak, "wavefronts_per_pair": wpp, "pairs": top_pairs,
+            "ncu_l1tex_throughput": calib["lat_top_kernel"].get("l1tex_throughput")}
     # (model, phase, combo, S) DP evaluations the reference performs: its per-combo S
     # loop runs S = 1..min(n, Lu) (templates.py:314-316: 8.125 M for c2)
     dp_evals = 0
@@ -410,7 +467,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic spec tables (reference catalog, BASELINE config 2)",
-        "config": {"workload": f"{w.name} (BASELINE config 2: 6 models x 20 node configs x 3 regions)",
+        "config": {"workload": workload_label(args.workload),
                    "candidates": ncand, "dp_evaluations": dp_evals,
                    "dp_evaluations_per_s": dp_evals * args.steps / (total_ms / 1e3),
                    "frontier_survivors": int(nf),
@@ -427,16 +484,21 @@ def main():
                      "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved / peaks.get("hbm_gbs", 6650.0), "traffic": traffic,
                      "peak_kind": peak_kind, "launch_ms": 1e3 * layer_launch_s,
-                     "launches_per_step": per_step,
-                     "share_of_lattice_kernel_time": layer_ms / max(lattice_ms, 1e-9),
+                     "launches_per_step": layer_n, "timing": "serialised pass (1 chain stream)",
+                     "serial_step_ms": serial_ms,
+                     "share_of_serial_step": layer_ms / max(serial_ms, 1e-9),
                      "alg_bytes_per_launch": alg_per_launch,
-                     "note": "fp64 max-min crossing searches over L2-resident lattice tables: issue- and "
-                             "L2-latency-bound, not HBM bandwidth (DESIGN.md 5)"},
+                     "note": "fp64 max-min crossing searches over L2-resident lattice tables: bound by "
+                             "instruction issue (roofline_onchip), not HBM bandwidth; the north_star's "
+                             ">=60% of HBM cannot apply to this DP (SURVEY.md 7 hard part 5, DESIGN.md 5)"},
         "roofline_top": {"kernel": "lat_top_kernel", "achieved": top_achieved, "unit": "GB/s",
                          "frac": top_achieved / peaks.get("hbm_gbs", 6650.0), "traffic": top_traffic,
-                         "launch_ms": 1e3 * top_launch_s, "launches_per_step": top_per_step,
-                         "share_of_lattice_kernel_time": top_ms / max(lattice_ms, 1e-9),
-                         "alg_bytes_per_launch": top_alg / top_per_step},
+                         "launch_ms": 1e3 * top_launch_s, "launches_per_step": top_n,
+                         "share_of_serial_step": top_ms / max(serial_ms, 1e-9),
+                         "alg_bytes_per_launch": top_alg / max(top_n, 1)},
+        "roofline_onchip": roofline_onchip,
+        "serial_kernel_ms": {"lat_layer_kernel": layer_ms, "lat_top_kernel": top_ms, "lat_value_kernel": sk[2][0],
+                             "lat_decode_kernel": sk[3][0], "lat_ranks_kernel": sk[4][0]},
     }
     if world == 1:
         line["other_configs"] = other_configs(args, h)

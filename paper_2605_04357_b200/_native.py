@@ -115,6 +115,8 @@ def load():
             "coral_s1_frontier_candidates": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
             "coral_s1_kernel_timeline": (C.c_int, [vp, C.c_int64, _i32p, _i32p, _f64p, _f64p, _i64p]),
             "coral_s1_census": (C.c_int, [vp, _i64p]),
+            "coral_s1_census_all": (C.c_int, [vp, _i64p, C.c_int]),
+            "coral_s1_set_streams": (C.c_int, [vp, C.c_int]),
             "coral_s1_write_library": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_int, _i32p,
                                                  C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
                                                  C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), _i64p]),
@@ -356,6 +358,15 @@ class Handle:
         v = C.c_int64()
         _check(self._lib.coral_s1_census(self._h, C.byref(v)))
         return v.value
+
+    def census_all(self):
+        """[layer alg bytes, layer (u, l) pairs, top (u, S) pairs, 0] of the last evaluate."""
+        out = np.zeros(4, dtype=np.int64)
+        _check(self._lib.coral_s1_census_all(self._h, _ptr(out, C.c_int64), 4))
+        return out.tolist()
+
+    def set_streams(self, n: int) -> None:
+        _check(self._lib.coral_s1_set_streams(self._h, int(n)))
 
     def kernel_timeline(self, cap: int = 512):
         """[(kind, stream slot, begin ms, end ms)] of the last evaluate's lattice launches."""

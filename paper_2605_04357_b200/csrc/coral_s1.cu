@@ -602,9 +602,41 @@ struct TopArgs {
   coral_s1_record* rec;             // this (model, phase)'s records
   int4* win;                        // per candidate: best value (lo, hi), S, u code << 10 | j
   const unsigned* ranks;            // [candidate][64] from lat_ranks_kernel
+  unsigned long long* census;       // census on: [2] += (u, S) pairs searched
 };
 
-__global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
+// One 32-byte read-only load (LDG.E.ENL2.256 on sm_100a): a row summary of LatWork.
+__device__ __forceinline__ double4 ld_sum(const double* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
+// dp_pair (placement_dp.cuh, kernels.py:210-239) for a top cell (l = Lu), with g(1),
+// g(jmax), h(1), h(jmax) and the caps J, K taken from the two row summaries (one load
+// each) instead of five scattered loads: the same shortcuts, bracket, probes and result.
+__device__ __forceinline__ void top_pair(const double* __restrict__ gv, const double* __restrict__ hv,
+                                         double g1, double gm, double h1, double hm, int J, int K, int l,
+                                         int jmax, bool cap, double floor, double& cand, int& cj) {
+  if (g1 <= h1) { cand = g1; cj = 1; return; }
+  if (gm >= hm) { cand = hm; cj = jmax; return; }
+  if ((g1 < hm ? g1 : hm) <= floor) { cand = kNegInf; cj = 0; return; }
+  int lo = 1, hi = jmax;
+  if (cap) {
+    hi = min(jmax, J + 1);
+    lo = max(1, min(min(J, l - K - 1), hi - 1));
+  }
+  const double* __restrict__ hl = hv + l;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (gv[mid] > hl[-mid]) lo = mid; else hi = mid;
+  }
+  const double vlo = hl[-lo];
+  const double vhi = gv[hi];
+  if (vlo >= vhi) { cand = vlo; cj = lo; } else { cand = vhi; cj = hi; }
+}
+
+__global__ void __launch_bounds__(256, 5) lat_top_kernel(TopArgs A) {
   const int lane = threadIdx.x & 31;
   const long long ci = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= A.ncombo) return;
@@ -616,25 +648,24 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
   const int Smax = min(n, Lu);
   // this lane's u codes (lane+1, lane+33): size, idx(u), idx(full-u) from the model's
   // rank table (code M-1-c is the complement of code c)
-  // (row offsets idx * LuP fit 32 bits in the GPU envelope)
   int su[2];
-  unsigned ru[2], rr[2];
+  unsigned iu[2], iy[2];
   const unsigned* rk = A.ranks + ci * 64;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int code = lane + 1 + 32 * k;
     su[k] = 1 << 20;
-    ru[k] = rr[k] = 0;
+    iu[k] = iy[k] = 0;
     if (code < M) {
       const unsigned e = rk[code], ec = rk[M - 1 - code];
       su[k] = (int)(e >> 24);
-      ru[k] = (e & 0xFFFFFFu) * (unsigned)LuP;
-      rr[k] = (ec & 0xFFFFFFu) * (unsigned)LuP;
+      iu[k] = e & 0xFFFFFFu;
+      iy[k] = ec & 0xFFFFFFu;
     }
   }
   // S ascending; strict improvement (templates.py:322) -> smaller S on ties
   double tbest = kNegInf;
-  int twin = 0, tcode = 0, tj = 0;
+  int twin = 0, tcode = 0, tj = 0, npairs = 0;
   if ((A.smask & 2u) && Smax >= 1) {  // S = 1: f[1][L][full] = value[full][L]
     double v = 0.0;
     for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], A.tab_mp[cfg[c] * Lu + (Lu - 1)]));
@@ -644,17 +675,26 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
     if (!((A.smask >> S) & 1u)) continue;
     const double* val = A.W.val(S);
     const double* lay = A.W.lay(S, S - 1);
+    const double* vsum = A.W.vs(S);
+    const double* hsum = S == 2 ? vsum : A.W.fs(S);
     double best = kNegInf;
     int bu = 1 << 20, bj = 0;
     // S == 2 reads value rows on both sides: symmetric, search the lower half only
     const int chalf = (S == 2 && ((A.xmask >> 2) & 1u)) ? (M - 1) / 2 : M;
     const bool cap = (A.xmask >> S) & 1u;  // exactly monotone rows: capped crossing search
+    const int jmax = Lu - (S - 1);
     for (int k = 0; k < 2; ++k) {
       if (su[k] > n - (S - 1) || lane + 1 + 32 * k > chalf) continue;
+      const double4 gs = ld_sum(vsum + (size_t)iu[k] * 4);
+      const double4 hs = ld_sum(hsum + (size_t)iy[k] * 4);
+      // S == 2: h(j) = value_2[Y][Lu - j]: h(1) = v[Lu-1] (.w), h(jmax) = v[1] (.y);
+      // S > 2:  h(j) = f_S[S-1][Y][Lu - j]: h(1) = f[Lu-1] (.z), h(jmax) = f[S-1] (.y)
       double cand;
       int cj;
       // only values above the best earlier S (and 1e-9) can matter (templates.py:322)
-      dp_pair<true>(val + ru[k], lay + rr[k], Lu, Lu - (S - 1), true, cand, cj, cap, tbest > 1e-9 ? tbest : 1e-9);
+      top_pair(val + (size_t)iu[k] * LuP, lay + (size_t)iy[k] * LuP, gs.y, gs.z, S == 2 ? hs.w : hs.z, hs.y,
+               __double2loint(gs.x), __double2loint(hs.x), Lu, jmax, cap, tbest > 1e-9 ? tbest : 1e-9, cand, cj);
+      ++npairs;
       if (cand > best) { best = cand; bu = lane + 1 + 32 * k; bj = cj; }
     }
     // an S only matters if some lane beats the best so far (strict, templates.py:322);
@@ -662,6 +702,10 @@ __global__ void __launch_bounds__(256) lat_top_kernel(TopArgs A) {
     if (!__any_sync(0xffffffffu, best > tbest && best > 1e-9)) continue;
     warp_argmax_code(best, bu, bj);
     if (best > tbest && best > 1e-9) { tbest = best; twin = S; tcode = bu; tj = bj; }
+  }
+  if (A.census) {
+    const unsigned np = __reduce_add_sync(0xffffffffu, (unsigned)npairs);
+    if (lane == 0) atomicAdd(A.census + 2, (unsigned long long)np);
   }
   if (lane) return;
   A.win[ci] = make_int4(__double2loint(tbest), __double2hiint(tbest), twin, (tcode << 10) | tj);
@@ -2112,7 +2156,10 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
   const long long LuP = lat_pitch(h->maxLu);
   const long long nS = std::max(h->n_max - 1, 1);                         // S = 2..n_max
   const long long nch = std::max((h->n_max - 2) * (h->n_max - 1) / 2, 1);  // (S, sg) choice layers
-  const size_t want_v = (size_t)(nS * ns * LuP * 8), want_f = 2 * want_v, want_c = (size_t)(nch * ns * LuP * 2);
+  // value tables + their row summaries (nS x states x 32 B); f tables + theirs
+  const size_t want_v = (size_t)(nS * ns * LuP * 8) + (size_t)(nS * ns * 32) + 32,
+               want_f = (size_t)(2 * nS * ns * LuP * 8) + (size_t)(nS * ns * 32) + 32,
+               want_c = (size_t)(nch * ns * LuP * 2);
   {  // already allocated: no memory query (cudaMemGetInfo can stall the step)
     int have = 0;
     while (have < h->nstreams && h->ws_value[have].cap >= want_v && h->ws_f0[have].cap >= want_f &&
@@ -2203,7 +2250,13 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   W.f = h->ws_f0[slot].as<double>();
   W.ch = h->ws_ch[slot].as<unsigned short>();
   W.stride = ns * lat_pitch(Lu);
-  (void)LuP;
+  {
+    const long long nS = std::max(h->n_max - 1, 1);  // summaries sit after the maxLu-pitched tables
+    // 32-byte aligned: lat_top_kernel reads a summary with one 256-bit load
+    W.vsum = h->ws_value[slot].as<double>() + ((nS * ns * LuP + 3) & ~3ll);
+    W.fsum = h->ws_f0[slot].as<double>() + ((2 * nS * ns * LuP + 3) & ~3ll);
+    W.sstride = ns * 4;
+  }
   const double* tab_mp = h->tab.as<double>() + h->tab_off[mp];
   if (Smax >= 2 && ns > 0) {
     const int ti = timed_begin(h, st, 2);
@@ -2242,6 +2295,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   T.rec = h->rec.as<coral_s1_record>() + h->cand_off[mp];
   T.win = h->ws_win[slot].as<int4>();
   T.ranks = ranks;
+  T.census = h->census_on ? h->census.as<unsigned long long>() : nullptr;
   const int ti = timed_begin(h, st, 0);
   lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
   timed_end(h, st, ti);
@@ -2277,7 +2331,7 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   h->ntimed = 0;
   // records not improved by any unit read as infeasible (num_stages 0)
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), st));
-  if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 8, st));
+  if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 32, st));
   if (h->lat_ready) {  // prepared on side[0] during enumerate (every model with candidates)
     CUDA_TRY(cudaStreamWaitEvent(st, h->prep_ev, 0));
   } else {
@@ -2351,7 +2405,7 @@ int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi) {
   h->own_mp.assign((size_t)h->NM * h->NP, 1);
   CUDA_TRY(cudaEventRecord(h->ev[4], h->stream));
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), h->stream));
-  if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 8, h->stream));
+  if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 32, h->stream));
   if ((rc = launch_percombo(h, h->stream, lo, hi, 1, 1, CORAL_S1_MAX_NODES))) return rc;
   CUDA_TRY(cudaEventRecord(h->ev[5], h->stream));
   h->have_eval = true;
@@ -2994,19 +3048,33 @@ int coral_s1_kernel_stats(const coral_s1_handle* h, int kind, double* total_ms, 
 int coral_s1_set_census(coral_s1_handle* h, int on) {
   if (!h) return fail(CORAL_S1_EINVAL, "null handle");
   int rc;
-  if (on && (rc = h->census.ensure(8))) return rc;
+  if (on && (rc = h->census.ensure(32))) return rc;
   h->census_on = on != 0;
   return 0;
 }
 
 int coral_s1_census(coral_s1_handle* h, int64_t* layer_bytes) {
+  int64_t v[4] = {0, 0, 0, 0};
+  const int rc = coral_s1_census_all(h, v, 4);
+  if (layer_bytes) *layer_bytes = v[0];
+  return rc;
+}
+
+int coral_s1_census_all(coral_s1_handle* h, int64_t* out, int n) {
   if (!h) return fail(CORAL_S1_EINVAL, "null handle");
-  unsigned long long v = 0;
+  unsigned long long v[4] = {0, 0, 0, 0};
   if (h->census_on) {
     CUDA_TRY(cudaStreamSynchronize(h->stream));
-    CUDA_TRY(cudaMemcpy(&v, h->census.p, 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(v, h->census.p, 32, cudaMemcpyDeviceToHost));
   }
-  if (layer_bytes) *layer_bytes = (int64_t)v;
+  for (int i = 0; i < n && i < 4; ++i) out[i] = (int64_t)v[i];
+  return 0;
+}
+
+int coral_s1_set_streams(coral_s1_handle* h, int n) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  if (n < 1 || n > coral_s1_handle::kStreams) return fail(CORAL_S1_EINVAL, "streams must be 1..4");
+  h->nstreams = n;
   return 0;
 }
 

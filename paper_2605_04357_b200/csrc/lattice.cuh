@@ -280,6 +280,14 @@ struct LatWork {
   double* f;              // [S-2][2][states][LuP]
   unsigned short* ch;     // [tri(S) + sg-2][states][LuP]
   long long stride;       // states * LuP
+  // per-row summaries the top cells read with ONE 32-byte load each (lat_top_kernel):
+  //   vsum(S)[X] = {J, value_S[X][1], value_S[X][Lu-S+1], value_S[X][Lu-1]}
+  //   fsum(S)[X] = {K, f_S[S-1][X][S-1], f_S[S-1][X][Lu-1], 0}
+  double* vsum;           // [S-2][states][4]
+  double* fsum;           // [S-2][states][4]
+  long long sstride;      // states * 4
+  __device__ __forceinline__ double* vs(int S) const { return vsum + (long long)(S - 2) * sstride; }
+  __device__ __forceinline__ double* fs(int S) const { return fsum + (long long)(S - 2) * sstride; }
   __device__ __forceinline__ double* val(int S) const { return value + (long long)(S - 2) * stride; }
   __device__ __forceinline__ double* lay(int S, int sg) const {
     return sg == 1 ? val(S) : f + ((long long)(S - 2) * 2 + (sg & 1)) * stride;
@@ -314,6 +322,7 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
   int cfg[kMaxC], cnt[kMaxC];
   const int C = lat_tokens(inv_rank, key, cfg, cnt);
   double* row = W.val(S) + idx * lat_pitch(Lu);
+  double* sum = W.vs(S) + idx * 4;
   int J = 0;
   for (int j0 = 1; j0 <= Lu; j0 += 32) {
     const int j = j0 + lane;
@@ -321,11 +330,17 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
     if (j <= Lu) {
       for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], tabS[cfg[c] * Lu + (j - 1)]));
       row[j] = v;
+      if (j == 1) sum[1] = v;
+      if (j == Lu - S + 1) sum[2] = v;
+      if (j == Lu - 1) sum[3] = v;
     }
     const unsigned pos = __ballot_sync(0xffffffffu, j <= Lu && v > 0.0);
     if (pos) J = j0 + 31 - __clz(pos);
   }
-  if (lane == 0) row[0] = __longlong_as_double((long long)J);  // J as integer bits
+  if (lane == 0) {
+    row[0] = __longlong_as_double((long long)J);  // J as integer bits
+    sum[0] = row[0];
+  }
 }
 
 // DP layer sg for every S in [S_lo, S_lo + gridDim.y) with S > sg: warp per state X,
@@ -376,8 +391,10 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
   // census (bench roofline, off in timed runs): algorithmic bytes of this state = its
   // f + choice cells written (10 B each), one read of its value_S and f_{sg-1} rows
   // and of its valid sub-table entries
-  if (census && lane == 0)
+  if (census && lane == 0) {
     atomicAdd(census, (unsigned long long)(10 * (lmax - sg + 1) + 16 * (Lu + 1) + 8 * nv));
+    atomicAdd(census + 1, (unsigned long long)nv * (unsigned long long)(lmax - sg + 1));  // (u, l) pairs
+  }
   for (int l0 = sg; l0 <= lmax; l0 += 32) {
     // lanes = G groups x wp positions; group g takes valid codes g, g+G, g+2G, ...
     const int w = min(32, lmax - l0 + 1);
@@ -415,11 +432,18 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
     if (act && g == 0) {
       fout[idx * LuP + l] = best;
       chout[idx * LuP + l] = (unsigned short)((bu << 10) | bj);
+      if (sg == S - 1) {  // the layer the top cells read: its summary entries
+        if (l == S - 1) W.fs(S)[idx * 4 + 1] = best;
+        if (l == Lu - 1) W.fs(S)[idx * 4 + 2] = best;
+      }
     }
     const unsigned pos = __ballot_sync(0xffffffffu, act && g == 0 && best > 0.0);  // group 0 = lanes 0..wp-1
     if (pos) kpos = l0 + 31 - __clz(pos);
   }
-  if (lane == 0) fout[idx * LuP] = __longlong_as_double((long long)kpos);  // K as integer bits
+  if (lane == 0) {
+    fout[idx * LuP] = __longlong_as_double((long long)kpos);  // K as integer bits
+    if (sg == S - 1) W.fs(S)[idx * 4] = fout[idx * LuP];
+  }
 }
 
 }  // namespace coral

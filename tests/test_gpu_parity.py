@@ -474,7 +474,7 @@ def test_lattice_workspace_beyond_device_memory(streams, monkeypatch):
     K, n_max = len(configs), caps.n_max
     ns = sum(comb(K + s - 1, s) for s in range(1, n_max))
     pitch = (int(max(lsteps)) + 2) & ~1  # lat_pitch
-    per_stream = ns * pitch * (8 * 3 * (n_max - 1) + 2 * ((n_max - 2) * (n_max - 1) // 2))
+    per_stream = ns * pitch * (8 * 3 * (n_max - 1) + 2 * ((n_max - 2) * (n_max - 1) // 2)) + 2 * ((n_max - 1) * ns * 32 + 32)
     # lattice_prepare first sets aside the evaluate's own buffers: records, per-stream
     # rank tables + winners, and the bounded frontier item buffer
     reserve = (64 << 20) + 2 * int(counts.sum()) * 32 + 4 * int(counts.max()) * (256 + 16)
