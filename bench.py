@@ -419,7 +419,7 @@ def main():
     counts = h.num_combos()
     _, lsteps, smax = h.table_layout()
     if masks is None:
-        masks = [sum(1 << S for S in range(1, 7))] * (len(w.models) * NP)
+        masks = [sum(1 << S for S in range(1, _native.MAX_NODES + 1))] * (len(w.models) * NP)
     top_alg = top_kernel_bytes(counts, lsteps, smax, masks, len(w.configs), w.n_max)
     top_launch_s = (top_ms / max(top_n, 1)) / 1e3
     top_achieved = (top_alg / max(top_n, 1)) / top_launch_s / 1e9 if top_n else 0.0
@@ -460,7 +460,7 @@ def main():
     dp_evals = 0
     for m in range(len(w.models)):
         keys = h.get_combos(m)
-        nodes = sum(((keys >> np.uint64(9 * t)) & np.uint64(7)).astype(np.int64) for t in range(6))
+        nodes = sum(((keys >> np.uint64(9 * t)) & np.uint64(7)).astype(np.int64) for t in range(_native.MAX_NODES))
         dp_evals += int(np.minimum(nodes, int(lsteps[m])).sum()) * NP
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -15,7 +15,7 @@
  *                                                      -> LibraryGenError
  *   CORAL_S1_ECUDA (3)           CUDA failure          -> RuntimeError
  *   CORAL_S1_EUNSUPPORTED (4)    input outside the GPU path's envelope
- *                                (n_max > 6, > 63 configs, > 128 layer units)
+ *                                (n_max > 7, > 63 configs, > 128 layer units)
  * The message of the last failure on the calling thread is coral_s1_last_error().
  * The library never aborts the process.
  */
@@ -38,9 +38,11 @@ extern "C" {
 #define CORAL_S1_PHASE_PREFILL 0
 #define CORAL_S1_PHASE_DECODE 1
 
-/* Largest envelope of the GPU path. n_max <= 6 keeps every node multiset's
- * sub-multiset lattice within 64 codes (kernels.py:147-150: M = prod(counts+1)). */
-#define CORAL_S1_MAX_NODES 6
+/* Largest envelope of the GPU path. n_max <= 7 (the reference's own acceptance sweep
+ * reaches (7, 14), pkg/tests/test_acceptance.py:320-348) keeps every node multiset's
+ * sub-multiset lattice within 128 codes (kernels.py:147-150: M = prod(counts+1)) and
+ * the packed combo key within 7 tokens x 9 bits = 63 bits. */
+#define CORAL_S1_MAX_NODES 7
 #define CORAL_S1_MAX_CONFIGS 63
 #define CORAL_S1_MAX_LAYER_UNITS 128
 
@@ -102,7 +104,7 @@ typedef struct coral_s1_record {
   uint8_t num_nodes;
   uint16_t layers_per_stage[CORAL_S1_MAX_NODES];
   uint8_t stage_of_node[CORAL_S1_MAX_NODES];
-  uint8_t _pad[4]; /* explicit, always zero: records compare bytewise */
+  uint8_t _pad[1]; /* explicit, always zero: records compare bytewise */
 } coral_s1_record; /* 32 bytes */
 
 /* One frontier survivor (new output). */
@@ -158,8 +160,8 @@ int coral_s1_enumerate(coral_s1_handle* h);
 int coral_s1_num_combos(const coral_s1_handle* h, int64_t* counts /* [num_models] */);
 /* keys of model m in str(combo) order (the library order, templates.py:340);
  * with enumeration_order != 0 in the reference's (num_nodes, str) order
- * (templates.py:112). key = 6 tokens x 9 bits, token = (rank'+1)<<3 | count,
- * first token most significant. */
+ * (templates.py:112). key = 7 tokens x 9 bits, token = (rank'+1)<<3 | count,
+ * first token most significant, zero padded. */
 int coral_s1_get_combos(coral_s1_handle* h, int model, int enumeration_order,
                         uint64_t* keys, int64_t n);
 
@@ -201,11 +203,11 @@ int coral_s1_frontier_candidates(coral_s1_handle* h, int num_regions, const doub
                                  int64_t* num_candidates);
 
 /* ---- operator: placement_search (kernels.py:279-295), batched ----------
- * case i: counts[i*6 .. +C_i) (int64), C_i = ncfg[i] <= 6, tput rows at
+ * case i: counts[i*7 .. +C_i) (int64), C_i = ncfg[i] <= 7, tput rows at
  * tput + tput_off[i] (C_i x L_i doubles, row-major), S_i. Outputs raw (not
  * canonicalised) results exactly as the numba kernel returns them:
- * best[i] (NEG_INF = -1e300 when infeasible), stage_j[i*6 + s],
- * stage_counts[(i*6 + s)*6 + c]. Host buffers. */
+ * best[i] (NEG_INF = -1e300 when infeasible), stage_j[i*7 + s],
+ * stage_counts[(i*7 + s)*7 + c] (7 = CORAL_S1_MAX_NODES). Host buffers. */
 int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t* ncfg,
                               const int64_t* counts, const int32_t* lsteps,
                               const int64_t* tput_off, const double* tput,

@@ -20,7 +20,7 @@ _LIB_PATH = os.environ.get("CORAL_S1_LIB") or os.path.join(os.path.dirname(os.pa
 
 OK, EINVAL, ENOTEMPLATE, ECUDA, EUNSUPPORTED = 0, 1, 2, 3, 4
 PHASE_CODE = {"prefill": 0, "decode": 1}
-MAX_NODES = 6
+MAX_NODES = 7
 NEG_INF = -1e300
 
 _i32p = C.POINTER(C.c_int32)
@@ -50,7 +50,7 @@ class Problem(C.Structure):
 
 RECORD_DTYPE = np.dtype([("throughput_tps", "<f8"), ("num_stages", "u1"), ("num_nodes", "u1"),
                          ("layers_per_stage", "<u2", (MAX_NODES,)),
-                         ("stage_of_node", "u1", (MAX_NODES,)), ("_pad", "u1", (4,))], align=True)
+                         ("stage_of_node", "u1", (MAX_NODES,)), ("_pad", "u1", (1,))], align=True)
 FRONTIER_DTYPE = np.dtype([("price_usd_h", "<f8"), ("throughput_tps", "<f8"),
                            ("combo_key", "<u8"), ("mp", "<i4"), ("region", "<i4"),
                            ("rec", RECORD_DTYPE)], align=True)

@@ -90,6 +90,7 @@ struct DevBuf {
 struct coral_s1_handle {
   int device = 0;
   int num_sms = 148, ranks_blocks_per_sm = 1;
+  size_t dp_smem_limit = 0;  // dynamic shared memory the per-candidate DP kernels may use
   cudaStream_t stream = nullptr;
   long long launches = 0;
   bool have_problem = false, have_tables = false, have_enum = false, have_eval = false;
@@ -260,7 +261,7 @@ __device__ __forceinline__ void unrank_key(const unsigned long long (*B)[8], con
     m -= c;
   }
   key <<= kKeyTokenBits * (kMaxC - ntok);
-  // picks in config-index (name) order: sort the <= 6 tokens by config
+  // picks in config-index (name) order: sort the <= 7 tokens by config
   for (int a = 1; a < ntok; ++a)
     for (int b = a; b > 0 && tcfg[b - 1] > tcfg[b]; --b) {
       const int t0 = tcfg[b], t1 = tcnt[b];
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
   const int m = mp / P.NP;
   const int K = P.K;
   const int Lu = sh.Lu, LuP = sh.LuP, C = sh.C, M = sh.M, n = sh.n;
-  const DpBuffers B = dp_carve(smem, M, LuP, Lu);
+  const DpBuffers B = dp_carve(smem, M, LuP, Lu, n - 2);
   const int Smax = min(min(n, Lu), A.S_hi);
   for (int S = A.S_lo; S <= Smax; ++S) {
     // tables[S][cfg_rows, :] (templates.py:320)
@@ -636,6 +637,9 @@ __device__ __forceinline__ void top_pair(const double* __restrict__ gv, const do
   if (vlo >= vhi) { cand = vlo; cj = lo; } else { cand = vhi; cj = hi; }
 }
 
+// kSlots code slots per lane (codes lane + 1 + 32k): 2 for candidates of <= 6 nodes
+// (M <= 64), 4 when a model has 7-node candidates (M <= 128).
+template <int kSlots>
 __global__ void __launch_bounds__(256, 5) lat_top_kernel(TopArgs A) {
   const int lane = threadIdx.x & 31;
   const long long ci = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -648,11 +652,11 @@ __global__ void __launch_bounds__(256, 5) lat_top_kernel(TopArgs A) {
   const int Smax = min(n, Lu);
   // this lane's u codes (lane+1, lane+33): size, idx(u), idx(full-u) from the model's
   // rank table (code M-1-c is the complement of code c)
-  int su[2];
-  unsigned iu[2], iy[2];
-  const unsigned* rk = A.ranks + ci * 64;
+  int su[kSlots];
+  unsigned iu[kSlots], iy[kSlots];
+  const unsigned* rk = A.ranks + ci * kRankStride;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kSlots; ++k) {
     const int code = lane + 1 + 32 * k;
     su[k] = 1 << 20;
     iu[k] = iy[k] = 0;
@@ -683,7 +687,8 @@ __global__ void __launch_bounds__(256, 5) lat_top_kernel(TopArgs A) {
     const int chalf = (S == 2 && ((A.xmask >> 2) & 1u)) ? (M - 1) / 2 : M;
     const bool cap = (A.xmask >> S) & 1u;  // exactly monotone rows: capped crossing search
     const int jmax = Lu - (S - 1);
-    for (int k = 0; k < 2; ++k) {
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) {
       if (su[k] > n - (S - 1) || lane + 1 + 32 * k > chalf) continue;
       const double4 gs = ld_sum(vsum + (size_t)iu[k] * 4);
       const double4 hs = ld_sum(hsum + (size_t)iy[k] * 4);
@@ -808,7 +813,7 @@ __global__ void __launch_bounds__(kDpThreads) placement_op_kernel(OpArgs A) {
     if (tid == 0) A.best[i] = kNegInf;
     return;
   }
-  const DpBuffers B = dp_carve(smem, M, LuP, Lu);
+  const DpBuffers B = dp_carve(smem, M, LuP, Lu, n - 2);
   const double* rows = A.tput + A.tput_off[i];
   for (int idx = tid; idx < C * Lu; idx += blockDim.x) B.tputS[idx] = rows[idx];
   __syncthreads();
@@ -1264,12 +1269,13 @@ __global__ void node_query_kernel(DevProblem P, int64_t n, const int* __restrict
 // Frontier order: segment asc, price asc, T desc, combo key asc,
 // stages asc -- the last only separates the per-rank partial records of one
 // (model, phase, combo) in the multi-GPU merge (fewer stages first, the
-// templates.py:322 tie rule). One 32-byte composite key, compared lexicographically.
+// templates.py:322 tie rule). One 40-byte composite key, compared lexicographically.
 struct FrontKey {
   unsigned seg, idx;            // segment = mp * R + region; idx = position in items
   unsigned long long price;     // bit pattern of price >= 0 (orders like the value)
   unsigned long long neg_t;     // ~bits(T), T > 0: ascending = T descending
-  unsigned long long key_s;     // combo_key << 3 | num_stages
+  unsigned long long key;       // packed combo key (63 bits)
+  unsigned stages, pad;         // num_stages
 };
 
 struct FrontLess {
@@ -1277,7 +1283,8 @@ struct FrontLess {
     if (a.seg != b.seg) return a.seg < b.seg;
     if (a.price != b.price) return a.price < b.price;
     if (a.neg_t != b.neg_t) return a.neg_t < b.neg_t;
-    return a.key_s < b.key_s;
+    if (a.key != b.key) return a.key < b.key;
+    return a.stages < b.stages;
   }
 };
 
@@ -1291,7 +1298,9 @@ __global__ void front_keys_kernel(const coral_s1_frontier_item* __restrict__ ite
   k.idx = (unsigned)i;
   k.price = (unsigned long long)__double_as_longlong(it.price_usd_h);
   k.neg_t = ~(unsigned long long)__double_as_longlong(it.throughput_tps);
-  k.key_s = it.combo_key << 3 | it.rec.num_stages;
+  k.key = it.combo_key;
+  k.stages = it.rec.num_stages;
+  k.pad = 0u;
   out[i] = k;
 }
 
@@ -1674,9 +1683,17 @@ int coral_s1_create(int device, coral_s1_handle** out) {
   if (const char* e = getenv("CORAL_S1_MEM_LIMIT")) h->mem_limit = (size_t)strtoull(e, nullptr, 10);
   if (h->lat_binom_d.ensure(sizeof(tab)) == 0)
     cudaMemcpy(h->lat_binom_d.p, tab, sizeof(tab), cudaMemcpyHostToDevice);
-  const size_t smem_max = dp_smem_bytes(kMaxM, CORAL_S1_MAX_LAYER_UNITS + 1, CORAL_S1_MAX_LAYER_UNITS);
-  cudaFuncSetAttribute(evaluate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
-  cudaFuncSetAttribute(placement_op_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+  {  // the per-candidate DP kernels may take all the shared memory their statics leave
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, evaluate_kernel);
+    h->dp_smem_limit = (size_t)std::max(0, optin - (int)fa.sharedSizeBytes);
+    cudaFuncGetAttributes(&fa, placement_op_kernel);
+    h->dp_smem_limit = std::min(h->dp_smem_limit, (size_t)std::max(0, optin - (int)fa.sharedSizeBytes));
+    cudaFuncSetAttribute(evaluate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dp_smem_limit);
+    cudaFuncSetAttribute(placement_op_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dp_smem_limit);
+  }
   cudaFuncSetAttribute(front_segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSegCap * sizeof(SegKey)));
   e = cudaGetLastError();
   if (e != cudaSuccess) { delete h; return fail(CORAL_S1_ECUDA, cudaGetErrorString(e)); }
@@ -1728,7 +1745,7 @@ int coral_s1_set_problem(coral_s1_handle* h, const coral_s1_problem* p) {
   if (p->n_max < 1) return fail(CORAL_S1_EINVAL, "n_max must be >= 1");
   if (!(p->rho > 1)) return fail(CORAL_S1_EINVAL, "rho must be > 1");
   if (p->n_max > CORAL_S1_MAX_NODES)
-    return fail(CORAL_S1_EUNSUPPORTED, "GPU path supports n_max <= 6");
+    return fail(CORAL_S1_EUNSUPPORTED, "GPU path supports n_max <= 7");
   if (p->num_configs < 0 || p->num_configs > CORAL_S1_MAX_CONFIGS)
     return fail(CORAL_S1_EUNSUPPORTED, "GPU path supports <= 63 node configs");
   if (p->num_models < 0 || p->num_phases < 0 || p->num_phases > 2)
@@ -2039,7 +2056,11 @@ static int launch_percombo(coral_s1_handle* h, cudaStream_t st, int64_t lo, int6
   A.tab_off = h->tab_off_d.as<int64_t>();
   A.flags = h->flags.as<unsigned char>();
   A.rec = h->rec.as<coral_s1_record>();
-  const size_t smem = dp_smem_bytes(kMaxM, h->maxLu + 1, h->maxLu);
+  const size_t smem = dp_smem_bytes(std::min(kMaxM, 1 << h->n_max), h->maxLu + 1, h->maxLu, h->n_max - 2);
+  if (smem > h->dp_smem_limit)
+    return fail(CORAL_S1_EUNSUPPORTED, "per-candidate placement DP: n_max " + std::to_string(h->n_max) +
+                                           " with " + std::to_string(h->maxLu) +
+                                           " layer units exceeds shared memory (the lattice path covers it)");
   const int64_t nblocks = (hi - lo + stride - 1) / stride;
   const int64_t chunk = 1ll << 30;
   for (int64_t b0 = 0; b0 < nblocks; b0 += chunk) {
@@ -2079,6 +2100,11 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
   }
   h->lat_states = h->lat_base[R + 1];
   int rc;
+  if (h->lat_states >= (1ll << 24)) {  // state indices are packed in 24 bits (rank tables,
+    h->lat_ok = false;                 // sub-tables): beyond that every unit takes the exact
+    h->lat_states = 0;                 // per-candidate kernel
+    return 0;
+  }
   if ((rc = upload(h, h->lat_base_d, h->lat_base, st))) return rc;
   if (h->lat_states == 0) return 0;
   const long long ns = h->lat_states;
@@ -2190,7 +2216,7 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
     const size_t have_rec = h->rec.cap, want_rec = (size_t)nc * sizeof(coral_s1_record);
     reserve += want_rec > have_rec ? want_rec - have_rec : 0;
     for (int i = 0; i < h->nstreams; ++i) {
-      const size_t want = (size_t)maxc * (64 * sizeof(unsigned) + sizeof(int4)), have = h->ws_ranks[i].cap + h->ws_win[i].cap;
+      const size_t want = (size_t)maxc * (kRankStride * sizeof(unsigned) + sizeof(int4)), have = h->ws_ranks[i].cap + h->ws_win[i].cap;
       reserve += want > have ? want - have : 0;
     }
   }
@@ -2270,10 +2296,16 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
     const long long nst = h->lat_base[h->n_max - 1 + 1] - h->lat_base[sg];
     if (nst <= 0) continue;
     const int ti = timed_begin(h, st, 1);
-    lat_layer_kernel<<<dim3((unsigned)((nst * 32 + 255) / 256), Smax - sg), 256, 0, st>>>(
-        L, sg, sg + 1, smask, xmask, h->n_max, Lu, h->lat_maxn.as<unsigned>() + (size_t)m * ns,
-        h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), W,
-        h->census_on ? h->census.as<unsigned long long>() : nullptr);
+    const dim3 lgrid((unsigned)((nst * 32 + 255) / 256), Smax - sg);
+    unsigned long long* cen = h->census_on ? h->census.as<unsigned long long>() : nullptr;
+    if (h->n_max >= 7)  // states of 6 configs: up to 63 sub-multiset codes
+      lat_layer_kernel<2><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu,
+                                                 h->lat_maxn.as<unsigned>() + (size_t)m * ns,
+                                                 h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), W, cen);
+    else
+      lat_layer_kernel<1><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu,
+                                                 h->lat_maxn.as<unsigned>() + (size_t)m * ns,
+                                                 h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), W, cen);
     timed_end(h, st, ti);
     LAUNCH_CHECK(h);
   }
@@ -2297,7 +2329,10 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   T.ranks = ranks;
   T.census = h->census_on ? h->census.as<unsigned long long>() : nullptr;
   const int ti = timed_begin(h, st, 0);
-  lat_top_kernel<<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
+  if (h->n_max >= 7)
+    lat_top_kernel<4><<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
+  else
+    lat_top_kernel<2><<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
   timed_end(h, st, ti);
   LAUNCH_CHECK(h);
   const int td = timed_begin(h, st, 3);
@@ -2356,7 +2391,7 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   // per chain stream: the model's sub-multiset rank table and the top cells' winners
   // (both stream-ordered within a model's chains, so one buffer per stream suffices)
   for (int i = 0; i < h->nstreams; ++i)
-    if ((rc = h->ws_ranks[i].ensure(maxc * 64 * sizeof(unsigned))) || (rc = h->ws_win[i].ensure(maxc * sizeof(int4))))
+    if ((rc = h->ws_ranks[i].ensure(maxc * kRankStride * sizeof(unsigned))) || (rc = h->ws_win[i].ensure(maxc * sizeof(int4))))
       return rc;
   int slot = 0;
   for (int m : order) {
@@ -2628,19 +2663,21 @@ int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t*
   if (!h) return fail(CORAL_S1_EINVAL, "null handle");
   if (ncases <= 0) return 0;
   CUDA_TRY(cudaSetDevice(h->device));
-  int maxLu = 1;
+  int maxLu = 1, maxM = 1, maxN = 0;
   for (int64_t i = 0; i < ncases; ++i) {
-    if (ncfg[i] < 1 || ncfg[i] > kMaxC) return fail(CORAL_S1_EUNSUPPORTED, "placement_search: 1..6 configs");
+    if (ncfg[i] < 1 || ncfg[i] > kMaxC) return fail(CORAL_S1_EUNSUPPORTED, "placement_search: 1..7 configs");
     long long M = 1;
     for (int c = 0; c < ncfg[i]; ++c) {
       if (counts[i * kMaxC + c] < 0) return fail(CORAL_S1_EINVAL, "negative count");
       M *= counts[i * kMaxC + c] + 1;
     }
-    if (M > kMaxM) return fail(CORAL_S1_EUNSUPPORTED, "placement_search: prod(counts+1) must be <= 64");
+    if (M > kMaxM) return fail(CORAL_S1_EUNSUPPORTED, "placement_search: prod(counts+1) must be <= 128");
     long long nodes = 0;
     for (int c = 0; c < ncfg[i]; ++c) nodes += counts[i * kMaxC + c];
-    if (nodes > CORAL_S1_MAX_NODES)  // the DP's per-size tables hold <= 6 nodes
-      return fail(CORAL_S1_EUNSUPPORTED, "placement_search: at most 6 nodes per multiset");
+    if (nodes > CORAL_S1_MAX_NODES)  // the DP's per-size tables hold <= 7 nodes
+      return fail(CORAL_S1_EUNSUPPORTED, "placement_search: at most 7 nodes per multiset");
+    maxM = std::max(maxM, (int)M);
+    maxN = std::max(maxN, (int)nodes);
     if (lsteps[i] < 1 || lsteps[i] > CORAL_S1_MAX_LAYER_UNITS)
       return fail(CORAL_S1_EUNSUPPORTED, "placement_search: 1..128 layer units");
     if (tput_off[i] < 0 || tput_off[i] + (int64_t)ncfg[i] * lsteps[i] > tput_len)
@@ -2684,7 +2721,9 @@ int coral_s1_placement_search(coral_s1_handle* h, int64_t ncases, const int32_t*
   A.stage_j = (long long*)(out + ob_sj);
   A.stage_counts = (long long*)(out + ob_sc);
   A.ncases = ncases;
-  const size_t smem = dp_smem_bytes(kMaxM, maxLu + 1, maxLu);
+  const size_t smem = dp_smem_bytes(maxM, maxLu + 1, maxLu, maxN - 2);
+  if (smem > h->dp_smem_limit)
+    return fail(CORAL_S1_EUNSUPPORTED, "placement_search: multiset x layer units exceed shared memory");
   placement_op_kernel<<<(unsigned)ncases, kDpThreads, smem, st>>>(A);
   LAUNCH_CHECK(h);
   CUDA_TRY(cudaMemcpyAsync(best, out + ob_best, ncases * 8, cudaMemcpyDeviceToHost, st));

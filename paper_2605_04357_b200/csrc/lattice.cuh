@@ -28,7 +28,8 @@
 
 namespace coral {
 
-constexpr int kLatMaxState = kMaxC - 1;  // lattice tables hold |X| <= 5
+constexpr int kLatMaxState = kMaxC - 1;  // lattice tables hold |X| <= n_max - 1 <= 6
+constexpr int kRankStride = kMaxM;       // rank-table entries per candidate (codes < 2^n)
 
 // Row pitch of the lattice value / f / choice tables: Lu + 1 rounded up to even, so
 // every row starts 16-byte aligned and dp_pair's capped search fetches (J, g[1]) with
@@ -135,10 +136,10 @@ __global__ void lat_maxn_closed_kernel(LatModel L, const int* __restrict__ inv_r
   maxn[idx] = best;
 }
 
-// ceil(2^16 / r) for radices r = 1..7: q = (x * kLatMagic[r]) >> 16 equals x / r for
-// every x < 2^16 / 7 (the error term x * (m r - 2^16) stays below 2^16), and sub-multiset
-// codes are < 64.
-__constant__ unsigned kLatMagic[8] = {0u, 65536u, 32768u, 21846u, 16384u, 13108u, 10923u, 9363u};
+// ceil(2^16 / r) for radices r = 1..8: q = (x * kLatMagic[r]) >> 16 equals x / r for
+// every x < 2^16 / 8 (the error term x * (m r - 2^16) stays below 2^16), and sub-multiset
+// codes are < 128.
+__constant__ unsigned kLatMagic[9] = {0u, 65536u, 32768u, 21846u, 16384u, 13108u, 10923u, 9363u, 8192u};
 
 // Colex sums of the sub-multiset u = digits(code) of the packed key (token 0 is the
 // least significant mixed-radix digit, radix count + 1 -- the code order of
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kRanksWarps * 32) lat_ranks_kernel(
       magic[t] = kLatMagic[radix[t]];
       M *= (int)radix[t];
     }
-    unsigned* out = ranks + ci * 64;
+    unsigned* out = ranks + ci * kRankStride;
     for (unsigned code = lane; (int)code < M; code += 32) {
       unsigned rest = code, acc = 0, p9 = 0;  // p9 = 9 * picks so far: C(cfg + p, p) at cb + 9p
 #pragma unroll
@@ -255,20 +256,22 @@ __global__ void lat_nsub_kernel(LatModel L, const unsigned long long* __restrict
 }
 
 // subtab[off[X] + code] = {size(u) << 24 | idx(u), idx(X - u)} for code in [0, M(X)).
-// Warp per state X, lane = code: |X| <= R <= 5 gives M(X) <= 32.
+// Warp per state X, lane = code (+32): |X| <= R <= 6 gives M(X) <= 64.
 __global__ void lat_subtab_kernel(LatModel L, const int* __restrict__ inv_rank,
                                   const unsigned long long* __restrict__ state_key,
                                   const long long* __restrict__ off, uint2* __restrict__ subtab) {
   const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (idx >= L.base[L.R + 1]) return;
-  const unsigned code = threadIdx.x & 31u;
-  int su, sr;
-  unsigned long long au, ar;
-  const int M = lat_code_ranks<true>(L, inv_rank, state_key[idx], code, &su, &au, &sr, &ar);
-  if ((int)code < M)
+  const unsigned long long key = state_key[idx];
+  for (unsigned code = threadIdx.x & 31u;; code += 32u) {
+    int su, sr;
+    unsigned long long au, ar;
+    const int M = lat_code_ranks<true>(L, inv_rank, key, code, &su, &au, &sr, &ar);
+    if ((int)code >= M) break;
     subtab[off[idx] + code] =
         make_uint2(((unsigned)su << 24) | (su ? (unsigned)(L.base[su] + (long long)au) : 0u),
                    sr ? (unsigned)(L.base[sr] + (long long)ar) : 0u);
+  }
 }
 
 // ---- per (model, phase): every S at once ----------------------------------------
@@ -345,6 +348,9 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
 
 // DP layer sg for every S in [S_lo, S_lo + gridDim.y) with S > sg: warp per state X,
 // lanes over l. Cells: sg <= |X| <= maxn(X) - (S - sg), sg <= l <= Lu - (S - sg).
+// kSlots = ceil((M(X) - 1) / 32) code slots per lane: 1 while n_max <= 6 (|X| <= 5),
+// 2 for n_max = 7 (|X| <= 6, M(X) <= 64).
+template <int kSlots>
 __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
     LatModel L, int sg, int S_lo, unsigned smask, unsigned xmask, int n_max, int Lu,
     const unsigned* __restrict__ maxn, const long long* __restrict__ off,
@@ -372,22 +378,49 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
   const double* __restrict__ fprev = W.lay(S, sg - 1);
   double* __restrict__ fout = W.lay(S, sg);
   unsigned short* __restrict__ chout = W.chl(S, sg);
-  // u codes of X that pass the size filter (M(X) <= 2^5 = 32): one per lane, ballot
-  const int mycode = lane + 1;
-  uint2 myent = make_uint2(0u, 0u);
-  bool ok = false;
-  if (mycode < cmax) {
-    myent = subtab[o + mycode];
-    ok = (int)(myent.x >> 24) <= usz;
+  // u codes of X that pass the size filter: slot k of a lane holds code lane + 1 + 32k;
+  // ballot per slot, then compaction (valid code #i at lane i & 31, slot i >> 5)
+  uint2 myent[kSlots];
+  unsigned vm[kSlots];
+  int nv = 0;
+#pragma unroll
+  for (int k = 0; k < kSlots; ++k) {
+    const int code = lane + 1 + 32 * k;
+    myent[k] = make_uint2(0u, 0u);
+    bool ok = false;
+    if (code < cmax) {
+      myent[k] = subtab[o + code];
+      ok = (int)(myent[k].x >> 24) <= usz;
+    }
+    vm[k] = __ballot_sync(0xffffffffu, ok);
+    nv += __popc(vm[k]);
   }
-  const unsigned vmask = __ballot_sync(0xffffffffu, ok);
-  const int nv = __popc(vmask);
   int kpos = 0;  // last l with f > 0 -> column 0 of the f row (dp_pair's search cap)
-  // compact once per state: lane k holds the k-th valid code (ascending) and the
-  // 32-bit row offsets of its value_S[u] and f[X-u] rows (< 2^32 in the envelope)
-  const int cpos = lane < nv ? (int)__fns(vmask, 0, lane + 1) : 0;
-  const unsigned cvo = (__shfl_sync(0xffffffffu, myent.x, cpos) & 0xFFFFFFu) * (unsigned)LuP;
-  const unsigned cfo = __shfl_sync(0xffffffffu, myent.y, cpos) * (unsigned)LuP;
+  // compacted slot r of a lane: the 32-bit row offsets of its value_S[u] and f[X-u]
+  // rows (< 2^32 in the envelope) and its code
+  unsigned cvo[kSlots], cfo[kSlots];
+  int ccode[kSlots];
+#pragma unroll
+  for (int r = 0; r < kSlots; ++r) {
+    const int i = lane + 32 * r;  // valid code #i
+    int before = 0, src = 0, word = 0;
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) {
+      const int cnt = __popc(vm[k]);
+      if (i >= before && i < before + cnt) { word = k; src = (int)__fns(vm[k], 0, i - before + 1); }
+      before += cnt;
+    }
+    unsigned ex = 0u, ey = 0u;
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) {
+      const unsigned x = __shfl_sync(0xffffffffu, myent[k].x, src);
+      const unsigned y = __shfl_sync(0xffffffffu, myent[k].y, src);
+      if (k == word) { ex = x; ey = y; }
+    }
+    cvo[r] = (ex & 0xFFFFFFu) * (unsigned)LuP;
+    cfo[r] = ey * (unsigned)LuP;
+    ccode[r] = src + 1 + 32 * word;
+  }
   // census (bench roofline, off in timed runs): algorithmic bytes of this state = its
   // f + choice cells written (10 B each), one read of its value_S and f_{sg-1} rows
   // and of its valid sub-table entries
@@ -411,15 +444,21 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
     const int T = (nv + G - 1) >> (5 - lw);
     for (int t = 0; t < T; ++t) {
       const int kk = t * G + g;  // this group's kk-th valid code (ascending per group)
-      const int src = kk < nv ? kk : 0;
-      const unsigned vo = __shfl_sync(0xffffffffu, cvo, src);
-      const unsigned fo = __shfl_sync(0xffffffffu, cfo, src);
-      const int pos = __shfl_sync(0xffffffffu, cpos, src);
+      const int src = (kk < nv ? kk : 0) & 31, slot = kSlots > 1 && kk < nv ? kk >> 5 : 0;
+      unsigned vo = 0u, fo = 0u;
+      int code = 0;
+#pragma unroll
+      for (int r = 0; r < kSlots; ++r) {
+        const unsigned a = __shfl_sync(0xffffffffu, cvo[r], src);
+        const unsigned b = __shfl_sync(0xffffffffu, cfo[r], src);
+        const int c = __shfl_sync(0xffffffffu, ccode[r], src);
+        if (r == slot) { vo = a; fo = b; code = c; }
+      }
       if (!act || kk >= nv) continue;
       double cand;
       int cj;
       dp_pair(value + vo, fprev + fo, l, jmax, true, cand, cj, cap);
-      if (cand > best) { best = cand; bu = pos + 1; bj = cj; }
+      if (cand > best) { best = cand; bu = code; bj = cj; }
     }
     // merge the groups of each l: value desc, then smallest code (the reference's
     // first strictly better u over the ascending code sequence)

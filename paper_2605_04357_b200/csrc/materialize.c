@@ -21,6 +21,7 @@ static PyObject *s_items, *s_num_stages, *s_layers, *s_son, *s_model, *s_phase, 
  * values (no per-object dict), which is what makes building and freeing ~10^6 small
  * frozen dataclass instances cheap. */
 static PyObject* s_empty;
+static PyObject* s_63; /* int 63: (mp << 63) | combo key as the survivor cache key */
 static PyObject* new_obj(PyTypeObject* tp) { return PyBaseObject_Type.tp_new(tp, s_empty, NULL); }
 
 /* setattr bypassing the frozen dataclass __setattr__ (object.__setattr__); steals v */
@@ -99,8 +100,17 @@ static PyObject* materialise(PyObject* self, PyObject* args) {
       PyErr_SetString(PyExc_ValueError, "frontier item outside the problem's (model, phase, region)");
       goto fail;
     }
-    /* (mp, combo) as one int: the packed key uses 9 * CORAL_S1_MAX_NODES = 54 bits */
-    PyObject* ck = PyLong_FromUnsignedLongLong(((unsigned long long)mp << 54) | x->combo_key);
+    /* (mp, combo) as one int: mp above the 9 * CORAL_S1_MAX_NODES = 63 key bits */
+    PyObject* ck = NULL;
+    {
+      PyObject* hi = PyLong_FromLong(mp);
+      PyObject* sh = hi ? PyNumber_Lshift(hi, s_63) : NULL;
+      PyObject* lo = PyLong_FromUnsignedLongLong(x->combo_key);
+      ck = (sh && lo) ? PyNumber_Or(sh, lo) : NULL;
+      Py_XDECREF(hi);
+      Py_XDECREF(sh);
+      Py_XDECREF(lo);
+    }
     if (!ck) goto fail;
     PyObject* t = PyDict_GetItem(cache, ck); /* borrowed */
     if (!t) {
@@ -506,6 +516,7 @@ static struct PyModuleDef mod = {PyModuleDef_HEAD_INIT, "_materialize", NULL, -1
 
 PyMODINIT_FUNC PyInit__materialize(void) {
   s_empty = PyTuple_New(0);
+  s_63 = PyLong_FromLong(9 * CORAL_S1_MAX_NODES);
   s_items = PyUnicode_InternFromString("items");
   s_num_stages = PyUnicode_InternFromString("num_stages");
   s_layers = PyUnicode_InternFromString("layers_per_stage");

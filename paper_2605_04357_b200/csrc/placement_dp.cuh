@@ -22,14 +22,15 @@
 //    in trip count); lanes differ only in the binary-search path.
 //  * The top cell is split over lanes by u and reduced with the reference's
 //    tie rule (largest value, then smallest u code).
-//  * Choices are kept as u16 (u << 10 | j) only for layers 2..S-1.
+//  * Choices are kept as u16 (u << 8 | j) only for layers 2..S-1 (u < 128 codes,
+//    j <= 128 layer units).
 #pragma once
 #include "roofline.cuh"
 
 namespace coral {
 
-constexpr int kMaxC = 6;
-constexpr int kMaxM = 64;
+constexpr int kMaxC = CORAL_S1_MAX_NODES;  // tokens per key, nodes per multiset, stages
+constexpr int kMaxM = 1 << kMaxC;          // sub-multiset codes: prod(counts + 1) <= 2^n
 constexpr int kDpWarps = 8;
 constexpr int kDpThreads = kDpWarps * 32;
 
@@ -39,8 +40,8 @@ struct DpShared {
   int mono;  // np.all(np.diff(tput, axis=1) <= 1e-12) over the rows in use (kernels.py:291)
   unsigned char digits[kMaxM][kMaxC];
   unsigned char sizes[kMaxM];
-  unsigned long long contain[kMaxM];  // bit u set <=> u is a sub-multiset of rem
-  unsigned long long size_le[kMaxC + 2];
+  unsigned long long contain[kMaxM][2];  // bit u set <=> u is a sub-multiset of rem (128 bits)
+  unsigned long long size_le[kMaxC + 2][2];
   unsigned char bysize[kMaxC + 1][kMaxM];
   int nbysize[kMaxC + 1];
   // top-cell result
@@ -55,26 +56,28 @@ struct DpShared {
 struct DpBuffers {
   double* value;       // [M][LuP]
   double* f;           // [M][LuP]
-  unsigned short* ch;  // [kMaxC-2][M][LuP]
+  unsigned short* ch;  // [n-2][M][LuP]
   double* tputS;       // [C][Lu]
 };
+// (choices: [n - 2][M][LuP], layer sg at (sg - 2))
 
-__host__ __device__ inline size_t dp_smem_bytes(int maxM, int maxLuP, int maxLu) {
+// nlayers = choice layers kept (stage counts S <= n need layers 2..S-1: n - 2)
+__host__ __device__ inline size_t dp_smem_bytes(int maxM, int maxLuP, int maxLu, int nlayers) {
   size_t b = 0;
   b += (size_t)maxM * maxLuP * sizeof(double) * 2;
-  b += (size_t)(kMaxC - 2) * maxM * maxLuP * sizeof(unsigned short);
+  b += (size_t)(nlayers > 0 ? nlayers : 0) * maxM * maxLuP * sizeof(unsigned short);
   b = (b + 15) & ~(size_t)15;
   b += (size_t)kMaxC * maxLu * sizeof(double);
   return b;
 }
 
-__device__ inline DpBuffers dp_carve(unsigned char* smem, int M, int LuP, int Lu) {
+__device__ inline DpBuffers dp_carve(unsigned char* smem, int M, int LuP, int Lu, int nlayers) {
   DpBuffers B;
   B.value = reinterpret_cast<double*>(smem);
   B.f = B.value + (size_t)M * LuP;
   B.ch = reinterpret_cast<unsigned short*>(B.f + (size_t)M * LuP);
   size_t off = (size_t)M * LuP * sizeof(double) * 2 +
-               (size_t)(kMaxC - 2) * M * LuP * sizeof(unsigned short);
+               (size_t)(nlayers > 0 ? nlayers : 0) * M * LuP * sizeof(unsigned short);
   off = (off + 15) & ~(size_t)15;
   B.tputS = reinterpret_cast<double*>(smem + off);
   (void)Lu;
@@ -105,19 +108,21 @@ __device__ inline void dp_setup_lattice(DpShared& sh) {
   }
   __syncthreads();
   for (int rem = tid; rem < M; rem += blockDim.x) {
-    unsigned long long mask = 0ull;
+    unsigned long long mask[2] = {0ull, 0ull};
     for (int u = 0; u <= rem; ++u) {
       bool ok = true;
       for (int c = 0; c < sh.C; ++c) ok &= sh.digits[u][c] <= sh.digits[rem][c];
-      if (ok) mask |= 1ull << u;
+      if (ok) mask[u >> 6] |= 1ull << (u & 63);
     }
-    sh.contain[rem] = mask;
+    sh.contain[rem][0] = mask[0];
+    sh.contain[rem][1] = mask[1];
   }
   if (tid < kMaxC + 2) {
-    unsigned long long mask = 0ull;
+    unsigned long long mask[2] = {0ull, 0ull};
     for (int u = 0; u < M; ++u)
-      if (sh.sizes[u] <= tid) mask |= 1ull << u;
-    sh.size_le[tid] = mask;
+      if (sh.sizes[u] <= tid) mask[u >> 6] |= 1ull << (u & 63);
+    sh.size_le[tid][0] = mask[0];
+    sh.size_le[tid][1] = mask[1];
   }
   if (tid == 0) {
     for (int s = 0; s <= kMaxC; ++s) sh.nbysize[s] = 0;
@@ -229,29 +234,31 @@ __device__ inline void dp_run(DpShared& sh, const DpBuffers& B, int S) {
     for (int s = smaxsz; s >= smin; --s) {
       const int nrem = sh.nbysize[s];
       const int ntasks = nrem * nchunks;
-      const unsigned long long umask = sh.size_le[s - (sg - 1)] & ~1ull;
+      const unsigned long long umask0 = sh.size_le[s - (sg - 1)][0] & ~1ull, umask1 = sh.size_le[s - (sg - 1)][1];
       for (int t = warp; t < ntasks; t += nwarps) {
         const int ri = t / nchunks;
         const int rem = sh.bysize[s][ri];
         const int l = sg + (t - ri * nchunks) * 32 + lane;
         const bool act = l <= lmax;
         const int jmax = l - (sg - 1);
-        unsigned long long mask = sh.contain[rem] & umask;
         double best = kNegInf;
         int bu = 0, bj = 0;
-        while (mask) {
-          const int u = __ffsll((long long)mask) - 1;
-          mask &= mask - 1;
-          if (act) {
-            double cand;
-            int cj;
-            dp_pair(B.value + u * LuP, fprev + (rem - u) * LuP, l, jmax, mono, cand, cj);
-            if (cand > best) { best = cand; bu = u; bj = cj; }
+        for (int w = 0; w < 2; ++w) {  // u ascending over the 128-bit sub-multiset mask
+          unsigned long long mask = sh.contain[rem][w] & (w ? umask1 : umask0);
+          while (mask) {
+            const int u = (w << 6) + __ffsll((long long)mask) - 1;
+            mask &= mask - 1;
+            if (act) {
+              double cand;
+              int cj;
+              dp_pair(B.value + u * LuP, fprev + (rem - u) * LuP, l, jmax, mono, cand, cj);
+              if (cand > best) { best = cand; bu = u; bj = cj; }
+            }
           }
         }
         if (act) {
           B.f[rem * LuP + l] = best;
-          chl[rem * LuP + l] = (unsigned short)((bu << 10) | bj);
+          chl[rem * LuP + l] = (unsigned short)((bu << 8) | bj);
         }
       }
       __syncthreads();
@@ -297,7 +304,7 @@ __device__ inline void dp_decode(DpShared& sh, const DpBuffers& B, int S) {
       u = sh.top_u; j = sh.top_j;
     } else {
       const unsigned short c = B.ch[(size_t)(sg - 2) * M * LuP + rem * LuP + l];
-      u = c >> 10; j = c & 1023;
+      u = c >> 8; j = c & 255;
     }
     sh.stage_j[s] = j;
     sh.stage_u[s] = u;

@@ -276,7 +276,7 @@ def sweep(configs, models, slos, caps_list, prices, regions=None, ctx=None, phas
     the problem is solved once at the widest caps and every entry is a device-side
     filter. Rows mirror the reference CSV:
     (n_max, rho, templates, gen_seconds, best_tokens_per_usd_h); gen_seconds is the
-    shared solve + sweep wall time. Caps must stay within the GPU envelope (n_max <= 6).
+    shared solve + sweep wall time. Caps must stay within the GPU envelope (n_max <= 7).
     """
     import time
 

@@ -51,7 +51,10 @@ def placement_search_batch(cases):
     for i, (cnt, _, S) in enumerate(cases):
         C = len(cnt)
         S = int(S)
-        out.append((float(best[i]), sj[i, :S].copy(), sc[i, :S, :C].copy()))
+        if S > _native.MAX_NODES:  # more stages than any multiset has nodes: all zeros
+            out.append((float(best[i]), np.zeros(S, dtype=np.int64), np.zeros((S, C), dtype=np.int64)))
+        else:
+            out.append((float(best[i]), sj[i, :S].copy(), sc[i, :S, :C].copy()))
     return out
 
 

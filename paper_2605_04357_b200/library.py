@@ -460,8 +460,8 @@ def throughput_table(configs, model, slo, phase, S, ctx) -> np.ndarray:
     lsteps = model.num_layers // g
     if S < 1:
         raise DomainError("S must be >= 1")
-    if S > min(6, model.num_layers):
-        raise DomainError("GPU T-hat tables cover S <= min(6, num_layers)")
+    if S > min(_native.MAX_NODES, model.num_layers):
+        raise DomainError(f"GPU T-hat tables cover S <= min({_native.MAX_NODES}, num_layers)")
     with _native.lease() as h:
         _tables_for(h, configs, model, slo, phase, S, ctx)
         tab, offs, ls = h.get_tables()
@@ -472,8 +472,8 @@ def throughput_table(configs, model, slo, phase, S, ctx) -> np.ndarray:
 
 def stage_budget_s(model, slo, phase, S, ctx) -> float:
     """Per-stage latency budget (templates.py:68-80), evaluated on the GPU."""
-    if not 1 <= S <= min(6, model.num_layers):
-        raise DomainError("GPU stage budgets cover 1 <= S <= min(6, num_layers)")
+    if not 1 <= S <= min(_native.MAX_NODES, model.num_layers):
+        raise DomainError(f"GPU stage budgets cover 1 <= S <= min({_native.MAX_NODES}, num_layers)")
     cfg = NodeConfig(GpuSpec("probe", 1.0, 1.0, 1.0, 1.0), 1)
     with _native.lease() as h:
         _tables_for(h, [cfg], model, slo, phase, S, ctx)

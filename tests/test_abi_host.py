@@ -118,7 +118,7 @@ def test_native_materialise_matches_python_twin():
     keys[n // 2:] = keys[: n - n // 2]
     items["combo_key"] = np.array(keys, dtype=np.uint64)
     items["mp"][n // 2:] = items["mp"][: n - n // 2]
-    nn = np.array([sum(((k >> (9 * t)) & 7) for t in range(6)) for k in keys])
+    nn = np.array([sum(((k >> (9 * t)) & 7) for t in range(_native.MAX_NODES)) for k in keys])
     items["rec"]["num_nodes"] = nn
     items["rec"]["num_stages"] = np.minimum(nn, 2)
     items["rec"]["layers_per_stage"][:, 0] = 30

@@ -257,7 +257,7 @@ def test_errors():
     with pytest.raises(DomainError):
         LibraryCaps(0, 2.0)
     with pytest.raises(DomainError):
-        build_library(configs, models, slos, LibraryCaps(7, 12.0), ctx)
+        build_library(configs, models, slos, LibraryCaps(8, 12.0), ctx)
     huge = ModelSpec("huge", 32, 5000.0, 5000.0, 4096)
     with pytest.raises(LibraryGenError):
         build_library(configs, [huge], {"huge": SloSpec(1500, 80)}, caps, ctx)

@@ -107,8 +107,9 @@ def test_c5_frontier_equals_host_skyline_of_all_device_records(c5):
 
 
 def _tokens(key):
-    for t in range(6):
-        tok = (key >> (9 * (5 - t))) & 511
+    from paper_2605_04357_b200._native import MAX_NODES
+    for t in range(MAX_NODES):
+        tok = (key >> (9 * (MAX_NODES - 1 - t))) & 511
         if not tok:
             break
         yield (tok >> 3) - 1, tok & 7

@@ -175,13 +175,13 @@ def test_live_problems_keep_their_own_device_state(tmp_path):
     assert hashlib.sha256(open(path, "rb").read()).hexdigest() == ref["sha256"]
 
 
-def test_placement_search_beyond_six_nodes_is_rejected():
-    """more than 6 nodes would overrun the DP's per-size tables; the GPU
-    operator raises DomainError instead (reference accepts them on the CPU)."""
+def test_placement_search_beyond_seven_nodes_is_rejected():
+    """more nodes than the envelope (7) would overrun the DP's per-size
+    tables; the GPU operator raises DomainError instead (the reference accepts them)."""
     with pytest.raises(DomainError):
-        placement_search(np.array([7]), np.ones((1, 8)), 2)
+        placement_search(np.array([8]), np.ones((1, 8)), 2)
     with pytest.raises(DomainError):
-        placement_search(np.array([4, 3]), np.ones((2, 8)), 7)
+        placement_search(np.array([4, 4]), np.ones((2, 8)), 7)
     # S above the node count stays the reference's infeasible answer (kernels.py:174-175)
     best, sj, sc = placement_search(np.array([2, 1]), np.ones((2, 8)), 5)
     assert best == -1e300

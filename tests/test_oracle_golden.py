@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
+from paper_2605_04357_b200._native import MAX_NODES
 from tests.helpers import (cfg_by_rank, digest, golden, key_str, oracle_library_lines,
                            oracle_problem, workload)
 
@@ -198,7 +199,7 @@ def test_library_big_sample(w):
         toks = combo.split("+")
         for name, n in (t.rsplit("*", 1) for t in toks):
             key = (key << 9) | ((rank_of[name] + 1) << 3) | int(n)
-        key <<= 9 * (6 - len(toks))
+        key <<= 9 * (MAX_NODES - len(toks))
         by_mp.setdefault((model, phase), []).append((key, ln))
     from tests.helpers import record_line
     checked = 0
