@@ -594,6 +594,7 @@ struct TopArgs {
   long long ncombo;
   unsigned smask;                   // S values of this chain
   unsigned xmask;                   // S values whose rows are exactly monotone
+  unsigned long long nonmono[8];    // per S: configs whose row fails kernels.py:291
   int K, Lu, g;
   const double* tab_mp;             // [S][K][Lu]
   LatWork W;
@@ -639,7 +640,7 @@ __device__ __forceinline__ void top_pair(const double* __restrict__ gv, const do
 
 // kSlots code slots per lane (codes lane + 1 + 32k): 2 for candidates of <= 6 nodes
 // (M <= 64), 4 when a model has 7-node candidates (M <= 128).
-template <int kSlots>
+template <int kSlots, bool kScan>
 __global__ void __launch_bounds__(256, 5) lat_top_kernel(TopArgs A) {
   const int lane = threadIdx.x & 31;
   const long long ci = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -647,7 +648,8 @@ __global__ void __launch_bounds__(256, 5) lat_top_kernel(TopArgs A) {
   int cfg[kMaxC], cnt[kMaxC];
   const int C = lat_tokens(A.inv_rank, A.keys[ci], cfg, cnt);
   int M = 1, n = 0;
-  for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; }
+  unsigned long long cmask = 0ull;  // the candidate's configs
+  for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; cmask |= 1ull << cfg[c]; }
   const int Lu = A.Lu, LuP = lat_pitch(Lu);
   const int Smax = min(n, Lu);
   // this lane's u codes (lane+1, lane+33): size, idx(u), idx(full-u) from the model's
@@ -670,13 +672,14 @@ __global__ void __launch_bounds__(256, 5) lat_top_kernel(TopArgs A) {
   // S ascending; strict improvement (templates.py:322) -> smaller S on ties
   double tbest = kNegInf;
   int twin = 0, tcode = 0, tj = 0, npairs = 0;
-  if ((A.smask & 2u) && Smax >= 1) {  // S = 1: f[1][L][full] = value[full][L]
+  if ((A.smask & 2u) && Smax >= 1 && !kScan) {  // S = 1: f[1][L][full] = value[full][L]
     double v = 0.0;
     for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], A.tab_mp[cfg[c] * Lu + (Lu - 1)]));
     if (v > 1e-9) { tbest = v; twin = 1; }
   }
   for (int S = 2; S <= Smax; ++S) {
     if (!((A.smask >> S) & 1u)) continue;
+    if (((cmask & A.nonmono[S]) != 0ull) != kScan) continue;  // the other pass's candidates at S
     const double* val = A.W.val(S);
     const double* lay = A.W.lay(S, S - 1);
     const double* vsum = A.W.vs(S);
@@ -696,9 +699,13 @@ __global__ void __launch_bounds__(256, 5) lat_top_kernel(TopArgs A) {
       // S > 2:  h(j) = f_S[S-1][Y][Lu - j]: h(1) = f[Lu-1] (.z), h(jmax) = f[S-1] (.y)
       double cand;
       int cj;
-      // only values above the best earlier S (and 1e-9) can matter (templates.py:322)
-      top_pair(val + (size_t)iu[k] * LuP, lay + (size_t)iy[k] * LuP, gs.y, gs.z, S == 2 ? hs.w : hs.z, hs.y,
-               __double2loint(gs.x), __double2loint(hs.x), Lu, jmax, cap, tbest > 1e-9 ? tbest : 1e-9, cand, cj);
+      if (kScan) {  // kernels.py:240-249 full scan (no bound: rows are not monotone)
+        dp_pair(val + (size_t)iu[k] * LuP, lay + (size_t)iy[k] * LuP, Lu, jmax, false, cand, cj);
+      } else {
+        // only values above the best earlier S (and 1e-9) can matter (templates.py:322)
+        top_pair(val + (size_t)iu[k] * LuP, lay + (size_t)iy[k] * LuP, gs.y, gs.z, S == 2 ? hs.w : hs.z, hs.y,
+                 __double2loint(gs.x), __double2loint(hs.x), Lu, jmax, cap, tbest > 1e-9 ? tbest : 1e-9, cand, cj);
+      }
       ++npairs;
       if (cand > best) { best = cand; bu = lane + 1 + 32 * k; bj = cj; }
     }
@@ -2245,32 +2252,21 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
 
 // One (model, phase) chain on stream `slot`: lattice for every monotone S of the
 // chain, the exact per-candidate kernel for the others.
-static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss, int slot,
-                         const unsigned* ranks) {
+// One lattice pass of a (model, phase) chain over the S values in smask: value tables,
+// DP layers, top cells, decode. scan = the reference's full-scan variant (kernels.py:
+// 240-249) for the candidates whose rows fail the monotone test at S; otherwise the
+// binary-search crossing (kernels.py:210-239) for the candidates whose rows pass it.
+static int lattice_pass(coral_s1_handle* h, int mp, int slot, const unsigned* ranks, unsigned smask,
+                        unsigned xmask, bool scan, const unsigned long long* nonmono) {
   cudaStream_t st = h->side[slot];
   const int m = mp / h->NP;
   const int K = h->K, Lu = h->Lu[m];
   const long long ns = h->lat_states, LuP = lat_pitch(h->maxLu);
   const long long ncombo = h->counts[m];
-  if (!ncombo) return 0;
   LatModel L{K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
-  unsigned smask = 0, xmask = 0;
   int Smax = 0;
-  for (int S : Ss) {
-    bool mono = true;  // kernels.py:291 over every config row at (mp, S)
-    for (int c = 0; c < K; ++c) mono &= (h->flags_h[((size_t)mp * h->n_max + (S - 1)) * K + c] & 1) != 0;
-    if (!mono || !h->lat_ok) {  // exact per-candidate kernel for this S
-      int rc = launch_percombo(h, st, h->cand_off[mp], h->cand_off[mp + 1], 1, S, S);
-      if (rc) return rc;
-      continue;
-    }
-    smask |= 1u << S;
-    Smax = std::max(Smax, S);
-    bool exact = true;  // bit 1 of the row flags: all diffs <= 0
-    for (int c = 0; c < K; ++c) exact &= (h->flags_h[((size_t)mp * h->n_max + (S - 1)) * K + c] & 2) != 0;
-    if (exact) xmask |= 1u << S;
-  }
-  if (!smask) return 0;
+  for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
+    if ((smask >> S) & 1u) Smax = S;
   LatWork W;
   W.value = h->ws_value[slot].as<double>();
   W.f = h->ws_f0[slot].as<double>();
@@ -2284,7 +2280,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
     W.sstride = ns * 4;
   }
   const double* tab_mp = h->tab.as<double>() + h->tab_off[mp];
-  if (Smax >= 2 && ns > 0) {
+  if (Smax >= 2 && ns > 0 && !scan) {  // value tables do not depend on the variant
     const int ti = timed_begin(h, st, 2);
     lat_value_kernel<<<dim3((unsigned)((ns * 32 + 255) / 256), Smax - 1), 256, 0, st>>>(
         L, h->dp.inv_rank, h->lat_key.as<unsigned long long>(), h->lat_maxn.as<unsigned>() + (size_t)m * ns,
@@ -2298,14 +2294,17 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
     const int ti = timed_begin(h, st, 1);
     const dim3 lgrid((unsigned)((nst * 32 + 255) / 256), Smax - sg);
     unsigned long long* cen = h->census_on ? h->census.as<unsigned long long>() : nullptr;
-    if (h->n_max >= 7)  // states of 6 configs: up to 63 sub-multiset codes
-      lat_layer_kernel<2><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu,
-                                                 h->lat_maxn.as<unsigned>() + (size_t)m * ns,
-                                                 h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), W, cen);
-    else
-      lat_layer_kernel<1><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu,
-                                                 h->lat_maxn.as<unsigned>() + (size_t)m * ns,
-                                                 h->lat_off.as<long long>(), h->lat_sub.as<uint2>(), W, cen);
+    const unsigned* maxn = h->lat_maxn.as<unsigned>() + (size_t)m * ns;
+    const long long* off = h->lat_off.as<long long>();
+    const uint2* sub = h->lat_sub.as<uint2>();
+    // states of 6 configs (n_max = 7): up to 63 sub-multiset codes -> 2 slots per lane
+    if (h->n_max >= 7) {
+      if (scan) lat_layer_kernel<2, true><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu, maxn, off, sub, W, cen);
+      else lat_layer_kernel<2, false><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu, maxn, off, sub, W, cen);
+    } else {
+      if (scan) lat_layer_kernel<1, true><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu, maxn, off, sub, W, cen);
+      else lat_layer_kernel<1, false><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu, maxn, off, sub, W, cen);
+    }
     timed_end(h, st, ti);
     LAUNCH_CHECK(h);
   }
@@ -2316,6 +2315,7 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   T.ncombo = ncombo;
   T.smask = smask;
   T.xmask = xmask;
+  for (int S = 0; S < 8; ++S) T.nonmono[S] = nonmono[S];
   T.K = K;
   T.Lu = Lu;
   T.g = h->g[m];
@@ -2329,10 +2329,14 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   T.ranks = ranks;
   T.census = h->census_on ? h->census.as<unsigned long long>() : nullptr;
   const int ti = timed_begin(h, st, 0);
-  if (h->n_max >= 7)
-    lat_top_kernel<4><<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
-  else
-    lat_top_kernel<2><<<(unsigned)((ncombo * 32 + 255) / 256), 256, 0, st>>>(T);
+  const unsigned tg = (unsigned)((ncombo * 32 + 255) / 256);
+  if (h->n_max >= 7) {
+    if (scan) lat_top_kernel<4, true><<<tg, 256, 0, st>>>(T);
+    else lat_top_kernel<4, false><<<tg, 256, 0, st>>>(T);
+  } else {
+    if (scan) lat_top_kernel<2, true><<<tg, 256, 0, st>>>(T);
+    else lat_top_kernel<2, false><<<tg, 256, 0, st>>>(T);
+  }
   timed_end(h, st, ti);
   LAUNCH_CHECK(h);
   const int td = timed_begin(h, st, 3);
@@ -2340,6 +2344,40 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
   timed_end(h, st, td);
   LAUNCH_CHECK(h);
   return 0;
+}
+
+// One (model, phase) chain on stream `slot`. Each candidate's DP mode at S follows its
+// own rows (kernels.py:291: np.all(np.diff(tput) <= 1e-12) over the combo's configs):
+// pass A runs the search variant for the candidates that pass the test, pass B the
+// full-scan variant (only for the S values where some config row fails it) for the
+// others. Without lattice tables (memory) every S takes the exact per-candidate kernel.
+static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss, int slot,
+                         const unsigned* ranks) {
+  const int m = mp / h->NP;
+  const int K = h->K;
+  if (!h->counts[m]) return 0;
+  unsigned smask = 0, xmask = 0, scanmask = 0;
+  unsigned long long nonmono[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int S : Ss) {
+    if (!h->lat_ok) {  // exact per-candidate kernel for this S
+      int rc = launch_percombo(h, h->side[slot], h->cand_off[mp], h->cand_off[mp + 1], 1, S, S);
+      if (rc) return rc;
+      continue;
+    }
+    smask |= 1u << S;
+    bool exact = true;  // bit 1 of the row flags: all diffs <= 0
+    for (int c = 0; c < K; ++c) {
+      const unsigned char f = h->flags_h[((size_t)mp * h->n_max + (S - 1)) * K + c];
+      exact &= (f & 2) != 0;
+      if (!(f & 1)) nonmono[S] |= 1ull << c;
+    }
+    if (exact) xmask |= 1u << S;
+    if (nonmono[S] && S >= 2) scanmask |= 1u << S;
+  }
+  if (!smask) return 0;
+  int rc = lattice_pass(h, mp, slot, ranks, smask, xmask, false, nonmono);
+  if (!rc && scanmask) rc = lattice_pass(h, mp, slot, ranks, scanmask, 0u, true, nonmono);
+  return rc;
 }
 
 // Evaluate the (mp, S) units selected by `take(mp, S)`.

@@ -349,8 +349,9 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
 // DP layer sg for every S in [S_lo, S_lo + gridDim.y) with S > sg: warp per state X,
 // lanes over l. Cells: sg <= |X| <= maxn(X) - (S - sg), sg <= l <= Lu - (S - sg).
 // kSlots = ceil((M(X) - 1) / 32) code slots per lane: 1 while n_max <= 6 (|X| <= 5),
-// 2 for n_max = 7 (|X| <= 6, M(X) <= 64).
-template <int kSlots>
+// 2 for n_max = 7 (|X| <= 6, M(X) <= 64). scan: the full-scan variant (rows that fail
+// the monotone test, kernels.py:240-249; xmask is then 0).
+template <int kSlots, bool kScan>
 __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
     LatModel L, int sg, int S_lo, unsigned smask, unsigned xmask, int n_max, int Lu,
     const unsigned* __restrict__ maxn, const long long* __restrict__ off,
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
       if (!act || kk >= nv) continue;
       double cand;
       int cj;
-      dp_pair(value + vo, fprev + fo, l, jmax, true, cand, cj, cap);
+      dp_pair(value + vo, fprev + fo, l, jmax, !kScan, cand, cj, cap);  // scan: kernels.py:240-249
       if (cand > best) { best = cand; bu = code; bj = cj; }
     }
     // merge the groups of each l: value desc, then smallest code (the reference's

@@ -142,3 +142,21 @@ def milp_digest(milp) -> dict:
         "first_vars": [f"{v.vid}|{v.kind}|{v.ub!r}" for v in list(milp.variables.values())[:40]],
         "first_cons": [f"{c.name}|{c.sense}|{c.rhs!r}|{len(c.coeffs)}" for c in milp.constraints[:40]],
     }
+
+
+def zigzag_profile(configs, models, table_cls, names=("1xL4", "2xA10G")):
+    """A ProfileTable (perf.py:94-141) that breaks the T-hat monotonicity test of
+    kernels.py:291 for two node configs: for every model, phase and layer count j a
+    zigzag throughput (odd layer units 30% faster than their even neighbours), any
+    budget (bucket -1). Combos with these configs take the reference's full-scan DP
+    (kernels.py:240-249); the rest keep the binary-search crossing."""
+    prof = table_cls()
+    for c in configs:
+        if c.name not in names:
+            continue
+        for m in models:
+            for ph in ("prefill", "decode"):
+                base = (4.0e5 if ph == "prefill" else 6.0e4) * c.gpu_count * c.gpu.tflops / (312.0 * m.params_active_b)
+                for j in range(1, m.num_layers + 1):
+                    prof.add(c.name, m.name, ph, j, -1, base / j * (1.3 if j % 2 else 1.0))
+    return prof

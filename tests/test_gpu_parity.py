@@ -489,3 +489,42 @@ def test_lattice_workspace_beyond_device_memory(streams, monkeypatch):
         assert not layers  # no lattice: per-candidate kernel only
     else:
         assert layers and set(layers) <= set(range(streams))
+
+
+@pytest.mark.parametrize("w", ["core", "extended"])
+def test_non_monotone_profile_rows_stay_on_the_lattice(w):
+    """ProfileTable overrides that break kernels.py:291's monotone test for two configs
+    (tests/helpers.zigzag_profile): the candidates containing them take the reference's
+    full-scan DP (kernels.py:240-249), the others the binary-search crossing, both on the
+    lattice (scan variant + search variant; no per-candidate kernel). The whole library
+    is identical to the unmodified reference's (golden profile_<w>.json.gz)."""
+    import time
+    from paper_2605_04357_b200.specs import ProfileTable
+    from tests.helpers import zigzag_profile
+    try:
+        g = golden(f"profile_{w}.json.gz")
+    except FileNotFoundError:
+        pytest.skip(f"profile_{w} golden not generated")
+    configs, models, slos, caps, ctx, regions, prices = workload(w)
+    ctxp = GenContext(perf=ctx.perf, profile=zigzag_profile(configs, models, ProfileTable))
+    prob = Stage1Problem(configs, models, slos, caps, ctxp)
+    prob.run()
+    t0 = time.perf_counter()
+    prob.run()
+    import torch
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    kinds = {k for k, _, _, _ in prob.h.kernel_timeline()}
+    assert 0 in kinds and 1 in kinds  # top cells and layers ran on the lattice
+    cbr = prob.cfg_by_rank
+    lines = []
+    order = sorted(range(len(models) * 2), key=lambda mp: (models[mp // 2].name, ("prefill", "decode")[mp % 2]))
+    for mp in order:
+        keys, recs = prob.keys(mp // 2), prob.records(mp)
+        for k, r in zip(keys, recs):
+            if r["num_stages"] > 0:
+                lines.append(record_line(models[mp // 2].name, ("prefill", "decode")[mp % 2], k, r, cbr))
+    assert len(lines) == g["count"]
+    assert lines[::g["sample_every"]] == g["sample"]
+    assert digest(lines) == g["sha256"]
+    print(f"{w} with non-monotone profile rows: {len(lines)} templates, solve {1e3 * dt:.2f} ms")
