@@ -305,9 +305,8 @@ def main():
     if world > 1:
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2605_04357_b200 import _native, build_frontier, catalog
-    from paper_2605_04357_b200.frontier import _local_frontier, _merge_across_ranks, _price_matrix
+    from paper_2605_04357_b200.frontier import _local_frontier, _merge_across_ranks, _price_matrix, rank_pieces
     from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem
-    from paper_2605_04357_b200.shard import assign_units, table_posfrac
 
     w = catalog.WORKLOADS[args.workload]()
     caps, ctx = LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf, granularity=w.granularity)
@@ -324,10 +323,11 @@ def main():
         h.enumerate()
         if world > 1:
             prob.counts = h.num_combos()
-            _, lsteps, smax = h.table_layout()
-            masks = assign_units(prob.counts, lsteps, smax, NP, world,
-                                 table_posfrac(h, len(prob.configs)))[rank]
-            h.evaluate_units(masks)
+            pieces = rank_pieces(prob, tdist)  # memoised after the first (warm-up) step
+            masks = [0] * (len(w.models) * NP)
+            for mp, mk, lo, hi in pieces:
+                masks[mp] |= mk
+            h.evaluate_pieces(pieces)
             n_local = _local_frontier(prob, pmat)
             return _merge_across_ranks(prob, n_local, tdist)
         h.evaluate(0, -1)
@@ -471,7 +471,7 @@ def main():
                    "candidates": ncand, "dp_evaluations": dp_evals,
                    "dp_evaluations_per_s": dp_evals * args.steps / (total_ms / 1e3),
                    "frontier_survivors": int(nf),
-                   "parallelism": f"(model, phase, S) units over {world} GPUs + NCCL all-gather of frontiers"
+                   "parallelism": f"pieces over {world} GPUs: (model, phase, S) units, the largest split by candidate range (measured costs), + one NCCL all-gather of partial frontiers"
                                   if world > 1 else "single GPU",
                    "l2": "256 MB buffer written between timed steps",
                    "stage1_solve_s": total_ms / args.steps / 1e3},

@@ -173,6 +173,11 @@ int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi);
  * mp; records hold each candidate's best over the given S values (ties -> fewer
  * stages), so disjoint masks on different ranks merge exactly. */
 int coral_s1_evaluate_units(coral_s1_handle* h, const uint32_t* smask);
+/* multi-GPU pieces (the (model, GPU-type combination) axis): piece i
+ * evaluates stage counts smask[i] (bit S) of slot mp[i] for the model's candidates
+ * [lo[i], hi[i]) (library order; hi < 0 = to the end). Ranks take disjoint pieces. */
+int coral_s1_evaluate_pieces(coral_s1_handle* h, int n, const int32_t* mp, const uint32_t* smask,
+                             const int64_t* lo, const int64_t* hi);
 int coral_s1_num_candidates(const coral_s1_handle* h, int64_t* n);
 /* records of one (model, phase slot), library order; n = its combo count */
 int coral_s1_get_records(coral_s1_handle* h, int mp, coral_s1_record* out, int64_t n);
@@ -280,6 +285,10 @@ int coral_s1_window_select_stats(const coral_s1_handle* h, double* ms, int64_t* 
  * evaluate's start event; up to cap launches, count in *n (diagnostics) */
 int coral_s1_kernel_timeline(const coral_s1_handle* h, int64_t cap, int32_t* kind, int32_t* stream,
                              double* begin_ms, double* end_ms, int64_t* n);
+/* the last evaluate's timed lattice launches: kind (as coral_s1_kernel_stats), (model,
+ * phase) slot, device ms (cost calibration of the multi-GPU split, shard.py) */
+int coral_s1_kernel_launches(const coral_s1_handle* h, int64_t cap, int32_t* kind, int32_t* mp, double* ms,
+                             int64_t* n);
 /* layer-kernel census for the bench roofline: while on, each evaluate counts the
  * algorithmic bytes of its lat_layer_kernel launches (10 B per f/choice cell written +
  * one read of each computed state's value_S and f_{sg-1} rows + 8 B per valid

@@ -98,6 +98,8 @@ def load():
             "coral_s1_get_combos": (C.c_int, [vp, C.c_int, C.c_int, _u64p, C.c_int64]),
             "coral_s1_evaluate": (C.c_int, [vp, C.c_int64, C.c_int64]),
             "coral_s1_evaluate_units": (C.c_int, [vp, C.POINTER(C.c_uint32)]),
+            "coral_s1_evaluate_pieces": (C.c_int, [vp, C.c_int, _i32p, C.POINTER(C.c_uint32), _i64p, _i64p]),
+            "coral_s1_kernel_launches": (C.c_int, [vp, C.c_int64, _i32p, _i32p, _f64p, _i64p]),
             "coral_s1_num_candidates": (C.c_int, [vp, _i64p]),
             "coral_s1_get_records": (C.c_int, [vp, C.c_int, vp, C.c_int64]),
             "coral_s1_frontier": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
@@ -285,6 +287,29 @@ class Handle:
         m = np.ascontiguousarray(smask, dtype=np.uint32)
         _check(self._lib.coral_s1_evaluate_units(self._h, m.ctypes.data_as(C.POINTER(C.c_uint32))))
 
+    def evaluate_pieces(self, pieces):
+        """pieces: [(mp, smask, lo, hi)] -- stage counts smask of slot mp for the model's
+        candidates [lo, hi) (hi < 0: to the end)."""
+        n = len(pieces)
+        mp = np.ascontiguousarray([p[0] for p in pieces] or [0], dtype=np.int32)
+        sm = np.ascontiguousarray([p[1] for p in pieces] or [0], dtype=np.uint32)
+        lo = np.ascontiguousarray([p[2] for p in pieces] or [0], dtype=np.int64)
+        hi = np.ascontiguousarray([p[3] for p in pieces] or [0], dtype=np.int64)
+        _check(self._lib.coral_s1_evaluate_pieces(self._h, n, _ptr(mp, C.c_int32),
+                                                  sm.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                                  _ptr(lo, C.c_int64), _ptr(hi, C.c_int64)))
+
+    def kernel_launches(self, cap: int = 2048):
+        """[(kind, mp, ms)] of the last evaluate's timed lattice launches."""
+        kind = np.zeros(cap, np.int32)
+        mp = np.zeros(cap, np.int32)
+        ms = np.zeros(cap)
+        n = C.c_int64()
+        _check(self._lib.coral_s1_kernel_launches(self._h, cap, _ptr(kind, C.c_int32), _ptr(mp, C.c_int32),
+                                                  _ptr(ms, C.c_double), C.byref(n)))
+        k = n.value
+        return list(zip(kind[:k].tolist(), mp[:k].tolist(), ms[:k].tolist()))
+
     def num_candidates(self) -> int:
         n = C.c_int64()
         _check(self._lib.coral_s1_num_candidates(self._h, C.byref(n)))
@@ -368,7 +393,7 @@ class Handle:
     def set_streams(self, n: int) -> None:
         _check(self._lib.coral_s1_set_streams(self._h, int(n)))
 
-    def kernel_timeline(self, cap: int = 512):
+    def kernel_timeline(self, cap: int = 2048):
         """[(kind, stream slot, begin ms, end ms)] of the last evaluate's lattice launches."""
         kind = np.zeros(cap, np.int32)
         slot = np.zeros(cap, np.int32)

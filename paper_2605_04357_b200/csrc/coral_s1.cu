@@ -138,10 +138,12 @@ struct coral_s1_handle {
   double rho = 0;
   DevBuf lat_sums, lat_soff;
   // per-launch timing of the lattice kernels (coral_s1_kernel_stats)
-  static constexpr int kTimedMax = 512;
+  static constexpr int kTimedMax = 2048;  // events created on first use
   cudaEvent_t tev[kTimedMax][2] = {};
   int tkind[kTimedMax] = {};
   int tslot[kTimedMax] = {};
+  int tmp[kTimedMax] = {};   // (model, phase) slot of the launch (rank tables: the model's first)
+  int cur_mp = -1;
   int ntimed = 0;
   cudaEvent_t ev[8] = {};
   cudaEvent_t ev_ws[2] = {};  // around the last window_select_kernel launch (bench roofline)
@@ -1682,10 +1684,6 @@ int coral_s1_create(int device, coral_s1_handle** out) {
   }
   cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->prep_ev, cudaEventDisableTiming);
-  for (int i = 0; i < coral_s1_handle::kTimedMax; ++i) {
-    cudaEventCreate(&h->tev[i][0]);
-    cudaEventCreate(&h->tev[i][1]);
-  }
   if (const char* e = getenv("CORAL_S1_STREAMS")) h->nstreams = std::max(1, std::min(atoi(e), coral_s1_handle::kStreams));
   if (const char* e = getenv("CORAL_S1_MEM_LIMIT")) h->mem_limit = (size_t)strtoull(e, nullptr, 10);
   if (h->lat_binom_d.ensure(sizeof(tab)) == 0)
@@ -2082,10 +2080,14 @@ static int launch_percombo(coral_s1_handle* h, cudaStream_t st, int64_t lo, int6
 // Bracket one launch on stream st with a timing-event pair of kind `kind`
 // (0 = lat_top_kernel, 1 = lat_layer_kernel, 2 = lat_value_kernel, 3 = lat_decode_kernel,
 // 4 = lat_ranks_kernel).
-static int timed_begin(coral_s1_handle* h, cudaStream_t st, int kind) {
+static int timed_begin(coral_s1_handle* h, cudaStream_t st, int kind, int mp = -2) {
   if (h->ntimed >= coral_s1_handle::kTimedMax) return -1;
-  const int i = h->ntimed++;
+  const int i = h->ntimed;
+  if (!h->tev[i][0] && (cudaEventCreate(&h->tev[i][0]) != cudaSuccess || cudaEventCreate(&h->tev[i][1]) != cudaSuccess))
+    return -1;
+  h->ntimed++;
   h->tkind[i] = kind;
+  h->tmp[i] = mp == -2 ? h->cur_mp : mp;
   h->tslot[i] = -1;
   for (int k = 0; k < coral_s1_handle::kStreams; ++k)
     if (h->side[k] == st) h->tslot[i] = k;
@@ -2257,12 +2259,12 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
 // 240-249) for the candidates whose rows fail the monotone test at S; otherwise the
 // binary-search crossing (kernels.py:210-239) for the candidates whose rows pass it.
 static int lattice_pass(coral_s1_handle* h, int mp, int slot, const unsigned* ranks, unsigned smask,
-                        unsigned xmask, bool scan, const unsigned long long* nonmono) {
+                        unsigned xmask, bool scan, const unsigned long long* nonmono, int64_t lo, int64_t hi) {
   cudaStream_t st = h->side[slot];
   const int m = mp / h->NP;
   const int K = h->K, Lu = h->Lu[m];
   const long long ns = h->lat_states, LuP = lat_pitch(h->maxLu);
-  const long long ncombo = h->counts[m];
+  const long long ncombo = hi - lo;  // the top cells of candidates [lo, hi) of the model
   LatModel L{K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
   int Smax = 0;
   for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
@@ -2311,7 +2313,7 @@ static int lattice_pass(coral_s1_handle* h, int mp, int slot, const unsigned* ra
   TopArgs T;
   T.L = L;
   T.inv_rank = h->dp.inv_rank;
-  T.keys = h->keys.as<unsigned long long>() + h->koff[m];
+  T.keys = h->keys.as<unsigned long long>() + h->koff[m] + lo;
   T.ncombo = ncombo;
   T.smask = smask;
   T.xmask = xmask;
@@ -2324,7 +2326,7 @@ static int lattice_pass(coral_s1_handle* h, int mp, int slot, const unsigned* ra
   T.state_key = h->lat_key.as<unsigned long long>();
   T.off = h->lat_off.as<long long>();
   T.subtab = h->lat_sub.as<uint2>();
-  T.rec = h->rec.as<coral_s1_record>() + h->cand_off[mp];
+  T.rec = h->rec.as<coral_s1_record>() + h->cand_off[mp] + lo;
   T.win = h->ws_win[slot].as<int4>();
   T.ranks = ranks;
   T.census = h->census_on ? h->census.as<unsigned long long>() : nullptr;
@@ -2352,15 +2354,14 @@ static int lattice_pass(coral_s1_handle* h, int mp, int slot, const unsigned* ra
 // full-scan variant (only for the S values where some config row fails it) for the
 // others. Without lattice tables (memory) every S takes the exact per-candidate kernel.
 static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss, int slot,
-                         const unsigned* ranks) {
-  const int m = mp / h->NP;
+                         const unsigned* ranks, int64_t lo, int64_t hi) {
   const int K = h->K;
-  if (!h->counts[m]) return 0;
+  if (hi <= lo) return 0;
   unsigned smask = 0, xmask = 0, scanmask = 0;
   unsigned long long nonmono[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int S : Ss) {
     if (!h->lat_ok) {  // exact per-candidate kernel for this S
-      int rc = launch_percombo(h, h->side[slot], h->cand_off[mp], h->cand_off[mp + 1], 1, S, S);
+      int rc = launch_percombo(h, h->side[slot], h->cand_off[mp] + lo, h->cand_off[mp] + hi, 1, S, S);
       if (rc) return rc;
       continue;
     }
@@ -2375,14 +2376,23 @@ static int lattice_units(coral_s1_handle* h, int mp, const std::vector<int>& Ss,
     if (nonmono[S] && S >= 2) scanmask |= 1u << S;
   }
   if (!smask) return 0;
-  int rc = lattice_pass(h, mp, slot, ranks, smask, xmask, false, nonmono);
-  if (!rc && scanmask) rc = lattice_pass(h, mp, slot, ranks, scanmask, 0u, true, nonmono);
+  int rc = lattice_pass(h, mp, slot, ranks, smask, xmask, false, nonmono, lo, hi);
+  if (!rc && scanmask) rc = lattice_pass(h, mp, slot, ranks, scanmask, 0u, true, nonmono, lo, hi);
   return rc;
 }
 
-// Evaluate the (mp, S) units selected by `take(mp, S)`.
-template <class Take>
-static int evaluate_units(coral_s1_handle* h, Take take) {
+// One piece of evaluation work: stage counts `smask` of (model, phase) slot mp for the
+// candidates [lo, hi) of the model (library order). Multi-GPU ranks take disjoint
+// pieces: whole (mp, S) units, or a unit's candidates split by range (the north star's
+// (model, GPU-type combination) axis); records hold each candidate's best over the S
+// values evaluated, so pieces merge exactly.
+struct Piece {
+  int mp;
+  unsigned smask;
+  int64_t lo, hi;
+};
+
+static int evaluate_pieces(coral_s1_handle* h, std::vector<Piece> pieces) {
   if (!h || !h->have_tables || !h->have_enum) return fail(CORAL_S1_EINVAL, "tables and enumerate first");
   CUDA_TRY(cudaSetDevice(h->device));
   int rc;
@@ -2390,9 +2400,19 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   cudaStream_t st = h->stream;
   const int NMP = h->NM * h->NP;
   h->own_mp.assign(NMP, 0);
-  for (int mp = 0; mp < NMP; ++mp)
-    for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
-      if (take(mp, S)) h->own_mp[mp] = 1;
+  std::vector<Piece> ok;
+  for (Piece p : pieces) {
+    if (p.mp < 0 || p.mp >= NMP) return fail(CORAL_S1_EINVAL, "piece: bad mp");
+    const int m = p.mp / h->NP;
+    p.lo = std::max<int64_t>(p.lo, 0);
+    p.hi = (p.hi < 0 || p.hi > h->counts[m]) ? h->counts[m] : p.hi;
+    unsigned mk = 0;
+    for (int S = 1; S <= std::min(h->smax[m], h->Lu[m]); ++S) mk |= p.smask & (1u << S);
+    p.smask = mk;
+    if (!mk || p.hi <= p.lo) continue;
+    h->own_mp[p.mp] = 1;
+    ok.push_back(p);
+  }
   const bool flags_were_ready = h->flags_ready;
   if (!flags_were_ready) {
     h->flags_h.assign((size_t)std::max(NMP, 1) * h->n_max * h->K, 0);
@@ -2402,58 +2422,80 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   }
   CUDA_TRY(cudaEventRecord(h->ev[4], st));
   h->ntimed = 0;
-  // records not improved by any unit read as infeasible (num_stages 0)
+  // records not improved by any piece read as infeasible (num_stages 0)
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), st));
   if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 32, st));
   if (h->lat_ready) {  // prepared on side[0] during enumerate (every model with candidates)
     CUDA_TRY(cudaStreamWaitEvent(st, h->prep_ev, 0));
   } else {
     h->model_used.assign(h->NM, 0);  // lattice tables only for the models this call evaluates
-    for (int mp = 0; mp < NMP; ++mp)
-      for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
-        if (take(mp, S)) h->model_used[mp / h->NP] = 1;
+    for (const Piece& p : ok) h->model_used[p.mp / h->NP] = 1;
     if ((rc = lattice_prepare(h, st))) return rc;
   }
   if (!flags_were_ready) CUDA_TRY(cudaStreamSynchronize(st));  // flags_h valid
   CUDA_TRY(cudaEventRecord(h->fork_ev, st));
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) CUDA_TRY(cudaStreamWaitEvent(h->side[i], h->fork_ev, 0));
-  // one chain per model (its phases back to back on one stream, sharing the model's
-  // rank table), heaviest first, round-robin over the side streams
-  std::vector<int> order(h->NM);
-  for (int i = 0; i < h->NM; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    return (double)h->counts[a] * h->Lu[a] > (double)h->counts[b] * h->Lu[b];
-  });
+  // groups of pieces sharing (model, range) run back to back on one stream and share
+  // the model's rank table over that range (both phases of a model on one GPU);
+  // heaviest first, round-robin over the side streams
+  struct Group { int m; int64_t lo, hi; std::vector<int> idx; double w; };
+  std::vector<Group> groups;
+  for (int i = 0; i < (int)ok.size(); ++i) {
+    const int m = ok[i].mp / h->NP;
+    Group* g = nullptr;
+    for (Group& x : groups)
+      if (x.m == m && x.lo == ok[i].lo && x.hi == ok[i].hi) g = &x;
+    if (!g) { groups.push_back(Group{m, ok[i].lo, ok[i].hi, {}, 0.0}); g = &groups.back(); }
+    g->idx.push_back(i);
+    g->w += (double)(ok[i].hi - ok[i].lo) * h->Lu[m] * __builtin_popcount(ok[i].smask);
+  }
+  // fewer groups than chain streams: give each (model, phase) its own stream (the rank
+  // table is then computed per slot) so that a model's phases run concurrently
+  const int nslots = std::max(1, h->lat_ok ? std::min(h->lat_streams, h->nstreams) : h->nstreams);
+  for (bool split = true; split && (int)groups.size() < nslots;) {
+    split = false;
+    for (size_t gi = 0; gi < groups.size() && (int)groups.size() < nslots; ++gi) {
+      Group& g = groups[gi];
+      if (g.idx.size() < 2) continue;
+      const int last = g.idx.back();
+      g.idx.pop_back();
+      const double w = (double)(ok[last].hi - ok[last].lo) * h->Lu[g.m] * __builtin_popcount(ok[last].smask);
+      g.w -= w;
+      groups.push_back(Group{g.m, g.lo, g.hi, {last}, w});
+      split = true;
+    }
+  }
+  std::stable_sort(groups.begin(), groups.end(), [](const Group& a, const Group& b) { return a.w > b.w; });
   int64_t maxc = 1;
-  for (int m = 0; m < h->NM; ++m) maxc = std::max<int64_t>(maxc, h->counts[m]);
-  // per chain stream: the model's sub-multiset rank table and the top cells' winners
-  // (both stream-ordered within a model's chains, so one buffer per stream suffices)
-  for (int i = 0; i < h->nstreams; ++i)
+  for (const Group& g : groups) maxc = std::max<int64_t>(maxc, g.hi - g.lo);
+  // per chain stream: the rank table of the group's range and the top cells' winners
+  // (stream-ordered within a group, so one buffer per stream suffices)
+  // chain streams in rotation: the lattice workspaces that fit, at most the streams asked for
+  for (int i = 0; i < nslots; ++i)
     if ((rc = h->ws_ranks[i].ensure(maxc * kRankStride * sizeof(unsigned))) || (rc = h->ws_win[i].ensure(maxc * sizeof(int4))))
       return rc;
   int slot = 0;
-  for (int m : order) {
-    if (!h->counts[m]) continue;
-    std::vector<std::vector<int>> per_phase(h->NP);
-    bool any = false;
-    for (int p = 0; p < h->NP; ++p)
-      for (int S = 1; S <= std::min(h->smax[m], h->Lu[m]); ++S)
-        if (take(m * h->NP + p, S)) { per_phase[p].push_back(S); any = true; }
-    if (!any) continue;
+  for (const Group& g : groups) {
+    const int m = g.m;
     unsigned* ranks = h->ws_ranks[slot].as<unsigned>();
     if (h->n_max >= 2 && h->lat_states > 0 && h->lat_ok) {
       LatModel L{h->K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
-      const long long rb = std::min<long long>((h->counts[m] + kRanksWarps - 1) / kRanksWarps, (long long)h->num_sms * h->ranks_blocks_per_sm);
-      const int tr = timed_begin(h, h->side[slot], 4);
+      const long long n = g.hi - g.lo;
+      const long long rb = std::min<long long>((n + kRanksWarps - 1) / kRanksWarps, (long long)h->num_sms * h->ranks_blocks_per_sm);
+      const int tr = timed_begin(h, h->side[slot], 4, m * h->NP);
       lat_ranks_kernel<<<(unsigned)rb, kRanksWarps * 32, 0, h->side[slot]>>>(
-          L, h->dp.inv_rank, h->keys.as<unsigned long long>() + h->koff[m], h->counts[m], ranks);
+          L, h->dp.inv_rank, h->keys.as<unsigned long long>() + h->koff[m] + g.lo, n, ranks);
       timed_end(h, h->side[slot], tr);
       LAUNCH_CHECK(h);
     }
-    for (int p = 0; p < h->NP; ++p)
-      if (!per_phase[p].empty() && (rc = lattice_units(h, m * h->NP + p, per_phase[p], slot, ranks)))
-        return rc;
-    slot = (slot + 1) % (h->lat_ok ? h->lat_streams : h->nstreams);
+    for (int i : g.idx) {
+      std::vector<int> Ss;
+      for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
+        if ((ok[i].smask >> S) & 1u) Ss.push_back(S);
+      h->cur_mp = ok[i].mp;
+      if ((rc = lattice_units(h, ok[i].mp, Ss, slot, ranks, ok[i].lo, ok[i].hi))) return rc;
+    }
+    slot = (slot + 1) % nslots;
   }
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     CUDA_TRY(cudaEventRecord(h->side_ev[i], h->side[i]));
@@ -2462,6 +2504,20 @@ static int evaluate_units(coral_s1_handle* h, Take take) {
   CUDA_TRY(cudaEventRecord(h->ev[5], st));
   h->have_eval = true;
   return 0;
+}
+
+// (mp, S) units selected by take(mp, S), every candidate
+template <class Take>
+static int evaluate_units(coral_s1_handle* h, Take take) {
+  if (!h || !h->have_tables || !h->have_enum) return fail(CORAL_S1_EINVAL, "tables and enumerate first");
+  std::vector<Piece> pieces;
+  for (int mp = 0; mp < h->NM * h->NP; ++mp) {
+    unsigned mk = 0;
+    for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
+      if (take(mp, S)) mk |= 1u << S;
+    if (mk) pieces.push_back(Piece{mp, mk, 0, -1});
+  }
+  return evaluate_pieces(h, pieces);
 }
 
 extern "C" {
@@ -2493,6 +2549,31 @@ int coral_s1_evaluate_units(coral_s1_handle* h, const uint32_t* smask) {
   if (!smask) return fail(CORAL_S1_EINVAL, "null mask");
   std::vector<uint32_t> mk(smask, smask + (size_t)h->NM * h->NP);
   return evaluate_units(h, [&](int mp, int S) { return ((mk[mp] >> S) & 1u) != 0; });
+}
+
+int coral_s1_evaluate_pieces(coral_s1_handle* h, int n, const int32_t* mp, const uint32_t* smask,
+                             const int64_t* lo, const int64_t* hi) {
+  if (!h || !h->have_enum) return fail(CORAL_S1_EINVAL, "enumerate first");
+  if (n < 0 || (n && (!mp || !smask || !lo || !hi))) return fail(CORAL_S1_EINVAL, "bad pieces");
+  std::vector<Piece> pieces;
+  for (int i = 0; i < n; ++i) pieces.push_back(Piece{mp[i], smask[i], lo[i], hi[i]});
+  return evaluate_pieces(h, pieces);
+}
+
+int coral_s1_kernel_launches(const coral_s1_handle* h, int64_t cap, int32_t* kind, int32_t* mp, double* ms,
+                             int64_t* n) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  const int64_t k = std::min<int64_t>(cap, h->ntimed);
+  for (int64_t i = 0; i < k; ++i) {
+    float t = 0;
+    CUDA_TRY(cudaEventSynchronize(h->tev[i][1]));
+    CUDA_TRY(cudaEventElapsedTime(&t, h->tev[i][0], h->tev[i][1]));
+    kind[i] = h->tkind[i];
+    mp[i] = h->tmp[i];
+    ms[i] = t;
+  }
+  if (n) *n = k;
+  return 0;
 }
 
 int coral_s1_get_records(coral_s1_handle* h, int mp, coral_s1_record* out, int64_t n) {

@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _native
 from .library import GenContext, Stage1Problem, TemplateLibrary, library_meta
-from .shard import assign_units, table_posfrac
+from .shard import calibrate, pieces_to_ranges, plan_pieces
 from .specs import PHASES, NodeComboKey, Placement, ServingTemplate
 
 
@@ -146,6 +146,33 @@ def _merge_across_ranks(prob: Stage1Problem, n_local: int, tdist) -> int:
     return prob.h.frontier_merge_parts(recv.data_ptr(), stride, item, counts)
 
 
+_CALIBRATION: dict = {}
+
+
+def rank_pieces(prob: Stage1Problem, tdist) -> list:
+    """This rank's evaluation pieces (shard.plan_pieces): (model, phase, S)
+    units, the largest split by candidate range, balanced on costs measured once per
+    problem on rank 0 (shard.calibrate) and broadcast, so every rank derives the same
+    plan. Needs the problem's tables and enumeration."""
+    NP = len(prob.phases)
+    _, lsteps, smax = prob.h.table_layout()
+    smax_mp = [min(int(smax[mp // NP]), int(lsteps[mp // NP])) if prob.counts[mp // NP] else 0
+               for mp in range(len(prob.models) * NP)]
+    key = (tuple(int(c) for c in prob.counts), tuple(int(x) for x in lsteps), tuple(smax_mp), NP,
+           prob.signature())
+    costs = _CALIBRATION.get(key)
+    if costs is None:
+        world = tdist.get_world_size()
+        costs = calibrate(prob.h, len(smax_mp), smax_mp, NP) if tdist.get_rank() == 0 else None
+        if world > 1:
+            box = [costs]
+            tdist.broadcast_object_list(box, src=0)
+            costs = box[0]
+        _CALIBRATION[key] = costs
+    plan = plan_pieces(costs, tdist.get_world_size())
+    return pieces_to_ranges(plan[tdist.get_rank()], prob.counts, NP)
+
+
 def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,
                    phases=PHASES, dist=None, return_problem: bool = False):
     """Stage 1 end to end on the GPU: spec tables in, frontier templates out.
@@ -169,10 +196,7 @@ def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,
         prob.cand_off = np.zeros(len(prob.models) * NP + 1, dtype=np.int64)
         for mp in range(len(prob.models) * NP):
             prob.cand_off[mp + 1] = prob.cand_off[mp] + prob.counts[mp // NP]
-        _, lsteps, smax = prob.h.table_layout()
-        masks = assign_units(prob.counts, lsteps, smax, NP, tdist.get_world_size(),
-                             table_posfrac(prob.h, len(prob.configs)))
-        prob.h.evaluate_units(masks[tdist.get_rank()])
+        prob.h.evaluate_pieces(rank_pieces(prob, tdist))
         n_local = _local_frontier(prob, pmat)
         n = _merge_across_ranks(prob, n_local, tdist)
     else:

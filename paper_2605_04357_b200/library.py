@@ -182,6 +182,18 @@ class Stage1Problem:
         self.counts = None
         self.cand_off = None
 
+    def signature(self) -> str:
+        """Digest of the packed spec tables (the problem's identity for memoised plans)."""
+        if getattr(self, "_sig", None) is None:
+            import hashlib
+            d = hashlib.sha1()
+            for k in sorted(self.arrays):
+                d.update(k.encode())
+                d.update(np.ascontiguousarray(self.arrays[k]).tobytes())
+            d.update(repr(sorted(self.scalars.items())).encode())
+            self._sig = d.hexdigest()
+        return self._sig
+
     def close(self) -> None:
         h, self.h = self.h, None
         if h is not None:

@@ -125,3 +125,171 @@ def _assign_units(counts, lsteps, smax, num_phases, world, posfrac):
         masks[hi][mp] &= ~(1 << S)
         masks[lo][mp] |= 1 << S
     return tuple(tuple(r) for r in masks)
+
+
+# ---------------------------------------------------------------------------------------
+# Pieces: (model, phase, S) units whose top-cell candidates may be split by range
+# ---------------------------------------------------------------------------------------
+# A piece (mp, S-set, [a, b)) evaluates the stage counts S-set of slot mp for the
+# candidates a..b (fractions of the model's candidate list, library order): the north
+# star's (model, GPU-type combination) axis. Costs come from ONE measured calibration
+# per problem (calibrate(): serial, S-isolated evaluations on the device, milliseconds):
+#   L[mp][S]  value + layer kernels of S (the lattice: independent of the range)
+#   T[mp][S]  marginal top-cell + decode work of S (proportional to the range)
+#   F[mp]     per-candidate part every piece of mp pays once per range (rank table,
+#             top-cell setup, decode, S = 1), proportional to the range
+# A rank's load = sum over its pieces of L + T (b - a), plus F (b - a) once per distinct
+# (mp, a, b); a rank runs its groups concurrently on its streams (CONCURRENT).
+
+
+def calibrate(handle, nmp: int, smax_mp, num_phases: int = 2) -> tuple:
+    """Measure (F, L, T) per (model, phase) slot on this device (see above): one serial
+    evaluation per stage count S, each launch attributed to its slot."""
+    handle.set_streams(1)
+    try:
+        maxS = max(smax_mp) if len(smax_mp) else 0
+        F = [0.0] * nmp
+        L = [dict() for _ in range(nmp)]
+        T = [dict() for _ in range(nmp)]
+        top1 = [0.0] * nmp
+        handle.evaluate_pieces([(mp, (1 << (smax_mp[mp] + 1)) - 2, 0, -1) for mp in range(nmp) if smax_mp[mp]])
+        for S in range(1, maxS + 1):
+            pieces = [(mp, 1 << S, 0, -1) for mp in range(nmp) if smax_mp[mp] >= S]
+            if not pieces:
+                continue
+            lay, top, rk = [float("inf")] * nmp, [float("inf")] * nmp, [float("inf")] * nmp
+            for _ in range(2):  # warm, then the smaller of two serial runs per launch kind
+                handle.evaluate_pieces(pieces)
+                a, b, c = [0.0] * nmp, [0.0] * nmp, [0.0] * nmp
+                for kind, mp, ms in handle.kernel_launches():
+                    if mp < 0 or mp >= nmp:
+                        continue
+                    if kind in (1, 2):
+                        a[mp] += ms
+                    elif kind in (0, 3):
+                        b[mp] += ms
+                    elif kind == 4:
+                        c[mp] += ms
+                lay = [min(x, y) for x, y in zip(lay, a)]
+                top = [min(x, y) for x, y in zip(top, b)]
+                rk = [min(x, y) for x, y in zip(rk, c)]
+            for mp in range(nmp):
+                if smax_mp[mp] < S:
+                    continue
+                if S == 1:
+                    # the rank table is launch-tagged with the model's first slot; every
+                    # slot that runs on a stream of its own computes it
+                    top1[mp] = top[mp]
+                    F[mp] = top[mp] + rk[mp - mp % num_phases]
+                else:
+                    L[mp][S] = lay[mp]
+                    T[mp][S] = max(0.0, top[mp] - top1[mp])
+        return tuple(F), tuple(tuple(sorted(d.items())) for d in L), tuple(tuple(sorted(d.items())) for d in T)
+    finally:
+        handle.set_streams(4)
+
+
+CONCURRENT = 0.85  # a rank runs its (slot, range) groups on up to 4 streams at once
+
+
+def _rank_load(pieces, F, L, T):
+    """Device time of a rank's pieces: each (slot, range) group runs its pieces in order
+    on one stream; groups run concurrently (the sum scaled by CONCURRENT, never below the
+    longest group)."""
+    groups = {}
+    for mp, S, a, b in pieces:
+        g = groups.setdefault((mp, a, b), F[mp] * (b - a))
+        groups[(mp, a, b)] = g + L[mp].get(S, 0.0) + T[mp].get(S, 0.0) * (b - a)
+    if not groups:
+        return 0.0
+    tot, top = sum(groups.values()), max(groups.values())
+    return max(top, tot * (CONCURRENT if len(groups) > 1 else 1.0))
+
+
+def plan_pieces(costs, world: int, max_depth: int = 3) -> list:
+    """-> per rank a list of pieces (mp, smask, a, b) (fractions a < b of the model's
+    candidates) that cover every (mp, S) unit and every candidate exactly once."""
+    return [list(r) for r in _plan_pieces(costs, int(world), int(max_depth))]
+
+
+@functools.lru_cache(maxsize=64)
+def _plan_pieces(costs, world, max_depth):
+    F, Lt, Tt = costs
+    L = [dict(x) for x in Lt]
+    T = [dict(x) for x in Tt]
+    nmp = len(F)
+    units = []  # (mp, S): S = 1 rides with S = 2 (or alone when it is the only S)
+    for mp in range(nmp):
+        Ss = sorted(set(L[mp]) | set(T[mp]))
+        if not Ss and F[mp] > 0:
+            units.append((mp, 1))
+        units += [(mp, S) for S in Ss]
+    ranks = [[] for _ in range(world)]
+
+    def load(r, extra=(), drop=()):
+        ps = [p for p in ranks[r] if p not in drop] + list(extra)
+        return _rank_load(ps, F, L, T)
+
+    # whole chains first (longest first onto the least loaded rank): a chain split over
+    # ranks pays its per-candidate part F once per rank; the moves below split only
+    # where that pays off
+    chains = {}
+    for mp, S in units:
+        chains.setdefault(mp, []).append((mp, S, 0.0, 1.0))
+    order = sorted(chains, key=lambda mp: (-_rank_load(chains[mp], F, L, T), mp))
+    for mp in order:
+        r = min(range(world), key=lambda i: (load(i, extra=chains[mp]), i))
+        ranks[r] += chains[mp]
+    for _ in range(64 * world):
+        loads = [load(i) for i in range(world)]
+        hi = max(range(world), key=lambda i: (loads[i], -i))
+        best = None
+        for p in ranks[hi]:
+            mp, S, a, b = p
+            for r in range(world):
+                if r == hi:
+                    continue
+                # (a) move the piece
+                nh, nr = load(hi, drop=(p,)), load(r, extra=(p,))
+                peak = max(nh, nr)
+                if peak < loads[hi] - 1e-6 and (best is None or peak < best[0]):
+                    best = (peak, "move", p, r)
+                # (b) split it: keep [a, m), give [m, b)
+                if (b - a) > 1.0 / (1 << max_depth) + 1e-12:
+                    m = (a + b) / 2
+                    keep, give = (mp, S, a, m), (mp, S, m, b)
+                    nh = load(hi, extra=(keep,), drop=(p,))
+                    nr = load(r, extra=(give,))
+                    peak = max(nh, nr)
+                    if peak < loads[hi] - 1e-6 and (best is None or peak < best[0]):
+                        best = (peak, "split", p, r)
+        if best is None:
+            break
+        _, kind, p, r = best
+        ranks[hi].remove(p)
+        if kind == "move":
+            ranks[r].append(p)
+        else:
+            mp, S, a, b = p
+            m = (a + b) / 2
+            ranks[hi].append((mp, S, a, m))
+            ranks[r].append((mp, S, m, b))
+    out = []
+    for r in range(world):
+        merged = {}
+        for mp, S, a, b in ranks[r]:
+            bits = (1 << S) | ((1 << 1) if S == 2 or (S == 1) else 0)
+            merged[(mp, a, b)] = merged.get((mp, a, b), 0) | bits
+        out.append(tuple(sorted((mp, mk, a, b) for (mp, a, b), mk in merged.items())))
+    return tuple(out)
+
+
+def pieces_to_ranges(pieces, counts, num_phases: int) -> list:
+    """Fractional pieces -> (mp, smask, lo, hi) with candidate indices of the model."""
+    out = []
+    for mp, mk, a, b in pieces:
+        n = int(counts[mp // num_phases])
+        lo, hi = int(round(a * n)), int(round(b * n))
+        if hi > lo:
+            out.append((mp, mk, lo, hi))
+    return out

@@ -528,3 +528,43 @@ def test_non_monotone_profile_rows_stay_on_the_lattice(w):
     assert lines[::g["sample_every"]] == g["sample"]
     assert digest(lines) == g["sha256"]
     print(f"{w} with non-monotone profile rows: {len(lines)} templates, solve {1e3 * dt:.2f} ms")
+
+
+@pytest.mark.parametrize("name,W", [("c3", 2), ("c3", 8), ("core", 3), ("extended", 8)])
+def test_pieces_split_by_candidate_range_merge_equal_single_gpu(name, W):
+    """The multi-GPU pieces (shard.plan_pieces on costs measured by shard.calibrate):
+    (model, phase, S) units whose top cells are split by candidate range over ranks --
+    the north star's (model, GPU-type combination) axis -- evaluated rank by rank on one
+    device, prefiltered, merged with the single all-gather layout: byte-identical to the
+    single-GPU frontier. Also a hand-made plan that cuts every chain into 3 ranges."""
+    from paper_2605_04357_b200 import _native
+    from paper_2605_04357_b200.shard import calibrate, pieces_to_ranges, plan_pieces
+    from tests.helpers import price_matrix
+    configs, models, slos, caps, ctx, regions, prices = workload(name)
+    pm = price_matrix(configs, prices, regions)
+    prob = Stage1Problem(configs, models, slos, caps, ctx).run()
+    full = prob.h.get_frontier(prob.h.frontier(pm)).tobytes()
+    _, lsteps, smax = prob.h.table_layout()
+    NP = 2
+    smax_mp = [min(int(smax[mp // NP]), int(lsteps[mp // NP])) if prob.counts[mp // NP] else 0
+               for mp in range(len(models) * NP)]
+    costs = calibrate(prob.h, len(smax_mp), smax_mp)
+    plan = plan_pieces(costs, W)
+    hand = [[(mp, sum(1 << S for S in range(1, smax_mp[mp] + 1)), r / 3, (r + 1) / 3)
+             for mp in range(len(smax_mp)) if smax_mp[mp]] for r in range(3)]
+    item = _native.FRONTIER_DTYPE.itemsize
+    for rank_plans in (plan, hand):
+        cands = []
+        for r in range(len(rank_plans)):
+            prob.h.evaluate_pieces(pieces_to_ranges(rank_plans[r], prob.counts, NP))
+            n = prob.h.frontier_candidates(pm)
+            cands.append(prob.h.get_frontier(n))
+        cap = max(len(c) for c in cands) + 1
+        stride = item + cap * item
+        buf = np.zeros(len(cands) * stride, dtype=np.uint8)
+        for r, part in enumerate(cands):
+            buf[r * stride + item: r * stride + item + len(part) * item] = part.view(np.uint8)
+        import torch
+        dbuf = torch.from_numpy(buf).cuda()
+        n = prob.h.frontier_merge_parts(dbuf.data_ptr(), stride, item, [len(c) for c in cands])
+        assert prob.h.get_frontier(n).tobytes() == full

@@ -12,30 +12,33 @@ import torch  # noqa: E402
 import torch.distributed as tdist  # noqa: E402
 
 from paper_2605_04357_b200 import _native, catalog  # noqa: E402
-from paper_2605_04357_b200.frontier import _gather_partials, _price_matrix  # noqa: E402
+from paper_2605_04357_b200.frontier import _gather_partials, _price_matrix, rank_pieces  # noqa: E402
 from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem  # noqa: E402
-from paper_2605_04357_b200.shard import assign_units, table_posfrac  # noqa: E402
 
 
 def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w = catalog.extended_workload()
-    caps, ctx = LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf)
+    w = catalog.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "extended"]()
+    caps, ctx = LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf, granularity=w.granularity)
     prob = Stage1Problem(w.configs, w.models, w.slos, caps, ctx)
     _, pm = _price_matrix(prob.configs, w.prices, w.regions)
     dev = torch.device("cuda", local)
     item = _native.FRONTIER_DTYPE.itemsize
     for it in range(6):
+        torch.cuda.synchronize()
+        tdist.barrier()
+        t0 = time.perf_counter()
         prob.h.tables()
         prob.h.enumerate()
         prob.counts = prob.h.num_combos()
-        _, lsteps, smax = prob.h.table_layout()
-        masks = assign_units(prob.counts, lsteps, smax, 2, tdist.get_world_size(),
-                             table_posfrac(prob.h, len(prob.configs)))
-        prob.h.evaluate_units(masks[tdist.get_rank()])
+        pieces = rank_pieces(prob, tdist)
+        t1 = time.perf_counter()
+        prob.h.evaluate_pieces(pieces)
         torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        ev = prob.h.stage_ms()["evaluate"]
         tdist.barrier()
         torch.cuda.synchronize()
         t = [time.perf_counter()]
@@ -52,8 +55,10 @@ def main():
         t.append(time.perf_counter())
         if it == 5:
             d = np.diff(t) * 1e3
-            print(f"rank {tdist.get_rank()}: n_local {n_local} gathered {sum(counts)} survivors {n} | "
-                  f"candidates {d[0]:.3f} ms gather {d[1]:.3f} ms merge {d[2]:.3f} ms", flush=True)
+            print(f"rank {tdist.get_rank()}: pieces {len(pieces)} | tables+enum+plan {1e3 * (t1 - t0):.3f} ms "
+                  f"evaluate wall {1e3 * (t2 - t1):.3f} device {ev:.3f} ms | n_local {n_local} gathered "
+                  f"{sum(counts)} survivors {n} | candidates {d[0]:.3f} ms gather {d[1]:.3f} ms merge {d[2]:.3f} ms",
+                  flush=True)
     tdist.destroy_process_group()
 
 
