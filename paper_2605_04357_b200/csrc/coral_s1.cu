@@ -2403,6 +2403,7 @@ static int evaluate_pieces(coral_s1_handle* h, std::vector<Piece> pieces) {
   std::vector<Piece> ok;
   for (Piece p : pieces) {
     if (p.mp < 0 || p.mp >= NMP) return fail(CORAL_S1_EINVAL, "piece: bad mp");
+    if (p.smask) h->own_mp[p.mp] = 1;  // requested: feasibility is checked even with no candidates
     const int m = p.mp / h->NP;
     p.lo = std::max<int64_t>(p.lo, 0);
     p.hi = (p.hi < 0 || p.hi > h->counts[m]) ? h->counts[m] : p.hi;
