@@ -2436,39 +2436,49 @@ static int evaluate_pieces(coral_s1_handle* h, std::vector<Piece> pieces) {
   if (!flags_were_ready) CUDA_TRY(cudaStreamSynchronize(st));  // flags_h valid
   CUDA_TRY(cudaEventRecord(h->fork_ev, st));
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) CUDA_TRY(cudaStreamWaitEvent(h->side[i], h->fork_ev, 0));
-  // groups of pieces sharing (model, range) run back to back on one stream and share
-  // the model's rank table over that range (both phases of a model on one GPU);
-  // heaviest first, round-robin over the side streams
-  struct Group { int m; int64_t lo, hi; std::vector<int> idx; double w; };
-  std::vector<Group> groups;
-  for (int i = 0; i < (int)ok.size(); ++i) {
-    const int m = ok[i].mp / h->NP;
-    Group* g = nullptr;
-    for (Group& x : groups)
-      if (x.m == m && x.lo == ok[i].lo && x.hi == ok[i].hi) g = &x;
-    if (!g) { groups.push_back(Group{m, ok[i].lo, ok[i].hi, {}, 0.0}); g = &groups.back(); }
-    g->idx.push_back(i);
-    g->w += (double)(ok[i].hi - ok[i].lo) * h->Lu[m] * __builtin_popcount(ok[i].smask);
-  }
-  // fewer groups than chain streams: give each (model, phase) its own stream (the rank
-  // table is then computed per slot) so that a model's phases run concurrently
+  // Pieces of one (model, phase) slot run back to back on one stream: their candidate
+  // ranges may overlap (different S), and the decode of each read-modify-writes the
+  // records. The two phases of a model (disjoint records) share a stream -- and the rank
+  // table of an equal range -- unless there are fewer such groups than chain streams,
+  // in which case each phase takes its own stream and both run concurrently.
   const int nslots = std::max(1, h->lat_ok ? std::min(h->lat_streams, h->nstreams) : h->nstreams);
-  for (bool split = true; split && (int)groups.size() < nslots;) {
-    split = false;
-    for (size_t gi = 0; gi < groups.size() && (int)groups.size() < nslots; ++gi) {
-      Group& g = groups[gi];
-      if (g.idx.size() < 2) continue;
-      const int last = g.idx.back();
-      g.idx.pop_back();
-      const double w = (double)(ok[last].hi - ok[last].lo) * h->Lu[g.m] * __builtin_popcount(ok[last].smask);
-      g.w -= w;
-      groups.push_back(Group{g.m, g.lo, g.hi, {last}, w});
-      split = true;
+  struct Group { int m; std::vector<int> idx; double w; };
+  std::vector<Group> groups;
+  {
+    std::vector<Group> per_mp;
+    for (int i = 0; i < (int)ok.size(); ++i) {
+      Group* g = nullptr;
+      for (Group& x : per_mp)
+        if (ok[x.idx[0]].mp == ok[i].mp) g = &x;
+      if (!g) { per_mp.push_back(Group{ok[i].mp / h->NP, {}, 0.0}); g = &per_mp.back(); }
+      g->idx.push_back(i);
+      g->w += (double)(ok[i].hi - ok[i].lo) * h->Lu[ok[i].mp / h->NP] * __builtin_popcount(ok[i].smask);
     }
+    int nmodels = 0;
+    for (size_t i = 0; i < per_mp.size(); ++i) {
+      bool seen = false;
+      for (size_t j = 0; j < i; ++j) seen |= per_mp[j].m == per_mp[i].m;
+      nmodels += !seen;
+    }
+    const bool by_model = nmodels >= nslots;
+    for (Group& g : per_mp) {
+      Group* t = nullptr;
+      if (by_model)
+        for (Group& x : groups)
+          if (x.m == g.m) t = &x;
+      if (!t) { groups.push_back(Group{g.m, {}, 0.0}); t = &groups.back(); }
+      t->idx.insert(t->idx.end(), g.idx.begin(), g.idx.end());
+      t->w += g.w;
+    }
+    // within a group, equal ranges back to back (one rank table each)
+    for (Group& g : groups)
+      std::stable_sort(g.idx.begin(), g.idx.end(), [&](int x, int y) {
+        return ok[x].lo != ok[y].lo ? ok[x].lo < ok[y].lo : ok[x].hi < ok[y].hi;
+      });
   }
   std::stable_sort(groups.begin(), groups.end(), [](const Group& a, const Group& b) { return a.w > b.w; });
   int64_t maxc = 1;
-  for (const Group& g : groups) maxc = std::max<int64_t>(maxc, g.hi - g.lo);
+  for (const Piece& p : ok) maxc = std::max<int64_t>(maxc, p.hi - p.lo);
   // per chain stream: the rank table of the group's range and the top cells' winners
   // (stream-ordered within a group, so one buffer per stream suffices)
   // chain streams in rotation: the lattice workspaces that fit, at most the streams asked for
@@ -2479,17 +2489,20 @@ static int evaluate_pieces(coral_s1_handle* h, std::vector<Piece> pieces) {
   for (const Group& g : groups) {
     const int m = g.m;
     unsigned* ranks = h->ws_ranks[slot].as<unsigned>();
-    if (h->n_max >= 2 && h->lat_states > 0 && h->lat_ok) {
-      LatModel L{h->K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
-      const long long n = g.hi - g.lo;
-      const long long rb = std::min<long long>((n + kRanksWarps - 1) / kRanksWarps, (long long)h->num_sms * h->ranks_blocks_per_sm);
-      const int tr = timed_begin(h, h->side[slot], 4, m * h->NP);
-      lat_ranks_kernel<<<(unsigned)rb, kRanksWarps * 32, 0, h->side[slot]>>>(
-          L, h->dp.inv_rank, h->keys.as<unsigned long long>() + h->koff[m] + g.lo, n, ranks);
-      timed_end(h, h->side[slot], tr);
-      LAUNCH_CHECK(h);
-    }
+    int64_t rlo = -1, rhi = -1;  // range of the rank table on this stream
     for (int i : g.idx) {
+      if ((ok[i].lo != rlo || ok[i].hi != rhi) && h->n_max >= 2 && h->lat_states > 0 && h->lat_ok) {
+        LatModel L{h->K, h->n_max - 1, h->lat_base_d.as<long long>(), h->lat_binom_d.as<unsigned long long>()};
+        const long long n = ok[i].hi - ok[i].lo;
+        const long long rb = std::min<long long>((n + kRanksWarps - 1) / kRanksWarps, (long long)h->num_sms * h->ranks_blocks_per_sm);
+        const int tr = timed_begin(h, h->side[slot], 4, ok[i].mp);
+        lat_ranks_kernel<<<(unsigned)rb, kRanksWarps * 32, 0, h->side[slot]>>>(
+            L, h->dp.inv_rank, h->keys.as<unsigned long long>() + h->koff[m] + ok[i].lo, n, ranks);
+        timed_end(h, h->side[slot], tr);
+        LAUNCH_CHECK(h);
+        rlo = ok[i].lo;
+        rhi = ok[i].hi;
+      }
       std::vector<int> Ss;
       for (int S = 1; S <= CORAL_S1_MAX_NODES; ++S)
         if ((ok[i].smask >> S) & 1u) Ss.push_back(S);

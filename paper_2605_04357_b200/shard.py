@@ -139,7 +139,7 @@ def _assign_units(counts, lsteps, smax, num_phases, world, posfrac):
 #   F[mp]     per-candidate part every piece of mp pays once per range (rank table,
 #             top-cell setup, decode, S = 1), proportional to the range
 # A rank's load = sum over its pieces of L + T (b - a), plus F (b - a) once per distinct
-# (mp, a, b); a rank runs its groups concurrently on its streams (CONCURRENT).
+# (mp, a, b); a rank runs its slots concurrently on its streams (CONCURRENT).
 
 
 def calibrate(handle, nmp: int, smax_mp, num_phases: int = 2) -> tuple:
@@ -189,17 +189,20 @@ def calibrate(handle, nmp: int, smax_mp, num_phases: int = 2) -> tuple:
         handle.set_streams(4)
 
 
-CONCURRENT = 0.85  # a rank runs its (slot, range) groups on up to 4 streams at once
+CONCURRENT = 0.85  # a rank runs its (model, phase) slots on up to 4 streams at once
 
 
 def _rank_load(pieces, F, L, T):
-    """Device time of a rank's pieces: each (slot, range) group runs its pieces in order
-    on one stream; groups run concurrently (the sum scaled by CONCURRENT, never below the
-    longest group)."""
-    groups = {}
+    """Device time of a rank's pieces: the pieces of one (model, phase) slot run in order
+    on one stream (a rank table + per-candidate setup F once per distinct range); slots
+    run concurrently (the sum scaled by CONCURRENT, never below the longest slot)."""
+    groups, ranges = {}, set()
     for mp, S, a, b in pieces:
-        g = groups.setdefault((mp, a, b), F[mp] * (b - a))
-        groups[(mp, a, b)] = g + L[mp].get(S, 0.0) + T[mp].get(S, 0.0) * (b - a)
+        g = groups.get(mp, 0.0)
+        if (mp, a, b) not in ranges:
+            ranges.add((mp, a, b))
+            g += F[mp] * (b - a)
+        groups[mp] = g + L[mp].get(S, 0.0) + T[mp].get(S, 0.0) * (b - a)
     if not groups:
         return 0.0
     tot, top = sum(groups.values()), max(groups.values())

@@ -552,8 +552,15 @@ def test_pieces_split_by_candidate_range_merge_equal_single_gpu(name, W):
     plan = plan_pieces(costs, W)
     hand = [[(mp, sum(1 << S for S in range(1, smax_mp[mp] + 1)), r / 3, (r + 1) / 3)
              for mp in range(len(smax_mp)) if smax_mp[mp]] for r in range(3)]
+    # overlapping ranges of one slot on one rank (S <= 3 over all candidates, S >= 4 over
+    # the first half): their decodes update the same records, in stream order
+    low = lambda mp: sum(1 << S for S in range(1, min(3, smax_mp[mp]) + 1))  # noqa: E731
+    high = lambda mp: sum(1 << S for S in range(4, smax_mp[mp] + 1))  # noqa: E731
+    overlap = [[(mp, low(mp), 0.0, 1.0) for mp in range(len(smax_mp)) if smax_mp[mp]] +
+               [(mp, high(mp), 0.0, 0.5) for mp in range(len(smax_mp)) if high(mp)],
+               [(mp, high(mp), 0.5, 1.0) for mp in range(len(smax_mp)) if high(mp)]]
     item = _native.FRONTIER_DTYPE.itemsize
-    for rank_plans in (plan, hand):
+    for rank_plans in (plan, hand, overlap):
         cands = []
         for r in range(len(rank_plans)):
             prob.h.evaluate_pieces(pieces_to_ranges(rank_plans[r], prob.counts, NP))
