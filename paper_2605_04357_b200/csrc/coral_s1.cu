@@ -133,6 +133,8 @@ struct coral_s1_handle {
   std::vector<char> model_used;
   std::vector<char> own_mp;  // (model, phase) chains with records from the last evaluate
   DevBuf run_off_d, run_mp_d;
+  DevBuf tokp;  // [R][512] token prices of the last frontier
+  DevBuf rect;  // per candidate: the record's throughput (0 = no template), for the frontier passes
   std::vector<double> memb_h, wbytes_h;  // config memory bytes, model weight bytes
   std::vector<int> inv_rank_h;           // str rank -> config index
   double rho = 0;
@@ -331,11 +333,13 @@ __global__ void __launch_bounds__(kEnumThreads) enum_count_kernel(
 }
 
 // pass 2: ONE read of the block's keys and memory sums, then every model's stable
-// compaction at its scanned block offset (element order = thread-major, as pass 1)
+// compaction at its scanned block offset (element order = thread-major, as pass 1),
+// staged in shared memory so that each model's survivors leave in one coalesced store
 __global__ void __launch_bounds__(kEnumThreads) window_select_kernel(
     DevProblem P, int64_t U, const unsigned long long* __restrict__ ukey, const double* __restrict__ umem,
     int nblk, const unsigned long long* __restrict__ blkoff, unsigned long long* __restrict__ keys) {
   __shared__ int s_warp[2][kEnumThreads / 32];
+  __shared__ unsigned long long s_keys[2][kEnumBlock];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t e0 = (int64_t)blockIdx.x * kEnumBlock + (int64_t)threadIdx.x * kEnumItems;
   unsigned long long k4[kEnumItems];
@@ -371,17 +375,24 @@ __global__ void __launch_bounds__(kEnumThreads) window_select_kernel(
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    const int buf = m & 1;  // double-buffered warp totals: one barrier per model
+    const int buf = m & 1;  // double-buffered warp totals and staged keys
     if (lane == 31) s_warp[buf][warp] = incl;
     __syncthreads();
-    if (!pass) continue;
-    int before = 0;
+    int before = 0, total = 0;
 #pragma unroll
-    for (int w = 0; w < kEnumThreads / 32; ++w) before += w < warp ? s_warp[buf][w] : 0;
-    unsigned long long out = blkoff[(int64_t)m * nblk + blockIdx.x] + (unsigned long long)(before + incl - c);
+    for (int w = 0; w < kEnumThreads / 32; ++w) {
+      before += w < warp ? s_warp[buf][w] : 0;
+      total += s_warp[buf][w];
+    }
+    if (!total) continue;  // uniform over the block
+    // stage the block's survivors in order, then one coalesced store of all of them
+    int pos = before + incl - c;
 #pragma unroll
     for (int k = 0; k < kEnumItems; ++k)
-      if ((pass >> k) & 1u) keys[out++] = k4[k];
+      if ((pass >> k) & 1u) s_keys[buf][pos++] = k4[k];
+    __syncthreads();
+    unsigned long long* out = keys + blkoff[(int64_t)m * nblk + blockIdx.x];
+    for (int i = threadIdx.x; i < total; i += kEnumThreads) out[i] = s_keys[buf][i];
   }
 }
 
@@ -479,6 +490,7 @@ struct EvalArgs {
   const int64_t* tab_off;
   const unsigned char* flags;
   coral_s1_record* rec;            // indexed by global candidate index
+  double* rect;                    // its throughput (frontier passes)
 };
 
 __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
@@ -558,7 +570,10 @@ __global__ void __launch_bounds__(kDpThreads) evaluate_kernel(EvalArgs A) {
     }
     __syncthreads();
   }
-  if (tid == 0) A.rec[ci] = s_rec;
+  if (tid == 0) {
+    A.rec[ci] = s_rec;
+    A.rect[ci] = s_rec.num_stages ? s_rec.throughput_tps : 0.0;
+  }
 }
 
 // Warp-wide (value desc, code asc) selection of the reference tie rule with the
@@ -604,6 +619,7 @@ struct TopArgs {
   const long long* off;
   const uint2* subtab;
   coral_s1_record* rec;             // this (model, phase)'s records
+  double* rect;                     // their throughputs (frontier passes)
   int4* win;                        // per candidate: best value (lo, hi), S, u code << 10 | j
   const unsigned* ranks;            // [candidate][64] from lat_ranks_kernel
   unsigned long long* census;       // census on: [2] += (u, S) pairs searched
@@ -780,6 +796,7 @@ __global__ void __launch_bounds__(256) lat_decode_kernel(TopArgs A) {
     }
   }
   canonical_record(twin, sj, sc, C, cnt, A.g, tbest, n, &A.rec[ci]);
+  A.rect[ci] = tbest;
 }
 
 // --------------------------------------------------------------------------------
@@ -865,12 +882,15 @@ struct FrontArgs {
   const coral_s1_record* rec;
   int64_t ncand;
   const double* prices;  // [R][K], NaN = not offered
+  const double* tok_price = nullptr;  // [R][512] count x price per packed token (frontier passes)
   int R;
   coral_s1_frontier_item* items;
   unsigned long long* nitems;
   unsigned long long cap = 0;      // items capacity (frontier_items_kernel counts past it)
-  // the prefilter passes run over the (model, phase) chains this device evaluated:
-  // thread t -> run k (run_off[k] <= t < run_off[k+1]) -> mp = run_mp[k]
+  // the prefilter passes run over the (model, phase) chains this device evaluated: run k
+  // (slot run_mp[k]) owns blocks run_boff[k] .. run_boff[k+1] - 1, 256 candidates each
+  const int64_t* run_boff = nullptr;
+  const double* rect = nullptr;    // per candidate: the record's throughput, 0 = no template
   const int64_t* run_off = nullptr;
   const int* run_mp = nullptr;
   int nrun = 0;
@@ -884,51 +904,59 @@ struct FrontCand {
   unsigned long long key;
   double T;      // the record's throughput (the full record is re-read for survivors only)
   int64_t ri;    // record index
-  int cfg[kMaxC], cnt[kMaxC];
+  unsigned tok[kMaxC];  // packed tokens ((rank + 1) << 3 | count), combo order
 };
-// false when t is past the end or the candidate has no template
-__device__ __forceinline__ bool frontier_cand(const FrontArgs& A, int64_t t, FrontCand& f) {
-  if (t >= A.ntot) return false;
-  int lo = 0, hi = A.nrun;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (A.run_off[mid] <= t) lo = mid; else hi = mid;
+
+// Token prices of every region, tp[r * 512 + token] = count x the config's price in
+// region r (rn_mul on the host: the same IEEE product allocation.py:97 computes as n * p;
+// NaN when the config is unpriced there, which then propagates through the sum), read
+// through the read-only cache: one load + add per token instead of a config lookup, a
+// price load and a multiply.
+// The block's run (one binary search per block, not per thread).
+__device__ __forceinline__ int frontier_block_run(const FrontArgs& A) {
+  __shared__ int s_run;
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = A.nrun;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (A.run_boff[mid] <= (int64_t)blockIdx.x) lo = mid; else hi = mid;
+    }
+    s_run = lo;
   }
-  const int mp = A.run_mp[lo];
-  const int64_t idx = t - A.run_off[lo];  // candidate index within its (model, phase)
+  __syncthreads();
+  return s_run;
+}
+// false when the thread is past its run's end or the candidate has no template
+__device__ __forceinline__ bool frontier_cand(const FrontArgs& A, int run, FrontCand& f) {
+  const int mp = A.run_mp[run];
+  const int64_t idx = ((int64_t)blockIdx.x - A.run_boff[run]) * blockDim.x + threadIdx.x;  // within (model, phase)
+  if (idx >= A.cand_off[mp + 1] - A.cand_off[mp]) return false;
   f.ri = A.cand_off[mp] + idx;
-  // throughput + num_stages: the record's first 16 bytes (one sector either way)
-  const double2 head = *reinterpret_cast<const double2*>(A.rec + f.ri);
-  if ((__double2loint(head.y) & 0xFF) == 0) return false;  // num_stages == 0: no template
-  f.T = head.x;
+  // the compact throughput array (8 B), not the 32-byte record: the full record is read
+  // for survivors only
+  f.T = A.rect[f.ri];
+  if (!(f.T > 0.0)) return false;  // no template
   f.mp = mp;
   const int m = mp / A.P.NP;
   f.key = A.keys[A.koff[m] + idx];
-  // tokens are contiguous from the top: unrolled, so cfg/cnt stay in registers
+  // tokens are contiguous from the top: unrolled, so they stay in registers
   f.C = 0;
 #pragma unroll
   for (int t = 0; t < kMaxC; ++t) {
-    const unsigned tok = (unsigned)(f.key >> (kKeyTokenBits * (kMaxC - 1 - t))) & 511u;
-    f.cnt[t] = (int)(tok & 7u);
-    f.cfg[t] = tok ? A.P.inv_rank[(tok >> 3) - 1] : 0;
-    f.C += tok != 0u;
+    f.tok[t] = (unsigned)(f.key >> (kKeyTokenBits * (kMaxC - 1 - t))) & 511u;
+    f.C += f.tok[t] != 0u;
   }
   return true;
 }
 // allocation.py:91-98 _template_price of the candidate in region r (combo order,
 // sequential); false when a config is not offered there (price None)
-__device__ __forceinline__ bool frontier_price(const FrontArgs& A, const FrontCand& f, int r,
-                                               double& total) {
+__device__ __forceinline__ bool frontier_price(const FrontArgs& A, const FrontCand& f, int r, double& total) {
   total = 0.0;
+  const double* __restrict__ row = A.tok_price + r * 512;
 #pragma unroll
-  for (int c = 0; c < kMaxC; ++c) {
-    if (c < f.C) {
-      const double p = A.prices[(int64_t)r * A.P.K + f.cfg[c]];
-      if (isnan(p)) return false;
-      total = rn_add(total, rn_mul((double)f.cnt[c], p));
-    }
-  }
-  return true;
+  for (int c = 0; c < kMaxC; ++c)
+    if (c < f.C) total = rn_add(total, __ldg(row + f.tok[c]));
+  return !isnan(total);
 }
 __device__ __forceinline__ unsigned long long dbits(double x) {
   return (unsigned long long)__double_as_longlong(x);  // monotone for x >= 0
@@ -947,12 +975,14 @@ __device__ __forceinline__ int bucket_of(double price, int shift, unsigned long 
 __global__ void frontier_bucket_kernel(FrontArgs A, int shift, unsigned long long base, int nb,
                                        unsigned long long* __restrict__ bmax) {
   FrontCand f;
-  if (!frontier_cand(A, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, f)) return;
+  if (!frontier_cand(A, frontier_block_run(A), f)) return;
   const unsigned long long tb = dbits(f.T);
   for (int r = 0; r < A.R; ++r) {
     double price;
     if (!frontier_price(A, f, r, price)) continue;
     const int b = bucket_of(price, shift, base, nb);
+    // most items do not raise their bucket: read first (an unconditional atomic per item
+    // serialises on the hot buckets, 2.5x slower at config 5)
     unsigned long long* slot = bmax + ((int64_t)f.mp * A.R + r) * nb + b;
     if (*slot < tb) atomicMax(slot, tb);
   }
@@ -983,7 +1013,7 @@ __global__ void frontier_prefix_kernel(int nb, unsigned long long* __restrict__ 
 __global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long base, int nb,
                                       const unsigned long long* __restrict__ pmax) {
   FrontCand f;
-  const bool valid = frontier_cand(A, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, f);
+  const bool valid = frontier_cand(A, frontier_block_run(A), f);
   const int lane = threadIdx.x & 31;
   for (int r = 0; r < A.R; ++r) {  // uniform over the warp: ballots stay converged
     double price = 0.0;
@@ -1714,7 +1744,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
                     &h->flagsel, &h->nsel, &h->front, &h->prices, &h->ukey_s, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->fbucket, &h->segbuf, &h->avars,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
-                    &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff, &h->run_off_d, &h->run_mp_d};
+                    &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff, &h->run_off_d, &h->run_mp_d, &h->rect, &h->tokp};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release(); h->ws_ranks[i].release();
@@ -2061,6 +2091,7 @@ static int launch_percombo(coral_s1_handle* h, cudaStream_t st, int64_t lo, int6
   A.tab_off = h->tab_off_d.as<int64_t>();
   A.flags = h->flags.as<unsigned char>();
   A.rec = h->rec.as<coral_s1_record>();
+  A.rect = h->rect.as<double>();
   const size_t smem = dp_smem_bytes(std::min(kMaxM, 1 << h->n_max), h->maxLu + 1, h->maxLu, h->n_max - 2);
   if (smem > h->dp_smem_limit)
     return fail(CORAL_S1_EUNSUPPORTED, "per-candidate placement DP: n_max " + std::to_string(h->n_max) +
@@ -2327,6 +2358,7 @@ static int lattice_pass(coral_s1_handle* h, int mp, int slot, const unsigned* ra
   T.off = h->lat_off.as<long long>();
   T.subtab = h->lat_sub.as<uint2>();
   T.rec = h->rec.as<coral_s1_record>() + h->cand_off[mp] + lo;
+  T.rect = h->rect.as<double>() + h->cand_off[mp] + lo;
   T.win = h->ws_win[slot].as<int4>();
   T.ranks = ranks;
   T.census = h->census_on ? h->census.as<unsigned long long>() : nullptr;
@@ -2396,7 +2428,9 @@ static int evaluate_pieces(coral_s1_handle* h, std::vector<Piece> pieces) {
   if (!h || !h->have_tables || !h->have_enum) return fail(CORAL_S1_EINVAL, "tables and enumerate first");
   CUDA_TRY(cudaSetDevice(h->device));
   int rc;
-  if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record)))) return rc;
+  if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record))) ||
+      (rc = h->rect.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(double))))
+    return rc;
   cudaStream_t st = h->stream;
   const int NMP = h->NM * h->NP;
   h->own_mp.assign(NMP, 0);
@@ -2425,6 +2459,7 @@ static int evaluate_pieces(coral_s1_handle* h, std::vector<Piece> pieces) {
   h->ntimed = 0;
   // records not improved by any piece read as infeasible (num_stages 0)
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), st));
+  CUDA_TRY(cudaMemsetAsync(h->rect.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(double), st));
   if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 32, st));
   if (h->lat_ready) {  // prepared on side[0] during enumerate (every model with candidates)
     CUDA_TRY(cudaStreamWaitEvent(st, h->prep_ev, 0));
@@ -2544,10 +2579,13 @@ int coral_s1_evaluate(coral_s1_handle* h, int64_t lo, int64_t hi) {
   // a sub-range: per-candidate kernel over [lo, hi), every S
   CUDA_TRY(cudaSetDevice(h->device));
   int rc;
-  if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record)))) return rc;
+  if ((rc = h->rec.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record))) ||
+      (rc = h->rect.ensure(std::max<int64_t>(h->ncand, 1) * sizeof(double))))
+    return rc;
   h->own_mp.assign((size_t)h->NM * h->NP, 1);
   CUDA_TRY(cudaEventRecord(h->ev[4], h->stream));
   CUDA_TRY(cudaMemsetAsync(h->rec.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(coral_s1_record), h->stream));
+  CUDA_TRY(cudaMemsetAsync(h->rect.p, 0, std::max<int64_t>(h->ncand, 1) * sizeof(double), h->stream));
   if (h->census_on) CUDA_TRY(cudaMemsetAsync(h->census.p, 0, 32, h->stream));
   if ((rc = launch_percombo(h, h->stream, lo, hi, 1, 1, CORAL_S1_MAX_NODES))) return rc;
   CUDA_TRY(cudaEventRecord(h->ev[5], h->stream));
@@ -2636,28 +2674,42 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
     A.R = num_regions;
     A.items = h->items.as<coral_s1_frontier_item>();
     A.nitems = h->nsel.as<unsigned long long>();
-    {  // only the chains this device evaluated (all of them on one GPU)
-      std::vector<int64_t> roff(1, 0);
+    int64_t nblocks = 0;
+    {  // only the chains this device evaluated (all of them on one GPU), 256 per block
+      std::vector<int64_t> boff(1, 0);
       std::vector<int> rmp;
+      int64_t tot = 0;
       for (int mp = 0; mp < A.NMP; ++mp) {
         const int64_t c = h->cand_off[mp + 1] - h->cand_off[mp];
         if (!c || (mp < (int)h->own_mp.size() && !h->own_mp[mp])) continue;
         rmp.push_back(mp);
-        roff.push_back(roff.back() + c);
+        boff.push_back(boff.back() + (c + 255) / 256);
+        tot += c;
       }
-      if (rmp.empty()) rmp.push_back(0);  // keeps the device arrays non-empty (ntot = 0)
-      if ((rc = upload(h, h->run_off_d, roff)) || (rc = upload(h, h->run_mp_d, rmp))) return rc;
-      A.run_off = h->run_off_d.as<int64_t>();
+      if (rmp.empty()) { rmp.push_back(0); boff.push_back(0); }  // non-empty device arrays
+      if ((rc = upload(h, h->run_off_d, boff)) || (rc = upload(h, h->run_mp_d, rmp))) return rc;
+      A.run_boff = h->run_off_d.as<int64_t>();
       A.run_mp = h->run_mp_d.as<int>();
-      A.nrun = (int)roff.size() - 1;
-      A.ntot = roff.back();
+      A.nrun = (int)rmp.size();
+      A.ntot = tot;
+      A.rect = h->rect.as<double>();
+      nblocks = boff.back();
+      std::vector<double> tp((size_t)std::max(num_regions, 1) * 512, 0.0);
+      for (int r = 0; r < num_regions; ++r)
+        for (int tok = 0; tok < 512; ++tok) {
+          const int rank1 = tok >> 3, cnt = tok & 7;
+          if (rank1 >= 1 && rank1 <= h->K && cnt > 0)
+            tp[(size_t)r * 512 + tok] = (double)cnt * pv[(size_t)r * h->K + h->inv_rank_h[rank1 - 1]];
+        }
+      if ((rc = upload(h, h->tokp, tp))) return rc;
+      A.tok_price = h->tokp.as<double>();
     }
     // exact prefilter: per (segment, price bucket) max T -> prefix max. The bucket range
     // only has to contain every item price (any non-decreasing price -> bucket map keeps
     // the filter exact), so it comes from the price matrix on the host: a combo costs at
     // least the cheapest offered config and at most n_max x the dearest (with margin for
     // rounding; bucket indices are clamped, which keeps the map non-decreasing).
-    const unsigned gb = (unsigned)((std::max<int64_t>(A.ntot, 1) + 255) / 256);  // thread per candidate, regions looped
+    const unsigned gb = (unsigned)std::max<int64_t>(nblocks, 1);  // thread per candidate, regions looped
     unsigned long long range[2] = {~0ull, 0ull};
     {
       double pmin = HUGE_VAL, pmax = 0.0;
