@@ -2331,13 +2331,22 @@ static int lattice_pass(coral_s1_handle* h, int mp, int slot, const unsigned* ra
     const long long* off = h->lat_off.as<long long>();
     const uint2* sub = h->lat_sub.as<uint2>();
     // states of 6 configs (n_max = 7): up to 63 sub-multiset codes -> 2 slots per lane
+    // one launch per search mode (exact: capped search; tolerance-monotone: literal
+    // search; scan pass: full scan), each over the S values of that mode
+    const unsigned m_exact = scan ? 0u : (smask & xmask), m_tol = scan ? 0u : (smask & ~xmask),
+                   m_scan = scan ? smask : 0u;
+#define CORAL_LAYER(SL, MODE, MASK) \
+    lat_layer_kernel<SL, MODE><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, MASK, xmask, h->n_max, Lu, maxn, off, sub, W, cen)
     if (h->n_max >= 7) {
-      if (scan) lat_layer_kernel<2, true><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu, maxn, off, sub, W, cen);
-      else lat_layer_kernel<2, false><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu, maxn, off, sub, W, cen);
+      if (m_exact) CORAL_LAYER(2, 1, m_exact);
+      if (m_tol) CORAL_LAYER(2, 0, m_tol);
+      if (m_scan) CORAL_LAYER(2, 2, m_scan);
     } else {
-      if (scan) lat_layer_kernel<1, true><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu, maxn, off, sub, W, cen);
-      else lat_layer_kernel<1, false><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, smask, xmask, h->n_max, Lu, maxn, off, sub, W, cen);
+      if (m_exact) CORAL_LAYER(1, 1, m_exact);
+      if (m_tol) CORAL_LAYER(1, 0, m_tol);
+      if (m_scan) CORAL_LAYER(1, 2, m_scan);
     }
+#undef CORAL_LAYER
     timed_end(h, st, ti);
     LAUNCH_CHECK(h);
   }

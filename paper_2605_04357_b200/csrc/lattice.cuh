@@ -349,9 +349,12 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
 // DP layer sg for every S in [S_lo, S_lo + gridDim.y) with S > sg: warp per state X,
 // lanes over l. Cells: sg <= |X| <= maxn(X) - (S - sg), sg <= l <= Lu - (S - sg).
 // kSlots = ceil((M(X) - 1) / 32) code slots per lane: 1 while n_max <= 6 (|X| <= 5),
-// 2 for n_max = 7 (|X| <= 6, M(X) <= 64). scan: the full-scan variant (rows that fail
-// the monotone test, kernels.py:240-249; xmask is then 0).
-template <int kSlots, bool kScan>
+// 2 for n_max = 7 (|X| <= 6, M(X) <= 64). kMode: 1 = exactly monotone rows (capped
+// crossing search, u <-> X-u symmetry at layer 2), 0 = rows monotone only within the
+// 1e-12 tolerance (the literal [1, jmax] search), 2 = the full-scan variant (rows that
+// fail the monotone test, kernels.py:240-249). One launch per mode; each launch's smask
+// holds only the S values of its mode.
+template <int kSlots, int kMode>
 __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
     LatModel L, int sg, int S_lo, unsigned smask, unsigned xmask, int n_max, int Lu,
     const unsigned* __restrict__ maxn, const long long* __restrict__ off,
@@ -373,10 +376,14 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
   // Layer 2 reads value rows on both sides: with exactly monotone rows the crossing
   // is the true max, so cand(u) == cand(X-u) (j <-> l-j); the smallest maximising
   // code lies in the lower half (code(X-u) = M-1-code(u)) and only it is searched.
-  const long long cmax = (sg == 2 && ((xmask >> S) & 1u)) ? (M - 1) / 2 + 1 : M;
-  const bool cap = (xmask >> S) & 1u;  // exactly monotone rows: capped crossing search
+  const long long cmax = (sg == 2 && kMode == 1) ? (M - 1) / 2 + 1 : M;
+  (void)xmask;
+  // the row bases stay in registers (the compiler would re-derive them from the launch
+  // parameters inside the search loop)
   const double* __restrict__ value = W.val(S);
   const double* __restrict__ fprev = W.lay(S, sg - 1);
+  asm volatile("" : "+l"(value));
+  asm volatile("" : "+l"(fprev));
   double* __restrict__ fout = W.lay(S, sg);
   unsigned short* __restrict__ chout = W.chl(S, sg);
   // u codes of X that pass the size filter: slot k of a lane holds code lane + 1 + 32k;
@@ -458,7 +465,7 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
       if (!act || kk >= nv) continue;
       double cand;
       int cj;
-      dp_pair(value + vo, fprev + fo, l, jmax, !kScan, cand, cj, cap);  // scan: kernels.py:240-249
+      dp_pair(value + vo, fprev + fo, l, jmax, kMode != 2, cand, cj, kMode == 1);  // 2: kernels.py:240-249
       if (cand > best) { best = cand; bu = code; bj = cj; }
     }
     // merge the groups of each l: value desc, then smallest code (the reference's
