@@ -411,7 +411,7 @@ def main():
     layer_ms, layer_n = h.kernel_stats(1)
     top_ms, top_n = h.kernel_stats(0)
     sk = {k: h.kernel_stats(k) for k in (2, 3, 4)}
-    h.set_streams(4)
+    h.set_streams(0)
     layer_alg, layer_pairs, top_pairs = census[0], census[1], census[2]
     layer_launch_s = (layer_ms / max(layer_n, 1)) / 1e3
     alg_per_launch = layer_alg / max(layer_n, 1)

@@ -298,8 +298,8 @@ int coral_s1_census(coral_s1_handle* h, int64_t* layer_bytes);
 /* all census counters of the last evaluate: [0] layer-kernel algorithmic bytes, [1] layer
  * (u, l) pairs, [2] top-cell (u, S) pairs searched, [3] reserved */
 int coral_s1_census_all(coral_s1_handle* h, int64_t* out, int n);
-/* chain streams used by evaluate (1..4; default 4 or CORAL_S1_STREAMS): 1 serialises the
- * lattice kernels (bench.py times the roofline launches that way) */
+/* chain streams used by evaluate (1..8; 0 = the default, 4 or CORAL_S1_STREAMS): 1
+ * serialises the lattice kernels (bench.py times the roofline launches that way) */
 int coral_s1_set_streams(coral_s1_handle* h, int n);
 
 #ifdef __cplusplus

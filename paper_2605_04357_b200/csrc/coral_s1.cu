@@ -114,8 +114,10 @@ struct coral_s1_handle {
   DevBuf op_in, op_out, tab_off_d, fbucket, segbuf, avars;
   int64_t navars = 0;
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
-  static constexpr int kStreams = 4;
-  int nstreams = kStreams;  // side streams in use (CORAL_S1_STREAMS)
+  static constexpr int kStreams = 8;
+  static constexpr int kDefaultStreams = 4;
+  int default_streams = kDefaultStreams;  // CORAL_S1_STREAMS
+  int nstreams = kDefaultStreams;  // side streams in use
   int lat_streams = kStreams;  // streams whose lattice workspace fits in device memory
   bool lat_ok = true;          // false: every unit runs the exact per-candidate kernel
   size_t mem_limit = 0;        // CORAL_S1_MEM_LIMIT: cap on usable device memory (tests)
@@ -1715,6 +1717,7 @@ int coral_s1_create(int device, coral_s1_handle** out) {
   cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->prep_ev, cudaEventDisableTiming);
   if (const char* e = getenv("CORAL_S1_STREAMS")) h->nstreams = std::max(1, std::min(atoi(e), coral_s1_handle::kStreams));
+  h->default_streams = h->nstreams;
   if (const char* e = getenv("CORAL_S1_MEM_LIMIT")) h->mem_limit = (size_t)strtoull(e, nullptr, 10);
   if (h->lat_binom_d.ensure(sizeof(tab)) == 0)
     cudaMemcpy(h->lat_binom_d.p, tab, sizeof(tab), cudaMemcpyHostToDevice);
@@ -3306,8 +3309,8 @@ int coral_s1_census_all(coral_s1_handle* h, int64_t* out, int n) {
 
 int coral_s1_set_streams(coral_s1_handle* h, int n) {
   if (!h) return fail(CORAL_S1_EINVAL, "null handle");
-  if (n < 1 || n > coral_s1_handle::kStreams) return fail(CORAL_S1_EINVAL, "streams must be 1..4");
-  h->nstreams = n;
+  if (n < 0 || n > coral_s1_handle::kStreams) return fail(CORAL_S1_EINVAL, "streams must be 0 (default) .. 8");
+  h->nstreams = n ? n : h->default_streams;
   return 0;
 }
 

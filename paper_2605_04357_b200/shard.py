@@ -186,7 +186,7 @@ def calibrate(handle, nmp: int, smax_mp, num_phases: int = 2) -> tuple:
                     T[mp][S] = max(0.0, top[mp] - top1[mp])
         return tuple(F), tuple(tuple(sorted(d.items())) for d in L), tuple(tuple(sorted(d.items())) for d in T)
     finally:
-        handle.set_streams(4)
+        handle.set_streams(0)
 
 
 CONCURRENT = 0.85  # a rank runs its (model, phase) slots on up to 4 streams at once
