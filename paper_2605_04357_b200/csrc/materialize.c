@@ -42,16 +42,48 @@ static PyObject* pair_for(unsigned tok, PyObject* cfgs, PyObject** pairs) {
   return pairs[tok];
 }
 
+/* Open-addressing map (tag, key) -> owned object, for the per-call caches (no
+ * Python int keys: the survivor loop runs ~1e3-1e5 times per frontier). */
+typedef struct {
+  uint64_t* key;
+  int32_t* tag;
+  PyObject** val;
+  size_t cap;
+} cmap;
+
+static int cmap_init(cmap* m, size_t n) {
+  size_t cap = 16;
+  while (cap < 2 * n + 2) cap <<= 1;
+  m->key = (uint64_t*)PyMem_Calloc(cap, sizeof(uint64_t));
+  m->tag = (int32_t*)PyMem_Malloc(cap * sizeof(int32_t));
+  m->val = (PyObject**)PyMem_Calloc(cap, sizeof(PyObject*));
+  m->cap = cap;
+  if (!m->key || !m->tag || !m->val) return -1;
+  for (size_t i = 0; i < cap; ++i) m->tag[i] = -1;
+  return 0;
+}
+static void cmap_free(cmap* m) {
+  if (m->val)
+    for (size_t i = 0; i < m->cap; ++i) Py_XDECREF(m->val[i]);
+  PyMem_Free(m->key);
+  PyMem_Free(m->tag);
+  PyMem_Free(m->val);
+}
+/* slot of (tag, key): the existing entry or the empty slot where it goes */
+static size_t cmap_slot(const cmap* m, int32_t tag, uint64_t key) {
+  uint64_t h = (key ^ ((uint64_t)(uint32_t)tag * 0x9E3779B97F4A7C15ull)) * 0xBF58476D1CE4E5B9ull;
+  size_t i = (size_t)(h >> 17) & (m->cap - 1);
+  while (m->tag[i] != -1 && !(m->tag[i] == tag && m->key[i] == key)) i = (i + 1) & (m->cap - 1);
+  return i;
+}
+
 /* New reference to the NodeComboKey of a packed combo key, cached in `combos`. */
-static PyObject* combo_for(uint64_t key, PyObject* cfgs, PyObject* combos, PyObject** pairs,
+static PyObject* combo_for(uint64_t key, PyObject* cfgs, cmap* combos, PyObject** pairs,
                            PyObject* T_combo) {
-  PyObject* kk = PyLong_FromUnsignedLongLong(key);
-  if (!kk) return NULL;
-  PyObject* combo = PyDict_GetItem(combos, kk);
-  if (combo) {
-    Py_DECREF(kk);
-    Py_INCREF(combo);
-    return combo;
+  const size_t slot = cmap_slot(combos, 0, key);
+  if (combos->val[slot]) {
+    Py_INCREF(combos->val[slot]);
+    return combos->val[slot];
   }
   int ntok = 0;
   for (int k = 0; k < CORAL_S1_MAX_NODES; ++k)
@@ -63,13 +95,15 @@ static PyObject* combo_for(uint64_t key, PyObject* cfgs, PyObject* combos, PyObj
     Py_INCREF(pr);
     PyTuple_SET_ITEM(items, k, pr);
   }
-  combo = items ? new_obj((PyTypeObject*)T_combo) : NULL;
-  if (!combo || seta(combo, s_items, items) < 0 || PyDict_SetItem(combos, kk, combo) < 0) {
+  PyObject* combo = items ? new_obj((PyTypeObject*)T_combo) : NULL;
+  if (!combo || seta(combo, s_items, items) < 0) {
     Py_XDECREF(combo);
-    Py_DECREF(kk);
     return NULL;
   }
-  Py_DECREF(kk);
+  combos->tag[slot] = 0;
+  combos->key[slot] = key;
+  combos->val[slot] = combo;  /* the map's reference */
+  Py_INCREF(combo);
   return combo;
 }
 
@@ -90,9 +124,13 @@ static PyObject* materialise(PyObject* self, PyObject* args) {
   PyObject** seg_lists = PyMem_Calloc((size_t)(nmp * nreg + 1), sizeof(PyObject*));
   PyObject* pairs[512] = {NULL};
   PyObject* segments = PyDict_New();
-  PyObject* cache = PyDict_New();
-  PyObject* combos = PyDict_New();
-  if (!segments || !cache || !combos || !seg_lists) goto fail;
+  cmap cache = {0}, combos = {0}, places = {0};
+  const coral_s1_record** places_rec = NULL;
+  if (!segments || !seg_lists || cmap_init(&cache, (size_t)n) < 0 || cmap_init(&combos, (size_t)n) < 0 ||
+      cmap_init(&places, (size_t)n) < 0)
+    goto fail;
+  places_rec = (const coral_s1_record**)PyMem_Calloc(places.cap, sizeof(void*));
+  if (!places_rec) goto fail;
   for (Py_ssize_t i = 0; i < n; ++i) {
     const coral_s1_frontier_item* x = &it[i];
     const int mp = x->mp, m = mp / NP, ph = mp % NP;
@@ -100,32 +138,40 @@ static PyObject* materialise(PyObject* self, PyObject* args) {
       PyErr_SetString(PyExc_ValueError, "frontier item outside the problem's (model, phase, region)");
       goto fail;
     }
-    /* (mp, combo) as one int: mp above the 9 * CORAL_S1_MAX_NODES = 63 key bits */
-    PyObject* ck = NULL;
-    {
-      PyObject* hi = PyLong_FromLong(mp);
-      PyObject* sh = hi ? PyNumber_Lshift(hi, s_63) : NULL;
-      PyObject* lo = PyLong_FromUnsignedLongLong(x->combo_key);
-      ck = (sh && lo) ? PyNumber_Or(sh, lo) : NULL;
-      Py_XDECREF(hi);
-      Py_XDECREF(sh);
-      Py_XDECREF(lo);
-    }
-    if (!ck) goto fail;
-    PyObject* t = PyDict_GetItem(cache, ck); /* borrowed */
+    const size_t cslot = cmap_slot(&cache, mp, x->combo_key);
+    PyObject* t = cache.val[cslot]; /* borrowed */
     if (!t) {
       /* NodeComboKey(items=((cfg, n), ...)), shared by every (model, phase) of the combo */
-      PyObject* combo = combo_for(x->combo_key, cfgs, combos, pairs, T_combo);
+      PyObject* combo = combo_for(x->combo_key, cfgs, &combos, pairs, T_combo);
       if (!combo) goto fail;
       const int S = x->rec.num_stages, nn = x->rec.num_nodes;
-      PyObject* layers = PyTuple_New(S);
-      for (int s = 0; s < S; ++s) PyTuple_SET_ITEM(layers, s, PyLong_FromLong(x->rec.layers_per_stage[s]));
-      PyObject* son = PyTuple_New(nn);
-      for (int k = 0; k < nn; ++k) PyTuple_SET_ITEM(son, k, PyLong_FromLong(x->rec.stage_of_node[k]));
-      PyObject* pl = new_obj((PyTypeObject*)T_pl);
-      if (!pl || seta(pl, s_num_stages, PyLong_FromLong(S)) < 0 || seta(pl, s_layers, layers) < 0 ||
-          seta(pl, s_son, son) < 0)
-        goto fail;
+      /* Placement objects are immutable: one per distinct (layers, stage_of_node) */
+      uint64_t phh = 1469598103934665603ull;
+      for (int s2 = 0; s2 < S; ++s2) phh = (phh ^ x->rec.layers_per_stage[s2]) * 1099511628211ull;
+      for (int k = 0; k < nn; ++k) phh = (phh ^ (0x10000u | x->rec.stage_of_node[k])) * 1099511628211ull;
+      size_t pslot = cmap_slot(&places, S | (nn << 8), phh);
+      while (places.val[pslot] &&
+             (memcmp(places_rec[pslot]->layers_per_stage, x->rec.layers_per_stage, (size_t)S * 2) ||
+              memcmp(places_rec[pslot]->stage_of_node, x->rec.stage_of_node, (size_t)nn))) {
+        phh = phh * 6364136223846793005ull + 1442695040888963407ull;  /* hash collision: rehash */
+        pslot = cmap_slot(&places, S | (nn << 8), phh);
+      }
+      PyObject* pl = places.val[pslot];
+      if (!pl) {
+        PyObject* layers = PyTuple_New(S);
+        for (int s2 = 0; s2 < S; ++s2) PyTuple_SET_ITEM(layers, s2, PyLong_FromLong(x->rec.layers_per_stage[s2]));
+        PyObject* son = PyTuple_New(nn);
+        for (int k = 0; k < nn; ++k) PyTuple_SET_ITEM(son, k, PyLong_FromLong(x->rec.stage_of_node[k]));
+        pl = new_obj((PyTypeObject*)T_pl);
+        if (!pl || seta(pl, s_num_stages, PyLong_FromLong(S)) < 0 || seta(pl, s_layers, layers) < 0 ||
+            seta(pl, s_son, son) < 0)
+          goto fail;
+        places.tag[pslot] = S | (nn << 8);
+        places.key[pslot] = phh;
+        places.val[pslot] = pl; /* owned by the map */
+        places_rec[pslot] = &x->rec;
+      }
+      Py_INCREF(pl);
       PyObject* tmpl = new_obj((PyTypeObject*)T_tmpl);
       PyObject* mname = PyList_GetItem(mnames, m);
       PyObject* phs = PyTuple_GetItem(phases, ph);
@@ -137,11 +183,11 @@ static PyObject* materialise(PyObject* self, PyObject* args) {
           seta(tmpl, s_combo, combo) < 0 || seta(tmpl, s_placement, pl) < 0 ||
           seta(tmpl, s_tps, PyFloat_FromDouble(x->rec.throughput_tps)) < 0)
         goto fail;
-      if (PyDict_SetItem(cache, ck, tmpl) < 0) goto fail;
-      Py_DECREF(tmpl);
-      t = tmpl; /* owned by cache */
+      cache.tag[cslot] = mp;
+      cache.key[cslot] = x->combo_key;
+      cache.val[cslot] = tmpl; /* owned by the cache */
+      t = tmpl;
     }
-    Py_DECREF(ck);
     PyObject** slot = &seg_lists[(Py_ssize_t)mp * nreg + x->region];
     if (!*slot) {
       PyObject* seg = PyTuple_Pack(3, PyList_GetItem(mnames, m), PyTuple_GetItem(phases, ph),
@@ -161,16 +207,20 @@ static PyObject* materialise(PyObject* self, PyObject* args) {
     if (PyList_Append(lst, entry) < 0) goto fail;
     Py_DECREF(entry);
   }
-  Py_DECREF(cache);
-  Py_DECREF(combos);
+  cmap_free(&cache);
+  cmap_free(&combos);
+  cmap_free(&places);
+  PyMem_Free(places_rec);
   for (int k = 0; k < 512; ++k) Py_XDECREF(pairs[k]);
   PyMem_Free(seg_lists);
   PyBuffer_Release(&buf);
   return segments;
 fail:
   Py_XDECREF(segments);
-  Py_XDECREF(cache);
-  Py_XDECREF(combos);
+  cmap_free(&cache);
+  cmap_free(&combos);
+  cmap_free(&places);
+  PyMem_Free(places_rec);
   for (int k = 0; k < 512; ++k) Py_XDECREF(pairs[k]);
   PyMem_Free(seg_lists);
   PyBuffer_Release(&buf);
