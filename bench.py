@@ -305,7 +305,7 @@ def main():
     if world > 1:
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2605_04357_b200 import _native, build_frontier, catalog
-    from paper_2605_04357_b200.frontier import _local_frontier, _merge_across_ranks, _price_matrix, rank_pieces
+    from paper_2605_04357_b200.frontier import _frontier_across_ranks, _price_matrix, rank_pieces
     from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem
 
     w = catalog.WORKLOADS[args.workload]()
@@ -322,14 +322,12 @@ def main():
         h.tables()
         h.enumerate()
         if world > 1:
-            prob.counts = h.num_combos()
             pieces = rank_pieces(prob, tdist)  # memoised after the first (warm-up) step
             masks = [0] * (len(w.models) * NP)
             for mp, mk, lo, hi in pieces:
                 masks[mp] |= mk
             h.evaluate_pieces(pieces)
-            n_local = _local_frontier(prob, pmat)
-            return _merge_across_ranks(prob, n_local, tdist)
+            return _frontier_across_ranks(prob, pmat, tdist)
         h.evaluate(0, -1)
         return h.frontier(pmat)
 

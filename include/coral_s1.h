@@ -206,6 +206,19 @@ int coral_s1_frontier_merge_parts(coral_s1_handle* h, const void* dev_base, int 
  * which equals the global skyline). */
 int coral_s1_frontier_candidates(coral_s1_handle* h, int num_regions, const double* prices,
                                  int64_t* num_candidates);
+/* Multi-GPU without host round trips: the prefilter's candidates written straight into
+ * this rank's slot of an all-gather send buffer (device memory): the int64 item count at
+ * dev_part (it may exceed cap: overflow, only the first cap items are written), the
+ * items at dev_part + item_offset_bytes. Enqueued on the handle's stream; no sync. */
+int coral_s1_frontier_candidates_into(coral_s1_handle* h, int num_regions, const double* prices,
+                                      void* dev_part, int64_t item_offset_bytes, int64_t cap);
+/* The merge of a gathered buffer of such slots (part p at dev_base + p * stride_bytes),
+ * counts read on the device. *max_count = the largest part count; if it exceeds cap the
+ * merge is void (*num_survivors = -1): every rank sees the same headers, so all grow
+ * cap and repeat candidates_into + all-gather + merge. */
+int coral_s1_frontier_merge_gathered(coral_s1_handle* h, const void* dev_base, int parts,
+                                     int64_t stride_bytes, int64_t item_offset_bytes, int64_t cap,
+                                     int64_t* num_survivors, int64_t* max_count);
 
 /* ---- operator: placement_search (kernels.py:279-295), batched ----------
  * case i: counts[i*7 .. +C_i) (int64), C_i = ncfg[i] <= 7, tput rows at

@@ -115,6 +115,9 @@ def load():
             "coral_s1_table_posfrac": (C.c_int, [vp, _f64p, C.c_int64]),
             "coral_s1_frontier_merge_parts": (C.c_int, [vp, vp, C.c_int, C.c_int64, C.c_int64, _i64p, _i64p]),
             "coral_s1_frontier_candidates": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
+            "coral_s1_frontier_candidates_into": (C.c_int, [vp, C.c_int, _f64p, vp, C.c_int64, C.c_int64]),
+            "coral_s1_frontier_merge_gathered": (C.c_int, [vp, vp, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                                           _i64p, _i64p]),
             "coral_s1_kernel_timeline": (C.c_int, [vp, C.c_int64, _i32p, _i32p, _f64p, _f64p, _i64p]),
             "coral_s1_census": (C.c_int, [vp, _i64p]),
             "coral_s1_census_all": (C.c_int, [vp, _i64p, C.c_int]),
@@ -333,6 +336,22 @@ class Handle:
         n = C.c_int64()
         _check(self._lib.coral_s1_frontier_candidates(self._h, pm.shape[0], _ptr(pm, C.c_double), C.byref(n)))
         return n.value
+
+    def frontier_candidates_into(self, prices, dev_part: int, item_offset_bytes: int, cap: int) -> None:
+        """The prefilter's candidates straight into a device slot: int64 count at dev_part
+        (may exceed cap), items after item_offset_bytes. No host sync."""
+        pm = np.ascontiguousarray(prices, dtype=np.float64)
+        _check(self._lib.coral_s1_frontier_candidates_into(self._h, pm.shape[0], _ptr(pm, C.c_double),
+                                                           C.c_void_p(dev_part), item_offset_bytes, cap))
+
+    def frontier_merge_gathered(self, dev_ptr: int, parts: int, stride_bytes: int, item_offset_bytes: int,
+                                cap: int):
+        """Merge of gathered candidates_into slots, counts read on the device.
+        -> (survivors or -1 if some part overflowed cap, largest part count)."""
+        n, mx = C.c_int64(), C.c_int64()
+        _check(self._lib.coral_s1_frontier_merge_gathered(self._h, C.c_void_p(dev_ptr), parts, stride_bytes,
+                                                          item_offset_bytes, cap, C.byref(n), C.byref(mx)))
+        return n.value, mx.value
 
     def get_frontier(self, count: int):
         out = np.zeros(max(count, 1), dtype=FRONTIER_DTYPE)

@@ -111,7 +111,7 @@ struct coral_s1_handle {
   DevBuf prob, tab, flags, budget, keys, koff_d, nvalid, cand_off_d, rec, cub_tmp;
   DevBuf items, items_sorted, sort_a, sort_b, segk, scanv, flagsel, nsel, front,
       prices, ukey_s, umem_s, blkcnt, blkoff;
-  DevBuf op_in, op_out, tab_off_d, fbucket, segbuf, avars;
+  DevBuf op_in, op_out, tab_off_d, fbucket, segbuf, avars, pcounts;
   int64_t navars = 0;
   // lattice (lattice.cuh): shared state tables + per-model maxn + per-stream workspaces
   static constexpr int kStreams = 8;
@@ -1400,15 +1400,41 @@ struct FrontParts {
   int nparts, R;
   long long n[kMaxParts];     // items per part
   long long first[kMaxParts + 1];  // ordinal of each part's first item
+  // device-side counts instead (parts_counts_kernel: n at dn[p], first at dn[kMaxParts + p]),
+  // so a gathered buffer merges without a host round trip for its headers
+  const long long* dn = nullptr;
+  __device__ __forceinline__ long long cnt(int p) const { return dn ? dn[p] : n[p]; }
+  __device__ __forceinline__ long long fst(int p) const { return dn ? dn[kMaxParts + p] : first[p]; }
   __device__ __forceinline__ const coral_s1_frontier_item& item(int p, long long i) const {
     return reinterpret_cast<const coral_s1_frontier_item*>(base + p * stride + offset)[i];
   }
   __device__ __forceinline__ const coral_s1_frontier_item& by_ord(long long o) const {
     int p = 0;
-    while (p + 1 < nparts && first[p + 1] <= o) ++p;
-    return item(p, o - first[p]);
+    while (p + 1 < nparts && fst(p + 1) <= o) ++p;
+    return item(p, o - fst(p));
   }
 };
+
+constexpr int kPartsCountsLen = 2 * kMaxParts + 2;
+
+// Headers of a gathered buffer (int64 item count at base + p * stride; a count above
+// `cap` means that part overflowed its slot) -> dn: n[p] = min(count, cap), first[p],
+// and dn[2 * kMaxParts + 1] = the largest count (the host checks it for overflow).
+__global__ void parts_counts_kernel(const unsigned char* __restrict__ base, long long stride, int nparts,
+                                    long long cap, long long* __restrict__ dn) {
+  if (threadIdx.x) return;
+  long long at = 0, mx = 0;
+  for (int p = 0; p < nparts; ++p) {
+    const long long c = *reinterpret_cast<const long long*>(base + p * stride);
+    mx = c > mx ? c : mx;
+    const long long k = c < cap ? c : cap;
+    dn[p] = k;
+    dn[kMaxParts + p] = at;
+    at += k;
+  }
+  dn[kMaxParts + nparts] = at;
+  dn[2 * kMaxParts + 1] = mx;
+}
 
 // block-wide exclusive scan (sum or max) of one value per thread; 1024 threads
 template <bool kMax>
@@ -1459,7 +1485,8 @@ __global__ void __launch_bounds__(kSegThreads) front_segment_kernel(FrontParts F
   if (tid == 0) s_cnt = 0u;
   __syncthreads();
   for (int p = 0; p < F.nparts; ++p) {
-    for (long long i = tid; i < F.n[p]; i += kSegThreads) {
+    const long long np = F.cnt(p), fp = F.fst(p);
+    for (long long i = tid; i < np; i += kSegThreads) {
       const coral_s1_frontier_item& it = F.item(p, i);
       const int2 mr = *reinterpret_cast<const int2*>(&it.mp);  // (mp, region)
       if (mr.x * F.R + mr.y != seg) continue;
@@ -1469,7 +1496,7 @@ __global__ void __launch_bounds__(kSegThreads) front_segment_kernel(FrontParts F
         k.price = (unsigned long long)__double_as_longlong(it.price_usd_h);
         k.neg_t = ~(unsigned long long)__double_as_longlong(it.throughput_tps);
         k.key = it.combo_key;
-        k.s_ord = ((unsigned long long)it.rec.num_stages << 32) | (unsigned long long)(F.first[p] + i);
+        k.s_ord = ((unsigned long long)it.rec.num_stages << 32) | (unsigned long long)(fp + i);
         s_keys[pos] = k;
       }
     }
@@ -1606,10 +1633,12 @@ int frontier_from_items_general(coral_s1_handle* h, int64_t n, int R) {
 // Frontier over the items of `F` (nseg = mp x region segments): the per-segment CTA path;
 // if some segment holds more than kSegCap items, the items are made contiguous in
 // h->items (when they are not already) and the general path runs instead.
-int frontier_segments(coral_s1_handle* h, const FrontParts& F, int64_t ntot, bool items_are_contiguous) {
+int frontier_segments(coral_s1_handle* h, const FrontParts& Fin, int64_t ntot, bool items_are_contiguous,
+                      long long* dn_host = nullptr) {
   cudaStream_t st = h->stream;
   h->nfront = 0;
   if (ntot == 0) return 0;
+  FrontParts F = Fin;
   const int nseg = h->NM * h->NP * F.R;
   int rc;
   const size_t o_surv = (size_t)nseg * kSegCap * 4, o_flag = o_surv + (size_t)nseg * 4 + 16;
@@ -1625,7 +1654,14 @@ int frontier_segments(coral_s1_handle* h, const FrontParts& F, int64_t ntot, boo
   LAUNCH_CHECK(h);
   long long res[2] = {0, 0};
   CUDA_TRY(cudaMemcpyAsync(res, sb + o_flag, 16, cudaMemcpyDeviceToHost, st));
+  if (F.dn) CUDA_TRY(cudaMemcpyAsync(dn_host, F.dn, kPartsCountsLen * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  if (F.dn) {  // the counts the kernels used, for the general path below
+    for (int p = 0; p < F.nparts; ++p) { F.n[p] = dn_host[p]; F.first[p] = dn_host[kMaxParts + p]; }
+    F.first[F.nparts] = dn_host[kMaxParts + F.nparts];
+    ntot = F.first[F.nparts];
+    F.dn = nullptr;
+  }
   if ((res[0] & 0xFFFFFFFFll) == 0) {
     h->nfront = res[1];
     return 0;
@@ -1745,7 +1781,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
   DevBuf* bufs[] = {&h->prob, &h->tab, &h->flags, &h->budget, &h->keys, &h->koff_d,
                     &h->nvalid, &h->cand_off_d, &h->rec, &h->cub_tmp, &h->items, &h->items_sorted,
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
-                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->ukey_s, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->fbucket, &h->segbuf, &h->avars,
+                    &h->flagsel, &h->nsel, &h->front, &h->prices, &h->ukey_s, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->fbucket, &h->segbuf, &h->avars, &h->pcounts,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
                     &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff, &h->run_off_d, &h->run_mp_d, &h->rect, &h->tokp};
   for (DevBuf* b : bufs) b->release();
@@ -2653,7 +2689,8 @@ int coral_s1_get_records(coral_s1_handle* h, int mp, coral_s1_record* out, int64
 }
 
 static int frontier_run(coral_s1_handle* h, int num_regions, const double* prices, bool skyline,
-                        int64_t* num_survivors) {
+                        int64_t* num_survivors, void* dst_part = nullptr, int64_t dst_item_off = 0,
+                        int64_t dst_cap = 0) {
   if (!h || !h->have_eval) return fail(CORAL_S1_EINVAL, "evaluate first");
   if (num_regions < 0) return fail(CORAL_S1_EINVAL, "num_regions < 0");
   CUDA_TRY(cudaSetDevice(h->device));
@@ -2748,6 +2785,18 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
       frontier_prefix_kernel<<<(unsigned)nseg, 256, 0, st>>>(nb, h->fbucket.as<unsigned long long>());
       LAUNCH_CHECK(h);
     }
+    if (dst_part) {  // straight into the caller's slot: count at dst_part, no host round trip
+      A.items = reinterpret_cast<coral_s1_frontier_item*>(static_cast<unsigned char*>(dst_part) + dst_item_off);
+      A.cap = (unsigned long long)dst_cap;
+      A.nitems = static_cast<unsigned long long*>(dst_part);
+      CUDA_TRY(cudaMemsetAsync(dst_part, 0, 8, st));
+      frontier_items_kernel<<<gb, 256, 0, st>>>(A, shift, base, nb, h->fbucket.as<unsigned long long>());
+      LAUNCH_CHECK(h);
+      h->nfront = 0;
+      CUDA_TRY(cudaEventRecord(h->ev[7], st));
+      if (num_survivors) *num_survivors = -1;
+      return 0;
+    }
     unsigned long long ni = 0;
     for (int pass = 0; pass < 2; ++pass) {
       A.items = h->items.as<coral_s1_frontier_item>();
@@ -2783,6 +2832,51 @@ int coral_s1_frontier(coral_s1_handle* h, int num_regions, const double* prices,
 int coral_s1_frontier_candidates(coral_s1_handle* h, int num_regions, const double* prices,
                                  int64_t* num_candidates) {
   return frontier_run(h, num_regions, prices, false, num_candidates);
+}
+
+int coral_s1_frontier_candidates_into(coral_s1_handle* h, int num_regions, const double* prices, void* dev_part,
+                                      int64_t item_offset_bytes, int64_t cap) {
+  if (!dev_part || cap < 0 || item_offset_bytes < 8 || item_offset_bytes % 8)
+    return fail(CORAL_S1_EINVAL, "candidates_into: bad slot");
+  return frontier_run(h, num_regions, prices, false, nullptr, dev_part, item_offset_bytes, cap);
+}
+
+int coral_s1_frontier_merge_gathered(coral_s1_handle* h, const void* dev_base, int parts, int64_t stride_bytes,
+                                     int64_t item_offset_bytes, int64_t cap, int64_t* num_survivors,
+                                     int64_t* max_count) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  if (parts < 1 || !dev_base || cap < 0 || item_offset_bytes < 8) return fail(CORAL_S1_EINVAL, "bad parts");
+  CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  if (parts > kMaxParts) {  // headers to the host, then the host-count merge
+    std::vector<int64_t> c(parts);
+    CUDA_TRY(cudaMemcpy2DAsync(c.data(), 8, dev_base, stride_bytes, 8, parts, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int64_t mx = 0;
+    for (int64_t v : c) mx = std::max(mx, v);
+    if (max_count) *max_count = mx;
+    if (mx > cap) { h->nfront = 0; if (num_survivors) *num_survivors = -1; return 0; }
+    return coral_s1_frontier_merge_parts(h, dev_base, parts, stride_bytes, item_offset_bytes, c.data(), num_survivors);
+  }
+  int rc;
+  if ((rc = h->pcounts.ensure(kPartsCountsLen * 8))) return rc;
+  parts_counts_kernel<<<1, 32, 0, st>>>(static_cast<const unsigned char*>(dev_base), stride_bytes, parts, cap,
+                                        h->pcounts.as<long long>());
+  LAUNCH_CHECK(h);
+  FrontParts F{};
+  F.base = static_cast<const unsigned char*>(dev_base);
+  F.stride = stride_bytes;
+  F.offset = item_offset_bytes;
+  F.nparts = parts;
+  F.R = h->num_regions;
+  F.dn = h->pcounts.as<long long>();
+  long long dn[kPartsCountsLen] = {};
+  if ((rc = frontier_segments(h, F, (int64_t)parts * cap, false, dn))) return rc;
+  const long long mx = dn[2 * kMaxParts + 1];
+  if (max_count) *max_count = mx;
+  if (mx > cap) { h->nfront = 0; if (num_survivors) *num_survivors = -1; return 0; }
+  if (num_survivors) *num_survivors = h->nfront;
+  return 0;
 }
 
 int coral_s1_get_frontier(coral_s1_handle* h, coral_s1_frontier_item* out, int64_t n) {

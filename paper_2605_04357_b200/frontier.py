@@ -92,30 +92,36 @@ def _dist_info(dist):
 # partial frontier seen; every rank derives it from the same gathered headers, so all
 # ranks always agree on it without a separate exchange.
 _MERGE_CAP = [16384]
+_GATHER_BUFS: dict = {}
 
 
-def _gather_partials(n_local: int, export, tdist, device, item_bytes: int):
+def _gather_merge(fill, merge, tdist, device, item_bytes: int):
     """ONE all-gather of fixed-capacity partial frontiers (north_star: "merged with a
-    single NCCL all-gather"). Each rank sends [header | cap items]; the header's first
-    int64 is its item count. If any rank overflowed the agreed capacity (all ranks see
-    the same headers), all grow it to the next power of two and repeat once.
-    export(buffer, offset_bytes, cap) writes this rank's items. -> (recv, stride, counts)."""
+    single NCCL all-gather"), with no host round trip before it: each rank's slot is
+    [int64 count | cap items], written by fill(send, offset_bytes, cap) on the device
+    (the count may exceed cap: overflow). merge(recv, stride, offset_bytes, cap) reads
+    the counts on the device and returns (result, largest count). All ranks see the
+    same headers, so if some part overflowed all grow cap to the next power of two and
+    repeat once."""
     import torch
     world = tdist.get_world_size()
     hdr = item_bytes
     for _ in range(2):
         cap = _MERGE_CAP[0]
         stride = hdr + cap * item_bytes
-        send = torch.empty(stride, dtype=torch.uint8, device=device)
-        send[:8].view(torch.int64).fill_(n_local)
-        if n_local <= cap:
-            export(send, hdr, cap)
-        recv = torch.empty(world * stride, dtype=torch.uint8, device=device)
+        key = (str(device), world, stride)
+        bufs = _GATHER_BUFS.get(key)
+        if bufs is None:
+            _GATHER_BUFS.clear()  # one live size
+            bufs = (torch.empty(stride, dtype=torch.uint8, device=device),
+                    torch.empty(world * stride, dtype=torch.uint8, device=device))
+            _GATHER_BUFS[key] = bufs
+        send, recv = bufs
+        fill(send, hdr, cap)
         tdist.all_gather_into_tensor(recv, send)
-        counts = recv.view(world, stride)[:, :8].contiguous().view(torch.int64).view(-1).tolist()
-        mx = max(counts)
+        res, mx = merge(recv, stride, hdr, cap)
         if mx <= cap:
-            return recv, stride, counts
+            return res
         grow = 1
         while grow < mx:
             grow <<= 1
@@ -123,37 +129,44 @@ def _gather_partials(n_local: int, export, tdist, device, item_bytes: int):
     raise RuntimeError("partial frontier capacity did not converge")
 
 
-def _local_frontier(prob: Stage1Problem, pmat) -> int:
-    """A rank's share of the frontier for the merge: its exactly prefiltered candidates
-    (items no strictly cheaper item of the shard dominates). The skyline is taken once,
-    over the union, in the merge; the skyline of the union of prefiltered shards is the
-    global skyline, because every dropped item's dominator is itself in the union or
-    dominated by a kept, cheaper one."""
-    return prob.h.frontier_candidates(pmat)
-
-
-def _merge_across_ranks(prob: Stage1Problem, n_local: int, tdist) -> int:
-    """Single all-gather of the partial frontiers, then the same skyline over their
-    union on every rank (associative: all ranks end identical)."""
+def _frontier_across_ranks(prob: Stage1Problem, pmat, tdist) -> int:
+    """Each rank's exactly prefiltered candidates (items no strictly cheaper item of the
+    shard dominates) go straight into its all-gather slot; after the single all-gather
+    every rank takes the same skyline over the union (associative: all ranks end
+    identical). The skyline of the union of prefiltered shards is the global skyline,
+    because every dropped item's dominator is itself in the union or dominated by a
+    kept, cheaper one. One host sync per step: the merge's survivor count."""
     import torch
     dev = torch.device("cuda", prob.h.device)
     item = _native.FRONTIER_DTYPE.itemsize
+    world = tdist.get_world_size()
 
-    def export(buf, offset, cap):
-        prob.h.frontier_export_device(buf.data_ptr() + offset, cap)
+    def fill(send, offset, cap):
+        prob.h.frontier_candidates_into(pmat, send.data_ptr(), offset, cap)
 
-    recv, stride, counts = _gather_partials(n_local, export, tdist, dev, item)
-    return prob.h.frontier_merge_parts(recv.data_ptr(), stride, item, counts)
+    def merge(recv, stride, offset, cap):
+        return prob.h.frontier_merge_gathered(recv.data_ptr(), world, stride, offset, cap)
+
+    return _gather_merge(fill, merge, tdist, dev, item)
 
 
 _CALIBRATION: dict = {}
+_PIECES: dict = {}
 
 
 def rank_pieces(prob: Stage1Problem, tdist) -> list:
     """This rank's evaluation pieces (shard.plan_pieces): (model, phase, S)
     units, the largest split by candidate range, balanced on costs measured once per
     problem on rank 0 (shard.calibrate) and broadcast, so every rank derives the same
-    plan. Needs the problem's tables and enumeration."""
+    plan. Needs the problem's tables and enumeration. Memoised on the problem's
+    signature (its inputs fix the candidate counts): a repeat solve enqueues its
+    evaluation without reading the counts back first."""
+    world, rank = tdist.get_world_size(), tdist.get_rank()
+    pkey = (prob.signature(), world, rank)
+    hit = _PIECES.get(pkey)
+    if hit is not None:
+        return hit
+    prob.counts = prob.h.num_combos()
     NP = len(prob.phases)
     _, lsteps, smax = prob.h.table_layout()
     smax_mp = [min(int(smax[mp // NP]), int(lsteps[mp // NP])) if prob.counts[mp // NP] else 0
@@ -169,8 +182,10 @@ def rank_pieces(prob: Stage1Problem, tdist) -> list:
             tdist.broadcast_object_list(box, src=0)
             costs = box[0]
         _CALIBRATION[key] = costs
-    plan = plan_pieces(costs, tdist.get_world_size())
-    return pieces_to_ranges(plan[tdist.get_rank()], prob.counts, NP)
+    plan = plan_pieces(costs, world)
+    pieces = pieces_to_ranges(plan[rank], prob.counts, NP)
+    _PIECES[pkey] = pieces
+    return pieces
 
 
 def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,
@@ -191,14 +206,13 @@ def build_frontier(configs, models, slos, caps, prices, regions=None, ctx=None,
     if tdist is not None:
         prob.h.tables()
         prob.h.enumerate()
-        prob.counts = prob.h.num_combos()
+        prob.h.evaluate_pieces(rank_pieces(prob, tdist))
+        n = _frontier_across_ranks(prob, pmat, tdist)
+        prob.counts = prob.h.num_combos()  # ready by now: no wait
         NP = len(prob.phases)
         prob.cand_off = np.zeros(len(prob.models) * NP + 1, dtype=np.int64)
         for mp in range(len(prob.models) * NP):
             prob.cand_off[mp + 1] = prob.cand_off[mp] + prob.counts[mp // NP]
-        prob.h.evaluate_pieces(rank_pieces(prob, tdist))
-        n_local = _local_frontier(prob, pmat)
-        n = _merge_across_ranks(prob, n_local, tdist)
     else:
         prob.run()
         n = prob.h.frontier(pmat)

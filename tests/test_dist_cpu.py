@@ -118,8 +118,9 @@ def test_two_rank_gloo_protocol_matches_single_process():
 
 
 def _gather_worker(rank, world, port, out):
-    """The frontier merge's single all-gather (frontier._gather_partials) over gloo:
-    fixed-capacity parts with a count header, capacity regrown on overflow."""
+    """The frontier merge's single all-gather (frontier._gather_merge) over gloo:
+    fixed-capacity parts with a count header written by the producer (it may exceed
+    the capacity), counts read by the merge, capacity regrown on overflow."""
     import torch
     from paper_2605_04357_b200 import _native, frontier
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -132,11 +133,16 @@ def _gather_worker(rank, world, port, out):
     mine["combo_key"] = np.arange(n_local) * 7 + rank
     raw = torch.from_numpy(mine.view(np.uint8).copy())
 
-    def export(buf, offset, cap):
-        assert n_local <= cap
-        buf[offset:offset + raw.numel()].copy_(raw)
+    def fill(buf, offset, cap):
+        buf[:8].view(torch.int64).fill_(n_local)  # the true count, even past cap
+        k = min(n_local, cap)
+        buf[offset:offset + k * item].copy_(raw[:k * item])
 
-    recv, stride, counts = frontier._gather_partials(n_local, export, dist, torch.device("cpu"), item)
+    def merge(recv, stride, offset, cap):
+        counts = recv.view(world, stride)[:, :8].contiguous().view(torch.int64).view(-1).tolist()
+        return (recv.clone(), stride, counts), max(counts)
+
+    recv, stride, counts = frontier._gather_merge(fill, merge, dist, torch.device("cpu"), item)
     parts = []
     for r, c in enumerate(counts):
         blob = recv[r * stride + item: r * stride + item + c * item].numpy().tobytes()

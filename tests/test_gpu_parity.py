@@ -575,3 +575,27 @@ def test_pieces_split_by_candidate_range_merge_equal_single_gpu(name, W):
         dbuf = torch.from_numpy(buf).cuda()
         n = prob.h.frontier_merge_parts(dbuf.data_ptr(), stride, item, [len(c) for c in cands])
         assert prob.h.get_frontier(n).tobytes() == full
+        # the product's path: each rank's candidates straight into its device slot
+        # (count header written on the device), merged on device-read counts; a slot
+        # too small reports the overflow instead of a frontier
+        mx = max(len(c) for c in cands)
+        for cap2, ok in ((max(mx - 1, 0), mx == 0), (mx, True), (mx + 37, True)):
+            stride2 = item + cap2 * item
+            gath = torch.zeros(len(cands) * stride2, dtype=torch.uint8, device="cuda")
+            for r in range(len(rank_plans)):
+                prob.h.evaluate_pieces(pieces_to_ranges(rank_plans[r], prob.counts, NP))
+                prob.h.frontier_candidates_into(pm, gath.data_ptr() + r * stride2, item, cap2)
+            n2, got_mx = prob.h.frontier_merge_gathered(gath.data_ptr(), len(cands), stride2, item, cap2)
+            assert got_mx == mx
+            if ok:
+                assert prob.h.get_frontier(n2).tobytes() == full
+            else:
+                assert n2 == -1
+        # more parts than the device-count path holds (32): headers read on the host
+        stride2 = item + mx * item
+        gath = torch.zeros(40 * stride2, dtype=torch.uint8, device="cuda")
+        for r in range(len(rank_plans)):
+            prob.h.evaluate_pieces(pieces_to_ranges(rank_plans[r], prob.counts, NP))
+            prob.h.frontier_candidates_into(pm, gath.data_ptr() + (39 - r) * stride2, item, mx)
+        n2, got_mx = prob.h.frontier_merge_gathered(gath.data_ptr(), 40, stride2, item, mx)
+        assert got_mx == mx and prob.h.get_frontier(n2).tobytes() == full

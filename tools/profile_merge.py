@@ -1,6 +1,8 @@
 """Per-phase wall time of the multi-GPU merge (torchrun): after a barrier (so waiting
-for the slowest rank is excluded) time the candidates export, the all-gather and the
-merge on every rank. python -m torch.distributed.run --nproc-per-node N tools/profile_merge.py"""
+for the slowest rank is excluded) time the candidates pass straight into the gather
+slot, the all-gather and the device-count merge on every rank -- once with a sync
+between the phases (breakdown) and once as the product runs them (one sync at the end).
+python -m torch.distributed.run --nproc-per-node N tools/profile_merge.py [workload]"""
 import os
 import sys
 import time
@@ -12,7 +14,7 @@ import torch  # noqa: E402
 import torch.distributed as tdist  # noqa: E402
 
 from paper_2605_04357_b200 import _native, catalog  # noqa: E402
-from paper_2605_04357_b200.frontier import _gather_partials, _price_matrix, rank_pieces  # noqa: E402
+from paper_2605_04357_b200.frontier import _frontier_across_ranks, _gather_merge, _price_matrix, rank_pieces  # noqa: E402
 from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem  # noqa: E402
 
 
@@ -32,7 +34,6 @@ def main():
         t0 = time.perf_counter()
         prob.h.tables()
         prob.h.enumerate()
-        prob.counts = prob.h.num_combos()
         pieces = rank_pieces(prob, tdist)
         t1 = time.perf_counter()
         prob.h.evaluate_pieces(pieces)
@@ -42,23 +43,36 @@ def main():
         tdist.barrier()
         torch.cuda.synchronize()
         t = [time.perf_counter()]
-        n_local = prob.h.frontier_candidates(pm)
-        t.append(time.perf_counter())
+        world = tdist.get_world_size()
+        gat = {}
 
-        def export(buf, offset, cap):
-            prob.h.frontier_export_device(buf.data_ptr() + offset, cap)
+        def fill(send, offset, cap):
+            prob.h.frontier_candidates_into(pm, send.data_ptr(), offset, cap)
+            torch.cuda.synchronize()
+            t.append(time.perf_counter())
 
-        recv, stride, counts = _gather_partials(n_local, export, tdist, dev, item)
-        t.append(time.perf_counter())
-        n = prob.h.frontier_merge_parts(recv.data_ptr(), stride, item, counts)
+        def merge(recv, stride, offset, cap):
+            torch.cuda.synchronize()
+            t.append(time.perf_counter())
+            gat["counts"] = recv.view(world, stride)[:, :8].contiguous().view(torch.int64).view(-1).tolist()
+            return prob.h.frontier_merge_gathered(recv.data_ptr(), world, stride, offset, cap)
+
+        n = _gather_merge(fill, merge, tdist, dev, item)
         torch.cuda.synchronize()
         t.append(time.perf_counter())
+        tdist.barrier()
+        torch.cuda.synchronize()
+        t5 = time.perf_counter()
+        n2 = _frontier_across_ranks(prob, pm, tdist)
+        torch.cuda.synchronize()
+        t6 = time.perf_counter()
+        assert n2 == n
         if it == 5:
             d = np.diff(t) * 1e3
             print(f"rank {tdist.get_rank()}: pieces {len(pieces)} | tables+enum+plan {1e3 * (t1 - t0):.3f} ms "
-                  f"evaluate wall {1e3 * (t2 - t1):.3f} device {ev:.3f} ms | n_local {n_local} gathered "
-                  f"{sum(counts)} survivors {n} | candidates {d[0]:.3f} ms gather {d[1]:.3f} ms merge {d[2]:.3f} ms",
-                  flush=True)
+                  f"evaluate wall {1e3 * (t2 - t1):.3f} device {ev:.3f} ms | parts {gat['counts']} survivors {n} | "
+                  f"candidates {d[0]:.3f} ms gather {d[1]:.3f} ms merge {d[2]:.3f} ms | "
+                  f"unsynced total {1e3 * (t6 - t5):.3f} ms", flush=True)
     tdist.destroy_process_group()
 
 

@@ -17,9 +17,12 @@ KIND = {0: "top", 1: "layer", 2: "value", 3: "decode", 4: "ranks"}
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    serial = "--serial" in sys.argv
     w = catalog.WORKLOADS[name]()
     prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho),
                          GenContext(perf=w.perf, granularity=w.granularity))
+    if serial:
+        prob.h.set_streams(1)
     for _ in range(3):
         prob.run()
     torch.cuda.synchronize()
@@ -43,7 +46,18 @@ def main():
     for k, _, b, e in tl:
         per[KIND[k]] = per.get(KIND[k], 0.0) + (e - b)
     print("summed event ms per kind:", {k: round(v, 3) for k, v in per.items()})
-
+    if serial:  # per (model, phase) chain alone: ms per kind, candidates, layers
+        per_mp = {}
+        for k, mp, ms in prob.h.kernel_launches(4096):
+            d = per_mp.setdefault(mp, {})
+            d[KIND[k]] = d.get(KIND[k], 0.0) + ms
+        NP = len(prob.phases)
+        for mp in sorted(per_mp):
+            m = prob.models[mp // NP]
+            n = int(prob.cand_off[mp + 1] - prob.cand_off[mp]) if hasattr(prob, "cand_off") else -1
+            d = per_mp[mp]
+            print(f"mp {mp} {m.name:14s} L={m.num_layers:3d} cand={n:7d} total={sum(d.values()):.3f} " +
+                  " ".join(f"{k}={v:.3f}" for k, v in sorted(d.items())))
 
 def KIND_ABBR(k):
     return {"top": "T", "layer": "L", "value": "V", "decode": "D", "ranks": "R"}[k]
