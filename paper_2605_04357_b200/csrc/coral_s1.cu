@@ -134,7 +134,7 @@ struct coral_s1_handle {
   std::vector<unsigned char> flags_h;
   std::vector<char> model_used;
   std::vector<char> own_mp;  // (model, phase) chains with records from the last evaluate
-  DevBuf run_off_d, run_mp_d;
+  DevBuf run_off_d, run_mp_d, run_ph_d;
   DevBuf tokp;  // [R][512] token prices of the last frontier
   DevBuf rect;  // per candidate: the record's throughput (0 = no template), for the frontier passes
   std::vector<double> memb_h, wbytes_h;  // config memory bytes, model weight bytes
@@ -643,18 +643,25 @@ __device__ __forceinline__ void top_pair(const double* __restrict__ gv, const do
   if (g1 <= h1) { cand = g1; cj = 1; return; }
   if (gm >= hm) { cand = hm; cj = jmax; return; }
   if ((g1 < hm ? g1 : hm) <= floor) { cand = kNegInf; cj = 0; return; }
+  // h(lo) and g(hi) of the final bracket are tracked instead of re-loaded: g(jmax) is
+  // in the summary and g(J + 1) == 0 (J is the row's last positive column, values are
+  // >= 0), so g(hi) is always known; h(lo) is known for lo == 1 or a probed lo
   int lo = 1, hi = jmax;
+  double vhi = gm, vlo = h1;
+  bool lo_known = true;
   if (cap) {
     hi = min(jmax, J + 1);
     lo = max(1, min(min(J, l - K - 1), hi - 1));
+    if (hi < jmax) vhi = 0.0;
+    lo_known = lo == 1;
   }
   const double* __restrict__ hl = hv + l;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (gv[mid] > hl[-mid]) lo = mid; else hi = mid;
+    const double gmid = gv[mid], hmid = hl[-mid];
+    if (gmid > hmid) { lo = mid; vlo = hmid; lo_known = true; } else { hi = mid; vhi = gmid; }
   }
-  const double vlo = hl[-lo];
-  const double vhi = gv[hi];
+  if (!lo_known) vlo = hl[-lo];
   if (vlo >= vhi) { cand = vlo; cj = lo; } else { cand = vhi; cj = hi; }
 }
 
@@ -889,31 +896,25 @@ struct FrontArgs {
   coral_s1_frontier_item* items;
   unsigned long long* nitems;
   unsigned long long cap = 0;      // items capacity (frontier_items_kernel counts past it)
-  // the prefilter passes run over the (model, phase) chains this device evaluated: run k
-  // (slot run_mp[k]) owns blocks run_boff[k] .. run_boff[k+1] - 1, 256 candidates each
+  // the prefilter passes run over the models this device evaluated (one or both of
+  // their phases): run k (model run_mp[k], phase mask run_ph[k]) owns blocks
+  // run_boff[k] .. run_boff[k+1] - 1, kFrontBlock of the model's candidates each
   const int64_t* run_boff = nullptr;
   const double* rect = nullptr;    // per candidate: the record's throughput, 0 = no template
   const int64_t* run_off = nullptr;
   const int* run_mp = nullptr;
+  const unsigned char* run_ph = nullptr;
   int nrun = 0;
   int64_t ntot = 0;
 };
 
-// One candidate of the frontier passes: its (model, phase), packed key, tokens and
-// record, fetched once and priced per region (thread per candidate, regions in a loop).
-struct FrontCand {
-  int mp, C;
-  unsigned long long key;
-  double T;      // the record's throughput (the full record is re-read for survivors only)
-  int64_t ri;    // record index
-  unsigned tok[kMaxC];  // packed tokens ((rank + 1) << 3 | count), combo order
-};
+// The frontier passes: thread t of a block serves the model candidates base + k * 256 + t,
+// k < kFrontItems (coalesced per k; all loads issued before the dependent pricing). A
+// candidate's key is read and priced once for both phases -- a combo costs the same in
+// both -- and its records' throughputs come from the compact per-phase arrays (8 B), the
+// 32-byte records being re-read for survivors only.
+constexpr int kFrontPhases = 2, kFrontItems = 4, kFrontBlock = 256 * kFrontItems;
 
-// Token prices of every region, tp[r * 512 + token] = count x the config's price in
-// region r (rn_mul on the host: the same IEEE product allocation.py:97 computes as n * p;
-// NaN when the config is unpriced there, which then propagates through the sum), read
-// through the read-only cache: one load + add per token instead of a config lookup, a
-// price load and a multiply.
 // The block's run (one binary search per block, not per thread).
 __device__ __forceinline__ int frontier_block_run(const FrontArgs& A) {
   __shared__ int s_run;
@@ -928,36 +929,53 @@ __device__ __forceinline__ int frontier_block_run(const FrontArgs& A) {
   __syncthreads();
   return s_run;
 }
-// false when the thread is past its run's end or the candidate has no template
-__device__ __forceinline__ bool frontier_cand(const FrontArgs& A, int run, FrontCand& f) {
-  const int mp = A.run_mp[run];
-  const int64_t idx = ((int64_t)blockIdx.x - A.run_boff[run]) * blockDim.x + threadIdx.x;  // within (model, phase)
-  if (idx >= A.cand_off[mp + 1] - A.cand_off[mp]) return false;
-  f.ri = A.cand_off[mp] + idx;
-  // the compact throughput array (8 B), not the 32-byte record: the full record is read
-  // for survivors only
-  f.T = A.rect[f.ri];
-  if (!(f.T > 0.0)) return false;  // no template
-  f.mp = mp;
-  const int m = mp / A.P.NP;
-  f.key = A.keys[A.koff[m] + idx];
-  // tokens are contiguous from the top: unrolled, so they stay in registers
-  f.C = 0;
+
+// This thread's candidates of the block's run: model m, the index of the first, and per
+// item the phase throughputs (0 = no template or phase not evaluated here) and the key
+// (0 when no phase has a template).
+struct FrontItems {
+  int m;
+  int64_t idx0;
+  double T[kFrontItems][kFrontPhases];
+  unsigned long long key[kFrontItems];
+};
+__device__ __forceinline__ void frontier_load(const FrontArgs& A, FrontItems& F) {
+  const int run = frontier_block_run(A);
+  const int m = A.run_mp[run];
+  const unsigned own = A.run_ph[run];
+  const int NP = A.P.NP;
+  F.m = m;
+  F.idx0 = ((int64_t)blockIdx.x - A.run_boff[run]) * kFrontBlock + threadIdx.x;
+  const int64_t n = A.cand_off[m * NP + 1] - A.cand_off[m * NP];
 #pragma unroll
-  for (int t = 0; t < kMaxC; ++t) {
-    f.tok[t] = (unsigned)(f.key >> (kKeyTokenBits * (kMaxC - 1 - t))) & 511u;
-    f.C += f.tok[t] != 0u;
+  for (int k = 0; k < kFrontItems; ++k) {
+    const int64_t idx = F.idx0 + (int64_t)k * 256;
+#pragma unroll
+    for (int p = 0; p < kFrontPhases; ++p)
+      F.T[k][p] = (idx < n && p < NP && ((own >> p) & 1u)) ? A.rect[A.cand_off[m * NP + p] + idx] : 0.0;
   }
-  return true;
+#pragma unroll
+  for (int k = 0; k < kFrontItems; ++k) {
+    const int64_t idx = F.idx0 + (int64_t)k * 256;
+    F.key[k] = (F.T[k][0] > 0.0 || F.T[k][1] > 0.0) ? A.keys[A.koff[m] + idx] : 0ull;
+  }
 }
+// Token prices of every region, tp[r * 512 + token] = count x the config's price in
+// region r (rn_mul on the host: the same IEEE product allocation.py:97 computes as n * p;
+// NaN when the config is unpriced there, which then propagates through the sum), read
+// through the read-only cache: one load + add per token instead of a config lookup, a
+// price load and a multiply.
 // allocation.py:91-98 _template_price of the candidate in region r (combo order,
-// sequential); false when a config is not offered there (price None)
-__device__ __forceinline__ bool frontier_price(const FrontArgs& A, const FrontCand& f, int r, double& total) {
+// sequential); false when a config is not offered there (price None). Tokens are
+// contiguous from the top of the key: the first zero token ends the combo.
+__device__ __forceinline__ bool frontier_price(const FrontArgs& A, unsigned long long key, int r, double& total) {
   total = 0.0;
   const double* __restrict__ row = A.tok_price + r * 512;
 #pragma unroll
-  for (int c = 0; c < kMaxC; ++c)
-    if (c < f.C) total = rn_add(total, __ldg(row + f.tok[c]));
+  for (int c = 0; c < kMaxC; ++c) {
+    const unsigned tok = (unsigned)(key >> (kKeyTokenBits * (kMaxC - 1 - c))) & 511u;
+    if (tok) total = rn_add(total, __ldg(row + tok));
+  }
   return !isnan(total);
 }
 __device__ __forceinline__ unsigned long long dbits(double x) {
@@ -974,19 +992,28 @@ __device__ __forceinline__ int bucket_of(double price, int shift, unsigned long 
 }
 
 // pass 1: per (segment, price bucket) the max throughput (bit pattern, T > 0)
-__global__ void frontier_bucket_kernel(FrontArgs A, int shift, unsigned long long base, int nb,
-                                       unsigned long long* __restrict__ bmax) {
-  FrontCand f;
-  if (!frontier_cand(A, frontier_block_run(A), f)) return;
-  const unsigned long long tb = dbits(f.T);
-  for (int r = 0; r < A.R; ++r) {
-    double price;
-    if (!frontier_price(A, f, r, price)) continue;
-    const int b = bucket_of(price, shift, base, nb);
-    // most items do not raise their bucket: read first (an unconditional atomic per item
-    // serialises on the hot buckets, 2.5x slower at config 5)
-    unsigned long long* slot = bmax + ((int64_t)f.mp * A.R + r) * nb + b;
-    if (*slot < tb) atomicMax(slot, tb);
+__global__ void __launch_bounds__(256) frontier_bucket_kernel(FrontArgs A, int shift, unsigned long long base,
+                                                              int nb, unsigned long long* __restrict__ bmax) {
+  FrontItems F;
+  frontier_load(A, F);
+  const int NP = A.P.NP;
+#pragma unroll
+  for (int k = 0; k < kFrontItems; ++k) {
+    if (!F.key[k]) continue;
+    for (int r = 0; r < A.R; ++r) {
+      double price;
+      if (!frontier_price(A, F.key[k], r, price)) continue;
+      const int b = bucket_of(price, shift, base, nb);
+#pragma unroll
+      for (int p = 0; p < kFrontPhases; ++p) {
+        if (!(F.T[k][p] > 0.0)) continue;
+        const unsigned long long tb = dbits(F.T[k][p]);
+        // most items do not raise their bucket: read first (an unconditional atomic per
+        // item serialises on the hot buckets, 2.5x slower at config 5)
+        unsigned long long* slot = bmax + ((int64_t)(F.m * NP + p) * A.R + r) * nb + b;
+        if (*slot < tb) atomicMax(slot, tb);
+      }
+    }
   }
 }
 // pass 2: exclusive prefix max over the buckets of each segment (block per segment)
@@ -1012,32 +1039,41 @@ __global__ void frontier_prefix_kernel(int nb, unsigned long long* __restrict__ 
 // pass 3: write the items that can still be on the frontier: T must exceed every
 // throughput of a strictly cheaper bucket, else a cheaper candidate dominates it
 // (SURVEY.md 8c keep rule: T > running max of the earlier items).
-__global__ void frontier_items_kernel(FrontArgs A, int shift, unsigned long long base, int nb,
-                                      const unsigned long long* __restrict__ pmax) {
-  FrontCand f;
-  const bool valid = frontier_cand(A, frontier_block_run(A), f);
+__global__ void __launch_bounds__(256) frontier_items_kernel(FrontArgs A, int shift, unsigned long long base,
+                                                             int nb, const unsigned long long* __restrict__ pmax) {
+  FrontItems F;
+  frontier_load(A, F);
   const int lane = threadIdx.x & 31;
-  for (int r = 0; r < A.R; ++r) {  // uniform over the warp: ballots stay converged
-    double price = 0.0;
-    bool keep = valid && frontier_price(A, f, r, price);
-    if (keep && nb > 0) {
-      const int b = bucket_of(price, shift, base, nb);
-      keep = dbits(f.T) > pmax[((int64_t)f.mp * A.R + r) * nb + b];
-    }
-    const unsigned ballot = __ballot_sync(0xffffffffu, keep);
-    if (!ballot) continue;
-    unsigned long long pos = 0;
-    if (lane == __ffs(ballot) - 1) pos = atomicAdd(A.nitems, (unsigned long long)__popc(ballot));
-    pos = __shfl_sync(0xffffffffu, pos, __ffs(ballot) - 1);
-    if (keep && pos + __popc(ballot & ((1u << lane) - 1u)) < A.cap) {  // bounded buffer: count the rest
-      coral_s1_frontier_item it;
-      it.price_usd_h = price;
-      it.throughput_tps = f.T;
-      it.combo_key = f.key;
-      it.mp = f.mp;
-      it.region = r;
-      it.rec = A.rec[f.ri];
-      A.items[pos + __popc(ballot & ((1u << lane) - 1u))] = it;
+  const int NP = A.P.NP;
+#pragma unroll
+  for (int k = 0; k < kFrontItems; ++k) {
+    if (!__any_sync(0xffffffffu, F.key[k] != 0ull)) continue;  // warp-uniform
+    for (int r = 0; r < A.R; ++r) {  // uniform over the warp: ballots stay converged
+      double price = 0.0;
+      const bool priced = F.key[k] && frontier_price(A, F.key[k], r, price);
+      const int b = priced && nb > 0 ? bucket_of(price, shift, base, nb) : 0;
+#pragma unroll
+      for (int p = 0; p < kFrontPhases; ++p) {
+        if (p >= NP) break;
+        const int mp = F.m * NP + p;
+        bool keep = priced && F.T[k][p] > 0.0;
+        if (keep && nb > 0) keep = dbits(F.T[k][p]) > pmax[((int64_t)mp * A.R + r) * nb + b];
+        const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+        if (!ballot) continue;
+        unsigned long long pos = 0;
+        if (lane == __ffs(ballot) - 1) pos = atomicAdd(A.nitems, (unsigned long long)__popc(ballot));
+        pos = __shfl_sync(0xffffffffu, pos, __ffs(ballot) - 1);
+        if (keep && pos + __popc(ballot & ((1u << lane) - 1u)) < A.cap) {  // bounded buffer: count the rest
+          coral_s1_frontier_item it;
+          it.price_usd_h = price;
+          it.throughput_tps = F.T[k][p];
+          it.combo_key = F.key[k];
+          it.mp = mp;
+          it.region = r;
+          it.rec = A.rec[A.cand_off[mp] + F.idx0 + (int64_t)k * 256];
+          A.items[pos + __popc(ballot & ((1u << lane) - 1u))] = it;
+        }
+      }
     }
   }
 }
@@ -1783,7 +1819,7 @@ int coral_s1_destroy(coral_s1_handle* h) {
                     &h->sort_a, &h->sort_b, &h->segk, &h->scanv,
                     &h->flagsel, &h->nsel, &h->front, &h->prices, &h->ukey_s, &h->umem_s, &h->blkcnt, &h->blkoff, &h->op_in, &h->op_out, &h->tab_off_d, &h->fbucket, &h->segbuf, &h->avars, &h->pcounts,
                     &h->lat_base_d, &h->lat_binom_d, &h->lat_key, &h->lat_nsub, &h->lat_off,
-                    &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff, &h->run_off_d, &h->run_mp_d, &h->rect, &h->tokp};
+                    &h->lat_sub, &h->lat_maxn, &h->census, &h->poscnt, &h->prep_tmp, &h->lat_flags_h, &h->lat_sums, &h->lat_soff, &h->run_off_d, &h->run_mp_d, &h->run_ph_d, &h->rect, &h->tokp};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < coral_s1_handle::kStreams; ++i) {
     h->ws_value[i].release(); h->ws_f0[i].release(); h->ws_ch[i].release(); h->ws_ranks[i].release();
@@ -2724,23 +2760,33 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
     A.items = h->items.as<coral_s1_frontier_item>();
     A.nitems = h->nsel.as<unsigned long long>();
     int64_t nblocks = 0;
-    {  // only the chains this device evaluated (all of them on one GPU), 256 per block
+    {  // only the models this device evaluated (all of them on one GPU), 256 per block;
+       // a run serves the model's evaluated phases together
+      if (h->NP > kFrontPhases) return fail(CORAL_S1_EUNSUPPORTED, "frontier: at most 2 phases");
       std::vector<int64_t> boff(1, 0);
-      std::vector<int> rmp;
-      int64_t tot = 0;
-      for (int mp = 0; mp < A.NMP; ++mp) {
-        const int64_t c = h->cand_off[mp + 1] - h->cand_off[mp];
-        if (!c || (mp < (int)h->own_mp.size() && !h->own_mp[mp])) continue;
-        rmp.push_back(mp);
-        boff.push_back(boff.back() + (c + 255) / 256);
-        tot += c;
+      std::vector<int> rm;
+      std::vector<unsigned char> rph;
+      for (int m = 0; m < h->NM; ++m) {
+        const int64_t c = h->counts[m];
+        unsigned char ph = 0;
+        for (int p = 0; p < h->NP; ++p) {
+          const int mp = m * h->NP + p;
+          if (mp >= (int)h->own_mp.size() || h->own_mp[mp]) ph |= (unsigned char)(1u << p);
+        }
+        if (!c || !ph) continue;
+        rm.push_back(m);
+        rph.push_back(ph);
+        boff.push_back(boff.back() + (c + kFrontBlock - 1) / kFrontBlock);
       }
-      if (rmp.empty()) { rmp.push_back(0); boff.push_back(0); }  // non-empty device arrays
-      if ((rc = upload(h, h->run_off_d, boff)) || (rc = upload(h, h->run_mp_d, rmp))) return rc;
+      if (rm.empty()) { rm.push_back(0); rph.push_back(0); boff.push_back(0); }  // non-empty device arrays
+      rph.resize((rph.size() + 7) & ~size_t(7), 0);
+      if ((rc = upload(h, h->run_off_d, boff)) || (rc = upload(h, h->run_mp_d, rm)) ||
+          (rc = upload(h, h->run_ph_d, rph)))
+        return rc;
       A.run_boff = h->run_off_d.as<int64_t>();
       A.run_mp = h->run_mp_d.as<int>();
-      A.nrun = (int)rmp.size();
-      A.ntot = tot;
+      A.run_ph = h->run_ph_d.as<unsigned char>();
+      A.nrun = (int)rm.size();
       A.rect = h->rect.as<double>();
       nblocks = boff.back();
       std::vector<double> tp((size_t)std::max(num_regions, 1) * 512, 0.0);
@@ -2758,7 +2804,7 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
     // the filter exact), so it comes from the price matrix on the host: a combo costs at
     // least the cheapest offered config and at most n_max x the dearest (with margin for
     // rounding; bucket indices are clamped, which keeps the map non-decreasing).
-    const unsigned gb = (unsigned)std::max<int64_t>(nblocks, 1);  // thread per candidate, regions looped
+    const unsigned gb = (unsigned)std::max<int64_t>(nblocks, 1);  // kFrontItems candidates per thread, regions looped
     unsigned long long range[2] = {~0ull, 0ull};
     {
       double pmin = HUGE_VAL, pmax = 0.0;

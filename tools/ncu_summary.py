@@ -12,8 +12,11 @@ KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Hit Rate", "
         "L1/TEX Cache Throughput", "L2 Cache Throughput", "DRAM Frequency", "SM Frequency"]
 
 
+KERNEL = []  # optional: --kernel-name regex:<argv[3]> (one kernel of a multi-kernel report)
+
+
 def ncu(rep, *args):
-    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", rep, *KERNEL, *args], capture_output=True, text=True).stdout
 
 
 def main(rep, nlines=25):
@@ -35,7 +38,17 @@ def main(rep, nlines=25):
                      "smsp__inst_executed.sum", "l1tex__t_bytes.sum"):
                 print(f"{k:40s} {x:>14s} {raw[1][h.index(k)]}")
     rows = list(csv.reader(io.StringIO(ncu(rep, "--page", "source", "--csv"))))
-    hdr, data = rows[1], rows[2:]
+    at = next(i for i, r in enumerate(rows) if "Source" in r and "Warp Stall Sampling (All Samples)" in r)
+    hdr = rows[at]
+    ci = hdr.index("Warp Stall Sampling (All Samples)")
+
+    def num(x):
+        try:
+            float(x or 0)
+            return True
+        except ValueError:
+            return False
+    data = [r for r in rows[at + 1:] if len(r) == len(hdr) and num(r[ci])]
     ix = {c: i for i, c in enumerate(hdr)}
     col = "Warp Stall Sampling (All Samples)"
     tot = sum(float(r[ix[col]] or 0) for r in data) or 1.0
@@ -51,4 +64,6 @@ def main(rep, nlines=25):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 3:
+        KERNEL[:] = ["--kernel-name", "regex:" + sys.argv[3]]
     main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)

@@ -1,6 +1,6 @@
 """Per-stream timeline of one warm c2 evaluate (CUDA events around each lattice launch).
 
-  python tools/timeline.py [workload]
+  python tools/timeline.py [workload] [--serial] [--zigzag]
 """
 import os
 import sys
@@ -19,8 +19,13 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
     serial = "--serial" in sys.argv
     w = catalog.WORKLOADS[name]()
-    prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho),
-                         GenContext(perf=w.perf, granularity=w.granularity))
+    ctx = GenContext(perf=w.perf, granularity=w.granularity)
+    if "--zigzag" in sys.argv:  # tests/helpers.zigzag_profile: non-monotone rows on two configs
+        from paper_2605_04357_b200.specs import ProfileTable
+        from tests.helpers import zigzag_profile
+        ctx = GenContext(perf=w.perf, granularity=w.granularity,
+                         profile=zigzag_profile(w.configs, w.models, ProfileTable))
+    prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho), ctx)
     if serial:
         prob.h.set_streams(1)
     for _ in range(3):
@@ -28,7 +33,14 @@ def main():
     torch.cuda.synchronize()
     tl = prob.h.kernel_timeline()
     ev = prob.h.stage_ms()["evaluate"]
-    print(f"evaluate {ev:.3f} ms, {len(tl)} timed launches")
+    print(f"evaluate {ev:.3f} ms, {len(tl)} timed launches; stages", {k: round(v, 3) for k, v in prob.h.stage_ms().items()})
+    import time
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prob.run()
+    torch.cuda.synchronize()
+    print(f"prob.run() wall {1e3 * (time.perf_counter() - t0):.3f} ms; stages",
+          {k: round(v, 3) for k, v in prob.h.stage_ms().items()})
     for slot in sorted({s for _, s, _, _ in tl}):
         row = [(b, e, KIND[k]) for k, s, b, e in tl if s == slot]
         print(f"stream {slot}: " + " ".join(f"{KIND_ABBR(k)}[{b:.2f}-{e:.2f}]" for b, e, k in row))
