@@ -288,19 +288,25 @@ __device__ __forceinline__ void model_window(const DevProblem& P, int m, double&
   hi = rn_mul(P.rho, wbytes);
 }
 
+// Both passes count and compact per 128-element chunk (one warp's share of a block):
+// chunk c = elements c * 128 .. c * 128 + 127, so the compaction needs no block-wide
+// scan, no shared-memory staging and no barrier -- a warp's survivors of a model go out
+// at the chunk's scanned offset in 4 coalesced stores.
+constexpr int kEnumChunk = 32 * kEnumItems, kEnumChunksPerBlock = kEnumBlock / kEnumChunk;
+
 // pass 1: thread t of block b unranks elements b * 1024 + 4t .. +3 (key order), stores
 // their keys and memory sums (16 B each, read once by pass 2) and counts each model's
-// window survivors per block: blkcnt[m * nblk + b] (model-major)
+// window survivors per chunk: chkcnt[m * nchunk + c] (model-major)
 __global__ void __launch_bounds__(kEnumThreads) enum_count_kernel(
-    DevProblem P, int64_t U, int nblk, unsigned long long* __restrict__ ukey, double* __restrict__ umem,
-    unsigned long long* __restrict__ blkcnt) {
+    DevProblem P, int64_t U, int64_t nchunk, unsigned long long* __restrict__ ukey, double* __restrict__ umem,
+    unsigned long long* __restrict__ chkcnt) {
   __shared__ unsigned long long s_binom[kEnumBinomRows][8];
-  extern __shared__ unsigned s_wcnt[];  // [NM] window counts of this block
   const int rows = min(kEnumBinomRows, P.K + P.n_max + 1);
   for (int i = threadIdx.x; i < rows * 8; i += blockDim.x) s_binom[i >> 3][i & 7] = c_binom[i >> 3][i & 7];
-  for (int m = threadIdx.x; m < P.NM; m += blockDim.x) s_wcnt[m] = 0u;
   __syncthreads();
+  const int lane = threadIdx.x & 31;
   const int64_t e0 = (int64_t)blockIdx.x * kEnumBlock + (int64_t)threadIdx.x * kEnumItems;
+  const int64_t chunk = (int64_t)blockIdx.x * kEnumChunksPerBlock + (threadIdx.x >> 5);
   unsigned long long k4[kEnumItems];
   double m4[kEnumItems];
 #pragma unroll
@@ -321,6 +327,7 @@ __global__ void __launch_bounds__(kEnumThreads) enum_count_kernel(
         umem[e0 + k] = m4[k];
       }
   }
+  if (chunk >= nchunk) return;  // warp-uniform
   for (int m = 0; m < P.NM; ++m) {
     double lo, hi;
     model_window(P, m, lo, hi);
@@ -328,81 +335,55 @@ __global__ void __launch_bounds__(kEnumThreads) enum_count_kernel(
 #pragma unroll
     for (int k = 0; k < kEnumItems; ++k) c += lo <= m4[k] && m4[k] < hi;
     c = __reduce_add_sync(0xffffffffu, c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_wcnt[m], (unsigned)c);
+    if (lane == (m & 31)) chkcnt[(int64_t)m * nchunk + chunk] = (unsigned long long)c;
   }
-  __syncthreads();
-  for (int m = threadIdx.x; m < P.NM; m += blockDim.x) blkcnt[(int64_t)m * nblk + blockIdx.x] = s_wcnt[m];
 }
 
-// pass 2: ONE read of the block's keys and memory sums, then every model's stable
-// compaction at its scanned block offset (element order = thread-major, as pass 1),
-// staged in shared memory so that each model's survivors leave in one coalesced store
+// pass 2: ONE read of the chunk's keys and memory sums (element c * 128 + 32k + lane:
+// coalesced), then every model's stable compaction at its scanned chunk offset: per k a
+// ballot, and the warp's survivors of that k land contiguously (coalesced store)
 __global__ void __launch_bounds__(kEnumThreads) window_select_kernel(
     DevProblem P, int64_t U, const unsigned long long* __restrict__ ukey, const double* __restrict__ umem,
-    int nblk, const unsigned long long* __restrict__ blkoff, unsigned long long* __restrict__ keys) {
-  __shared__ int s_warp[2][kEnumThreads / 32];
-  __shared__ unsigned long long s_keys[2][kEnumBlock];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t e0 = (int64_t)blockIdx.x * kEnumBlock + (int64_t)threadIdx.x * kEnumItems;
+    int64_t nchunk, const unsigned long long* __restrict__ chkoff, unsigned long long* __restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t chunk = (int64_t)blockIdx.x * kEnumChunksPerBlock + (threadIdx.x >> 5);
+  if (chunk >= nchunk) return;
+  const int64_t e0 = chunk * kEnumChunk + lane;
   unsigned long long k4[kEnumItems];
   double m4[kEnumItems];
-  if (e0 + kEnumItems <= U) {
-    const ulonglong2 a = reinterpret_cast<const ulonglong2*>(ukey + e0)[0];
-    const ulonglong2 b = reinterpret_cast<const ulonglong2*>(ukey + e0)[1];
-    const double2 c = reinterpret_cast<const double2*>(umem + e0)[0];
-    const double2 d = reinterpret_cast<const double2*>(umem + e0)[1];
-    k4[0] = a.x; k4[1] = a.y; k4[2] = b.x; k4[3] = b.y;
-    m4[0] = c.x; m4[1] = c.y; m4[2] = d.x; m4[3] = d.y;
-  } else {
 #pragma unroll
-    for (int k = 0; k < kEnumItems; ++k) {
-      k4[k] = e0 + k < U ? ukey[e0 + k] : 0ull;
-      m4[k] = e0 + k < U ? umem[e0 + k] : -1.0;
-    }
+  for (int k = 0; k < kEnumItems; ++k) {
+    const int64_t e = e0 + 32 * k;
+    k4[k] = e < U ? ukey[e] : 0ull;
+    m4[k] = e < U ? umem[e] : -1.0;
   }
+  const unsigned lt = (1u << lane) - 1u;
   for (int m = 0; m < P.NM; ++m) {
     double lo, hi;
     model_window(P, m, lo, hi);
-    unsigned pass = 0u;
-    int c = 0;
+    unsigned bal[kEnumItems];
+    int tot = 0;
 #pragma unroll
     for (int k = 0; k < kEnumItems; ++k) {
-      const bool in = lo <= m4[k] && m4[k] < hi;
-      pass |= (unsigned)in << k;
-      c += in;
+      bal[k] = __ballot_sync(0xffffffffu, lo <= m4[k] && m4[k] < hi);
+      tot += __popc(bal[k]);
     }
-    int incl = c;  // inclusive scan of the per-thread counts over the warp
+    if (!tot) continue;  // warp-uniform
+    unsigned long long* out = keys + chkoff[(int64_t)m * nchunk + chunk];
+    int at = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+    for (int k = 0; k < kEnumItems; ++k) {
+      if ((bal[k] >> lane) & 1u) out[at + __popc(bal[k] & lt)] = k4[k];
+      at += __popc(bal[k]);
     }
-    const int buf = m & 1;  // double-buffered warp totals and staged keys
-    if (lane == 31) s_warp[buf][warp] = incl;
-    __syncthreads();
-    int before = 0, total = 0;
-#pragma unroll
-    for (int w = 0; w < kEnumThreads / 32; ++w) {
-      before += w < warp ? s_warp[buf][w] : 0;
-      total += s_warp[buf][w];
-    }
-    if (!total) continue;  // uniform over the block
-    // stage the block's survivors in order, then one coalesced store of all of them
-    int pos = before + incl - c;
-#pragma unroll
-    for (int k = 0; k < kEnumItems; ++k)
-      if ((pass >> k) & 1u) s_keys[buf][pos++] = k4[k];
-    __syncthreads();
-    unsigned long long* out = keys + blkoff[(int64_t)m * nblk + blockIdx.x];
-    for (int i = threadIdx.x; i < total; i += kEnumThreads) out[i] = s_keys[buf][i];
   }
 }
 
-// per-model survivor counts from the scanned block offsets (offset array has NM*nblk+1)
-__global__ void window_totals_kernel(int NM, int nblk, const unsigned long long* __restrict__ blkoff,
+// per-model survivor counts from the scanned chunk offsets (offset array has NM*nchunk+1)
+__global__ void window_totals_kernel(int NM, int64_t nchunk, const unsigned long long* __restrict__ chkoff,
                                      unsigned long long* __restrict__ nvalid) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m < NM) nvalid[m] = blkoff[(int64_t)(m + 1) * nblk] - blkoff[(int64_t)m * nblk];
+  if (m < NM) nvalid[m] = chkoff[(int64_t)(m + 1) * nchunk] - chkoff[(int64_t)m * nchunk];
 }
 
 
@@ -2037,14 +2018,15 @@ int coral_s1_enumerate(coral_s1_handle* h) {
   h->koff.assign(NM + 1, 0);
   if (NM > 0 && U > 0) {
     const int nblk = (int)((U + kEnumBlock - 1) / kEnumBlock);
-    const int64_t nb = (int64_t)NM * nblk;
+    const int64_t nchunk = (U + kEnumChunk - 1) / kEnumChunk;
+    const int64_t nb = (int64_t)NM * nchunk;
     if ((rc = h->ukey_s.ensure(U * 8)) || (rc = h->umem_s.ensure(U * 8)) ||
         (rc = h->blkcnt.ensure((nb + 1) * 8)) || (rc = h->blkoff.ensure((nb + 1) * 8)))
       return rc;
     // the universe once, unranked in key order: keys + memory sums + per-model window
     // counts per block; one scan -> block offsets and model totals
-    enum_count_kernel<<<(unsigned)nblk, kEnumThreads, (size_t)NM * sizeof(unsigned), st>>>(
-        h->dp, U, nblk, h->ukey_s.as<unsigned long long>(), h->umem_s.as<double>(),
+    enum_count_kernel<<<(unsigned)nblk, kEnumThreads, 0, st>>>(
+        h->dp, U, nchunk, h->ukey_s.as<unsigned long long>(), h->umem_s.as<double>(),
         h->blkcnt.as<unsigned long long>());
     LAUNCH_CHECK(h);
     CUDA_TRY(cudaMemsetAsync(h->blkcnt.as<unsigned long long>() + nb, 0, 8, st));
@@ -2054,7 +2036,7 @@ int coral_s1_enumerate(coral_s1_handle* h) {
     if ((rc = ensure_tmp(h, tmp))) return rc;
     CUDA_TRY(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, h->blkcnt.as<unsigned long long>(),
                                            h->blkoff.as<unsigned long long>(), (int)(nb + 1), st));
-    window_totals_kernel<<<(NM + 127) / 128, 128, 0, st>>>(NM, nblk, h->blkoff.as<unsigned long long>(),
+    window_totals_kernel<<<(NM + 127) / 128, 128, 0, st>>>(NM, nchunk, h->blkoff.as<unsigned long long>(),
                                                            h->nvalid.as<unsigned long long>());
     LAUNCH_CHECK(h);
     h->launches += 2;
@@ -2078,7 +2060,7 @@ int coral_s1_enumerate(coral_s1_handle* h) {
     if (nk > 0) {  // model-major, str(combo) order within a model: the library order
       CUDA_TRY(cudaEventRecord(h->ev_ws[0], st));
       window_select_kernel<<<(unsigned)nblk, kEnumThreads, 0, st>>>(
-          h->dp, U, h->ukey_s.as<unsigned long long>(), h->umem_s.as<double>(), nblk,
+          h->dp, U, h->ukey_s.as<unsigned long long>(), h->umem_s.as<double>(), nchunk,
           h->blkoff.as<unsigned long long>(), h->keys.as<unsigned long long>());
       LAUNCH_CHECK(h);
       CUDA_TRY(cudaEventRecord(h->ev_ws[1], st));

@@ -18,7 +18,7 @@ def main():
     w = catalog.WORKLOADS[name]()
     prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho),
                          GenContext(perf=w.perf, granularity=w.granularity))
-    ms, wall = [], []
+    ms, wall, wsm = [], [], []
     for _ in range(int(os.environ.get("ENUM_ITERS", "5"))):
         prob.h.tables()
         torch.cuda.synchronize()
@@ -27,13 +27,14 @@ def main():
         t1 = time.perf_counter()
         torch.cuda.synchronize()
         ms.append(prob.h.stage_ms()["enumerate"])
+        wsm.append(prob.h.window_select_stats()[0])
         wall.append(1e3 * (t1 - t0))
     prob.counts = prob.h.num_combos()
     sha = hashlib.sha256()
     for m in range(len(w.models)):
         sha.update(prob.keys(m).tobytes())
     print(f"{name} enumerate ms: {' '.join(f'{x:.3f}' for x in ms)}  host call ms: "
-          f"{' '.join(f'{x:.3f}' for x in wall)}  combos {sum(prob.h.num_combos())} digest {sha.hexdigest()[:16]}")
+          f"{' '.join(f'{x:.3f}' for x in wall)}  window_select ms: {' '.join(f'{x:.3f}' for x in wsm)}  combos {sum(prob.h.num_combos())} digest {sha.hexdigest()[:16]}")
 
 
 if __name__ == "__main__":
