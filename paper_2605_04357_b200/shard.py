@@ -189,7 +189,8 @@ def calibrate(handle, nmp: int, smax_mp, num_phases: int = 2) -> tuple:
         handle.set_streams(0)
 
 
-CONCURRENT = 0.85  # a rank runs its (model, phase) slots on up to 4 streams at once
+CONCURRENT = 0.92  # a rank runs its (model, phase) slots on up to 4 streams at once
+#                   (tools/plan_check.py: two big slots overlap to ~0.90-0.93 of their sum)
 
 
 def _rank_load(pieces, F, L, T):
@@ -266,11 +267,25 @@ def _plan_pieces(costs, world, max_depth):
                     peak = max(nh, nr)
                     if peak < loads[hi] - 1e-6 and (best is None or peak < best[0]):
                         best = (peak, "split", p, r)
+            # (c) swap it with a piece of another rank
+            for r in range(world):
+                if r == hi:
+                    continue
+                for q in ranks[r]:
+                    nh, nr = load(hi, extra=(q,), drop=(p,)), load(r, extra=(p,), drop=(q,))
+                    peak = max(nh, nr)
+                    if peak < loads[hi] - 1e-6 and (best is None or peak < best[0]):
+                        best = (peak, "swap", p, (r, q))
         if best is None:
             break
         _, kind, p, r = best
         ranks[hi].remove(p)
-        if kind == "move":
+        if kind == "swap":
+            r, q = r
+            ranks[r].remove(q)
+            ranks[r].append(p)
+            ranks[hi].append(q)
+        elif kind == "move":
             ranks[r].append(p)
         else:
             mp, S, a, b = p
