@@ -293,6 +293,11 @@ int coral_s1_kernel_stats(const coral_s1_handle* h, int kind, double* total_ms, 
  * enumerate's window_select_kernel, the per-model memory-window compaction of
  * templates.py:110-111 (bench roofline of the streaming path); ms = -1 if none ran */
 int coral_s1_window_select_stats(const coral_s1_handle* h, double* ms, int64_t* alg_bytes);
+/* per-launch timing events of the lattice kernels (kernel_stats / kernel_timeline /
+ * kernel_launches read them): off by default -- the evaluate then records no
+ * per-launch events -- on for diagnostics, the bench roofline pass and the multi-GPU
+ * cost calibration */
+int coral_s1_set_timing(coral_s1_handle* h, int on);
 /* per-launch timeline of the last evaluate's lattice kernels (kinds as above plus
  * 3 decode, 4 sub-multiset ranks): side-stream slot and begin/end in ms from the
  * evaluate's start event; up to cap launches, count in *n (diagnostics) */

@@ -112,6 +112,7 @@ def load():
             "coral_s1_kernel_stats": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
             "coral_s1_window_select_stats": (C.c_int, [vp, _f64p, _i64p]),
             "coral_s1_set_census": (C.c_int, [vp, C.c_int]),
+            "coral_s1_set_timing": (C.c_int, [vp, C.c_int]),
             "coral_s1_table_posfrac": (C.c_int, [vp, _f64p, C.c_int64]),
             "coral_s1_frontier_merge_parts": (C.c_int, [vp, vp, C.c_int, C.c_int64, C.c_int64, _i64p, _i64p]),
             "coral_s1_frontier_candidates": (C.c_int, [vp, C.c_int, _f64p, _i64p]),
@@ -394,6 +395,11 @@ class Handle:
             _ptr(best, C.c_double), _ptr(sj, C.c_int64), _ptr(sc, C.c_int64)))
         return best, sj, sc
 
+    def set_timing(self, on: bool) -> None:
+        """Per-launch timing events of the lattice kernels (kernel_stats / _timeline /
+        _launches); off by default (no event records in the evaluate)."""
+        _check(self._lib.coral_s1_set_timing(self._h, 1 if on else 0))
+
     def set_census(self, on: bool) -> None:
         _check(self._lib.coral_s1_set_census(self._h, 1 if on else 0))
 
@@ -548,6 +554,9 @@ def release(h: Handle) -> None:
     if any(x is h for x in free):
         return
     if len(free) < _POOL_KEEP:
+        h.set_timing(False)  # per-lease diagnostics settings do not carry over
+        h.set_census(False)
+        h.set_streams(0)
         free.append(h)
     else:
         h.close()

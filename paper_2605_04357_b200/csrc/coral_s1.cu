@@ -147,6 +147,7 @@ struct coral_s1_handle {
   int tkind[kTimedMax] = {};
   int tslot[kTimedMax] = {};
   int tmp[kTimedMax] = {};   // (model, phase) slot of the launch (rank tables: the model's first)
+  bool timing = false;       // per-launch events on (coral_s1_set_timing); off: no event records
   int cur_mp = -1;
   int ntimed = 0;
   cudaEvent_t ev[8] = {};
@@ -2169,6 +2170,7 @@ static int launch_percombo(coral_s1_handle* h, cudaStream_t st, int64_t lo, int6
 // (0 = lat_top_kernel, 1 = lat_layer_kernel, 2 = lat_value_kernel, 3 = lat_decode_kernel,
 // 4 = lat_ranks_kernel).
 static int timed_begin(coral_s1_handle* h, cudaStream_t st, int kind, int mp = -2) {
+  if (!h->timing) return -1;  // two event records per launch cost ~2 us of host time each
   if (h->ntimed >= coral_s1_handle::kTimedMax) return -1;
   const int i = h->ntimed;
   if (!h->tev[i][0] && (cudaEventCreate(&h->tev[i][0]) != cudaSuccess || cudaEventCreate(&h->tev[i][1]) != cudaSuccess))
@@ -3426,6 +3428,12 @@ int coral_s1_census_all(coral_s1_handle* h, int64_t* out, int n) {
     CUDA_TRY(cudaMemcpy(v, h->census.p, 32, cudaMemcpyDeviceToHost));
   }
   for (int i = 0; i < n && i < 4; ++i) out[i] = (int64_t)v[i];
+  return 0;
+}
+
+int coral_s1_set_timing(coral_s1_handle* h, int on) {
+  if (!h) return fail(CORAL_S1_EINVAL, "null handle");
+  h->timing = on != 0;
   return 0;
 }
 

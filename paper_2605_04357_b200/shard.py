@@ -146,6 +146,7 @@ def calibrate(handle, nmp: int, smax_mp, num_phases: int = 2) -> tuple:
     """Measure (F, L, T) per (model, phase) slot on this device (see above): one serial
     evaluation per stage count S, each launch attributed to its slot."""
     handle.set_streams(1)
+    handle.set_timing(True)
     try:
         maxS = max(smax_mp) if len(smax_mp) else 0
         F = [0.0] * nmp
@@ -187,6 +188,7 @@ def calibrate(handle, nmp: int, smax_mp, num_phases: int = 2) -> tuple:
         return tuple(F), tuple(tuple(sorted(d.items())) for d in L), tuple(tuple(sorted(d.items())) for d in T)
     finally:
         handle.set_streams(0)
+        handle.set_timing(False)
 
 
 CONCURRENT = 0.92  # a rank runs its (model, phase) slots on up to 4 streams at once

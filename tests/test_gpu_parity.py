@@ -481,6 +481,7 @@ def test_lattice_workspace_beyond_device_memory(streams, monkeypatch):
     limit = 1 if streams == 0 else int((per_stream * streams + reserve) / 0.9) + (1 << 20)
     monkeypatch.setenv("CORAL_S1_MEM_LIMIT", str(limit))
     fresh = _native.Handle(0)
+    fresh.set_timing(True)  # per-launch events: which stream each layer launch ran on
     monkeypatch.setitem(_native._pool, 0, [fresh])
     lib = build_library(configs, models, slos, caps, ctx)
     assert [template_line(t) for t in lib.entries] == golden("library_core.json.gz")["records"]
@@ -509,6 +510,7 @@ def test_non_monotone_profile_rows_stay_on_the_lattice(w):
     ctxp = GenContext(perf=ctx.perf, profile=zigzag_profile(configs, models, ProfileTable))
     prob = Stage1Problem(configs, models, slos, caps, ctxp)
     prob.run()
+    prob.h.set_timing(True)  # per-launch events: which kernels ran
     t0 = time.perf_counter()
     prob.run()
     import torch

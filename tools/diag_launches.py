@@ -6,6 +6,7 @@ w = catalog.WORKLOADS["extended"]()
 prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf)).run()
 h = prob.h
 h.set_streams(1)
+h.set_timing(True)
 for S in (1, 2, 4):
     for rep in range(2):
         h.evaluate_pieces([(mp, 1 << S, 0, -1) for mp in range(12)])

@@ -33,6 +33,7 @@ def run(name):
                          GenContext(perf=w.perf, granularity=w.granularity))
     _, pm = _price_matrix(prob.configs, w.prices, w.regions)
     prob.h.set_streams(1)
+    prob.h.set_timing(True)
     prob.run()
     prob.h.frontier(pm)
     per_solve = {k: prob.h.kernel_stats(k)[1] for k in (0, 1)}

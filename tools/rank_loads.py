@@ -21,6 +21,7 @@ def main():
     worlds = [int(a) for a in sys.argv[1:]] or [2, 4]
     w = catalog.extended_workload()
     prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho), GenContext(perf=w.perf))
+    prob.h.set_timing(True)
     prob.h.tables()
     prob.h.enumerate()
     counts = prob.h.num_combos()

@@ -26,6 +26,7 @@ def main():
         ctx = GenContext(perf=w.perf, granularity=w.granularity,
                          profile=zigzag_profile(w.configs, w.models, ProfileTable))
     prob = Stage1Problem(w.configs, w.models, w.slos, LibraryCaps(w.n_max, w.rho), ctx)
+    prob.h.set_timing(True)
     if serial:
         prob.h.set_streams(1)
     for _ in range(3):
