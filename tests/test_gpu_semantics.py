@@ -202,3 +202,40 @@ def test_sweep_raises_like_build_library_and_cmd_sweep():
     with pytest.raises(KeyError):
         sweep([FAST, SLOW], [big], {"big": SLO}, [LibraryCaps(3, 12.0)], {("r", FAST.name): 2.0},
               regions=["r"], ctx=CTX)
+
+
+def test_per_launch_timing_is_opt_in_and_reset_on_release(monkeypatch):
+    """coral_s1_set_timing: the evaluate records per-launch events only when asked (the
+    default path records none); a handle returned to the pool forgets the diagnostics
+    settings of its last lease (timing, census, streams)."""
+    from paper_2605_04357_b200 import _native
+    from paper_2605_04357_b200.library import Stage1Problem
+    from tests.helpers import workload
+    configs, models, slos, caps, ctx, regions, prices = workload("core")
+    monkeypatch.setitem(_native._pool, 0, [])  # an empty pool: the released handle comes back
+    prob = Stage1Problem(configs, models, slos, caps, ctx)
+    prob.run()
+    assert prob.h.kernel_timeline() == []
+    prob.h.set_timing(True)
+    prob.run()
+    tl = prob.h.kernel_timeline()
+    assert tl and {k for k, _, _, _ in tl} >= {0, 1, 2, 3}
+    assert all(e >= b >= 0.0 for _, _, b, e in tl)
+    h = prob.h
+    prob.h.set_census(True)
+    prob.h.set_streams(1)
+    prob.close()
+    again = _native.acquire(h.device)
+    try:
+        assert again is h
+        from paper_2605_04357_b200.library import _pack_problem
+        arrays, scalars = _pack_problem(sorted(configs, key=lambda c: c.name), models, slos,
+                                        ("prefill", "decode"), caps, ctx)
+        again.set_problem(arrays, scalars)
+        again.tables()
+        again.enumerate()
+        again.evaluate(0, -1)
+        assert again.kernel_timeline() == []
+        assert again.census_all() == [0, 0, 0, 0]
+    finally:
+        _native.release(again)
