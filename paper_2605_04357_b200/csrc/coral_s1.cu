@@ -624,7 +624,9 @@ __device__ __forceinline__ void top_pair(const double* __restrict__ gv, const do
                                          int jmax, bool cap, double floor, double& cand, int& cj) {
   if (g1 <= h1) { cand = g1; cj = 1; return; }
   if (gm >= hm) { cand = hm; cj = jmax; return; }
-  if ((g1 < hm ? g1 : hm) <= floor) { cand = kNegInf; cj = 0; return; }
+  // the bound min(g(1), h(jmax)) holds for exactly monotone rows only (cap): rows
+  // monotone within 1e-12 may exceed it by that much
+  if (cap && (g1 < hm ? g1 : hm) <= floor) { cand = kNegInf; cj = 0; return; }
   // h(lo) and g(hi) of the final bracket are tracked instead of re-loaded: g(jmax) is
   // in the summary and g(J + 1) == 0 (J is the row's last positive column, values are
   // >= 0), so g(hi) is always known; h(lo) is known for lo == 1 or a probed lo
