@@ -2731,6 +2731,13 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
       (rc = h->nsel.ensure(32)))
     return rc;
   int64_t n = 0;
+  if (dst_part && nmax == 0) {  // nothing to price: an empty slot (count 0)
+    CUDA_TRY(cudaMemsetAsync(dst_part, 0, 8, st));
+    h->nfront = 0;
+    CUDA_TRY(cudaEventRecord(h->ev[7], st));
+    if (num_survivors) *num_survivors = -1;
+    return 0;
+  }
   if (nmax > 0) {
     CUDA_TRY(cudaMemsetAsync(h->nsel.p, 0, 8, st));
     FrontArgs A;

@@ -601,3 +601,17 @@ def test_pieces_split_by_candidate_range_merge_equal_single_gpu(name, W):
             prob.h.frontier_candidates_into(pm, gath.data_ptr() + (39 - r) * stride2, item, mx)
         n2, got_mx = prob.h.frontier_merge_gathered(gath.data_ptr(), 40, stride2, item, mx)
         assert got_mx == mx and prob.h.get_frontier(n2).tobytes() == full
+
+
+def test_candidates_into_empty_price_matrix_writes_an_empty_slot():
+    """The multi-GPU slot path with nothing to price (no regions): the count header is
+    still written (0), so the all-gather never carries a stale count."""
+    import torch
+    from paper_2605_04357_b200 import _native
+    configs, models, slos, caps, ctx, regions, prices = workload("c1")
+    prob = Stage1Problem(configs, models, slos, caps, ctx).run()
+    item = _native.FRONTIER_DTYPE.itemsize
+    slot = torch.full((item + 4 * item,), 0xFF, dtype=torch.uint8, device="cuda")
+    prob.h.frontier_candidates_into(np.zeros((0, len(configs))), slot.data_ptr(), item, 4)
+    torch.cuda.synchronize()
+    assert slot[:8].view(torch.int64).item() == 0
