@@ -652,7 +652,7 @@ __device__ __forceinline__ void top_pair(const double* __restrict__ gv, const do
 // kSlots code slots per lane (codes lane + 1 + 32k): 2 for candidates of <= 6 nodes
 // (M <= 64), 4 when a model has 7-node candidates (M <= 128).
 template <int kSlots, bool kScan>
-__global__ void __launch_bounds__(256, 5) lat_top_kernel(TopArgs A) {
+__global__ void __launch_bounds__(256, 6) lat_top_kernel(TopArgs A) {
   const int lane = threadIdx.x & 31;
   const long long ci = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= A.ncombo) return;
