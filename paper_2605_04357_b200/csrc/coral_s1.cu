@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
@@ -59,9 +60,15 @@ constexpr int kKeyTokenBits = 9;
 
 __constant__ unsigned long long c_binom[160][8];  // C(N, k), N < 160, k <= 7
 
+inline unsigned long long next_alloc_id() {  // process-wide, never reused
+  static std::atomic<unsigned long long> n{0};
+  return ++n;
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  unsigned long long id = 0;  // changes with every allocation (a freed address may come back)
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -75,12 +82,14 @@ struct DevBuf {
     cudaError_t e = cudaMalloc(&p, want);
     if (e != cudaSuccess) return fail(CORAL_S1_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     cap = want;
+    id = next_alloc_id();
     return 0;
   }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
+    id = 0;
   }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
@@ -136,6 +145,8 @@ struct coral_s1_handle {
   std::vector<char> own_mp;  // (model, phase) chains with records from the last evaluate
   DevBuf run_off_d, run_mp_d, run_ph_d;
   DevBuf tokp;  // [R][512] token prices of the last frontier
+  std::vector<unsigned char> tokp_shadow, runph_shadow;  // upload_same: bytes last copied
+  unsigned long long tokp_at = 0, runph_at = 0;  // DevBuf ids the shadows belong to
   DevBuf rect;  // per candidate: the record's throughput (0 = no template), for the frontier passes
   std::vector<double> memb_h, wbytes_h;  // config memory bytes, model weight bytes
   std::vector<int> inv_rank_h;           // str rank -> config index
@@ -1719,6 +1730,21 @@ int upload(coral_s1_handle* h, DevBuf& buf, const std::vector<T>& v, cudaStream_
   return 0;
 }
 
+// upload() that skips the copy when the buffer still holds exactly these bytes (the
+// frontier's token-price table and run masks repeat call after call for one market)
+template <class T>
+int upload_same(coral_s1_handle* h, DevBuf& buf, const std::vector<T>& v, std::vector<unsigned char>& shadow,
+                unsigned long long& shadow_id) {
+  const size_t nb = v.size() * sizeof(T);
+  if (buf.id && buf.id == shadow_id && shadow.size() == nb && (nb == 0 || !std::memcmp(shadow.data(), v.data(), nb)))
+    return 0;
+  int rc = upload(h, buf, v);
+  if (rc) return rc;
+  shadow.assign(reinterpret_cast<const unsigned char*>(v.data()), reinterpret_cast<const unsigned char*>(v.data()) + nb);
+  shadow_id = buf.id;
+  return 0;
+}
+
 int64_t universe_size(int K, int n_max) {
   // sum_{n=1}^{n_max} C(K+n-1, n)
   int64_t tot = 0;
@@ -2726,8 +2752,7 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
   // buffer is bounded: it starts at 1 Mi items, the items pass counts past its end, and
   // only an overflow grows it (to the exact count) and re-runs that pass
   const int64_t icap0 = std::max<int64_t>(std::min<int64_t>(nmax, 1 << 20), (int64_t)(h->items.cap / sizeof(coral_s1_frontier_item)));
-  if ((rc = upload(h, h->prices, pv)) ||
-      (rc = h->items.ensure(std::max<int64_t>(icap0, 1) * sizeof(coral_s1_frontier_item))) ||
+  if ((rc = h->items.ensure(std::max<int64_t>(icap0, 1) * sizeof(coral_s1_frontier_item))) ||
       (rc = h->nsel.ensure(32)))
     return rc;
   int64_t n = 0;
@@ -2748,7 +2773,7 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
     A.NMP = h->NM * h->NP;
     A.rec = h->rec.as<coral_s1_record>();
     A.ncand = h->ncand;
-    A.prices = h->prices.as<double>();
+    A.prices = nullptr;  // the passes price through the token table (tok_price)
     A.R = num_regions;
     A.items = h->items.as<coral_s1_frontier_item>();
     A.nitems = h->nsel.as<unsigned long long>();
@@ -2774,7 +2799,7 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
       if (rm.empty()) { rm.push_back(0); rph.push_back(0); boff.push_back(0); }  // non-empty device arrays
       rph.resize((rph.size() + 7) & ~size_t(7), 0);
       if ((rc = upload(h, h->run_off_d, boff)) || (rc = upload(h, h->run_mp_d, rm)) ||
-          (rc = upload(h, h->run_ph_d, rph)))
+          (rc = upload_same(h, h->run_ph_d, rph, h->runph_shadow, h->runph_at)))
         return rc;
       A.run_boff = h->run_off_d.as<int64_t>();
       A.run_mp = h->run_mp_d.as<int>();
@@ -2789,7 +2814,7 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
           if (rank1 >= 1 && rank1 <= h->K && cnt > 0)
             tp[(size_t)r * 512 + tok] = (double)cnt * pv[(size_t)r * h->K + h->inv_rank_h[rank1 - 1]];
         }
-      if ((rc = upload(h, h->tokp, tp))) return rc;
+      if ((rc = upload_same(h, h->tokp, tp, h->tokp_shadow, h->tokp_at))) return rc;
       A.tok_price = h->tokp.as<double>();
     }
     // exact prefilter: per (segment, price bucket) max T -> prefix max. The bucket range
