@@ -69,6 +69,9 @@ struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
   unsigned long long id = 0;  // changes with every allocation (a freed address may come back)
+  // upload_same: the bytes last copied in (host-written, device-read-only buffers only)
+  std::vector<unsigned char> shadow;
+  unsigned long long shadow_id = 0;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -145,8 +148,6 @@ struct coral_s1_handle {
   std::vector<char> own_mp;  // (model, phase) chains with records from the last evaluate
   DevBuf run_off_d, run_mp_d, run_ph_d;
   DevBuf tokp;  // [R][512] token prices of the last frontier
-  std::vector<unsigned char> tokp_shadow, runph_shadow;  // upload_same: bytes last copied
-  unsigned long long tokp_at = 0, runph_at = 0;  // DevBuf ids the shadows belong to
   DevBuf rect;  // per candidate: the record's throughput (0 = no template), for the frontier passes
   std::vector<double> memb_h, wbytes_h;  // config memory bytes, model weight bytes
   std::vector<int> inv_rank_h;           // str rank -> config index
@@ -1730,18 +1731,20 @@ int upload(coral_s1_handle* h, DevBuf& buf, const std::vector<T>& v, cudaStream_
   return 0;
 }
 
-// upload() that skips the copy when the buffer still holds exactly these bytes (the
-// frontier's token-price table and run masks repeat call after call for one market)
+// upload() that skips the copy when the buffer still holds exactly these bytes: for the
+// host-written, device-read-only tables a repeat solve re-sends unchanged (offsets, run
+// lists, the frontier's token prices); the allocation id guards against a freed
+// address coming back
 template <class T>
-int upload_same(coral_s1_handle* h, DevBuf& buf, const std::vector<T>& v, std::vector<unsigned char>& shadow,
-                unsigned long long& shadow_id) {
+int upload_same(coral_s1_handle* h, DevBuf& buf, const std::vector<T>& v, cudaStream_t st = nullptr) {
   const size_t nb = v.size() * sizeof(T);
-  if (buf.id && buf.id == shadow_id && shadow.size() == nb && (nb == 0 || !std::memcmp(shadow.data(), v.data(), nb)))
+  if (buf.id && buf.id == buf.shadow_id && buf.shadow.size() == nb &&
+      (nb == 0 || !std::memcmp(buf.shadow.data(), v.data(), nb)))
     return 0;
-  int rc = upload(h, buf, v);
+  int rc = upload(h, buf, v, st);
   if (rc) return rc;
-  shadow.assign(reinterpret_cast<const unsigned char*>(v.data()), reinterpret_cast<const unsigned char*>(v.data()) + nb);
-  shadow_id = buf.id;
+  buf.shadow.assign(reinterpret_cast<const unsigned char*>(v.data()), reinterpret_cast<const unsigned char*>(v.data()) + nb);
+  buf.shadow_id = buf.id;
   return 0;
 }
 
@@ -1969,7 +1972,7 @@ int coral_s1_tables(coral_s1_handle* h) {
       (rc = h->flags.ensure(std::max<int64_t>((int64_t)NMP * h->n_max * h->K, 1))) ||
       (rc = h->budget.ensure(std::max<int64_t>((int64_t)NMP * h->n_max, 1) * 8)) ||
       (rc = h->poscnt.ensure(std::max<int64_t>((int64_t)NMP * h->n_max, 1) * 4)) ||
-      (rc = upload(h, h->tab_off_d, h->tab_off)))
+      (rc = upload_same(h, h->tab_off_d, h->tab_off)))
     return rc;
   CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
   if (NMP > 0 && h->K > 0) {
@@ -2115,7 +2118,7 @@ int coral_s1_enumerate(coral_s1_handle* h) {
   h->cand_off.assign(NMP + 1, 0);
   for (int mp = 0; mp < NMP; ++mp) h->cand_off[mp + 1] = h->cand_off[mp] + h->counts[mp / h->NP];
   h->ncand = h->cand_off[NMP];
-  if ((rc = upload(h, h->cand_off_d, h->cand_off)) || (rc = upload(h, h->koff_d, h->koff))) return rc;
+  if ((rc = upload_same(h, h->cand_off_d, h->cand_off)) || (rc = upload_same(h, h->koff_d, h->koff))) return rc;
   h->have_enum = true;
   h->have_eval = false;
   return 0;
@@ -2232,7 +2235,7 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
     h->lat_states = 0;                 // per-candidate kernel
     return 0;
   }
-  if ((rc = upload(h, h->lat_base_d, h->lat_base, st))) return rc;
+  if ((rc = upload_same(h, h->lat_base_d, h->lat_base, st))) return rc;
   if (h->lat_states == 0) return 0;
   const long long ns = h->lat_states;
   if ((rc = h->lat_key.ensure(ns * 8)) || (rc = h->lat_nsub.ensure((ns + 1) * 8)) ||
@@ -2292,7 +2295,7 @@ static int lattice_prepare(coral_s1_handle* h, cudaStream_t st) {
     }
     const std::vector<double>& flat = h->sums_flat;
     const std::vector<int>& soff = h->sums_off;
-    if ((rc = upload(h, h->lat_sums, flat, st)) || (rc = upload(h, h->lat_soff, soff, st))) return rc;
+    if ((rc = upload_same(h, h->lat_sums, flat, st)) || (rc = upload_same(h, h->lat_soff, soff, st))) return rc;
     for (int m = 0; m < h->NM; ++m) {
       if (!h->counts[m] || !h->model_used[m]) continue;
       const double lo = h->wbytes_h[m], hi = h->rho * lo;
@@ -2798,8 +2801,8 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
       }
       if (rm.empty()) { rm.push_back(0); rph.push_back(0); boff.push_back(0); }  // non-empty device arrays
       rph.resize((rph.size() + 7) & ~size_t(7), 0);
-      if ((rc = upload(h, h->run_off_d, boff)) || (rc = upload(h, h->run_mp_d, rm)) ||
-          (rc = upload_same(h, h->run_ph_d, rph, h->runph_shadow, h->runph_at)))
+      if ((rc = upload_same(h, h->run_off_d, boff)) || (rc = upload_same(h, h->run_mp_d, rm)) ||
+          (rc = upload_same(h, h->run_ph_d, rph)))
         return rc;
       A.run_boff = h->run_off_d.as<int64_t>();
       A.run_mp = h->run_mp_d.as<int>();
@@ -2814,7 +2817,7 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
           if (rank1 >= 1 && rank1 <= h->K && cnt > 0)
             tp[(size_t)r * 512 + tok] = (double)cnt * pv[(size_t)r * h->K + h->inv_rank_h[rank1 - 1]];
         }
-      if ((rc = upload_same(h, h->tokp, tp, h->tokp_shadow, h->tokp_at))) return rc;
+      if ((rc = upload_same(h, h->tokp, tp))) return rc;
       A.tok_price = h->tokp.as<double>();
     }
     // exact prefilter: per (segment, price bucket) max T -> prefix max. The bucket range
