@@ -615,3 +615,17 @@ def test_candidates_into_empty_price_matrix_writes_an_empty_slot():
     prob.h.frontier_candidates_into(np.zeros((0, len(configs))), slot.data_ptr(), item, 4)
     torch.cuda.synchronize()
     assert slot[:8].view(torch.int64).item() == 0
+
+
+@pytest.mark.parametrize("seed", [1, 2, 4, 12, 16, 32])
+def test_random_scenarios_library_frontier_and_pieces(seed):
+    """tools/stress_random.py scenarios (n_max up to 7, non-monotone / 1e-12-tolerance
+    ProfileTable rows, regional prices with unpriced configs): records, frontier and a
+    three-rank pieces merge through the device slots all equal the oracle."""
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "stress_random.py")
+    spec = importlib.util.spec_from_file_location("stress_random", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.check(seed) == ""
