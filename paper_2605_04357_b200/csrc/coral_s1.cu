@@ -668,12 +668,25 @@ __global__ void __launch_bounds__(256, 6) lat_top_kernel(TopArgs A) {
   const int lane = threadIdx.x & 31;
   const long long ci = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= A.ncombo) return;
-  int cfg[kMaxC], cnt[kMaxC];
-  const int C = lat_tokens(A.inv_rank, A.keys[ci], cfg, cnt);
+  const int Lu = A.Lu, LuP = lat_pitch(Lu);
+  // one pass over the key's tokens (combo order; no per-thread arrays): M, n, the
+  // config mask and the S = 1 value (f[1][L][full] = value[full][L], the same sum order)
   int M = 1, n = 0;
   unsigned long long cmask = 0ull;  // the candidate's configs
-  for (int c = 0; c < C; ++c) { M *= cnt[c] + 1; n += cnt[c]; cmask |= 1ull << cfg[c]; }
-  const int Lu = A.Lu, LuP = lat_pitch(Lu);
+  double v1 = 0.0;
+  {
+    const unsigned long long key = A.keys[ci];
+#pragma unroll
+    for (int t = 0; t < kMaxC; ++t) {
+      const unsigned tok = (unsigned)(key >> (9 * (kMaxC - 1 - t))) & 511u;
+      if (!tok) break;
+      const int cfg = A.inv_rank[(tok >> 3) - 1], cnt = (int)(tok & 7u);
+      M *= cnt + 1;
+      n += cnt;
+      cmask |= 1ull << cfg;
+      v1 = rn_add(v1, rn_mul((double)cnt, A.tab_mp[cfg * Lu + (Lu - 1)]));
+    }
+  }
   const int Smax = min(n, Lu);
   // this lane's u codes (lane+1, lane+33): size, idx(u), idx(full-u) from the model's
   // rank table (code M-1-c is the complement of code c)
@@ -695,11 +708,7 @@ __global__ void __launch_bounds__(256, 6) lat_top_kernel(TopArgs A) {
   // S ascending; strict improvement (templates.py:322) -> smaller S on ties
   double tbest = kNegInf;
   int twin = 0, tcode = 0, tj = 0, npairs = 0;
-  if ((A.smask & 2u) && Smax >= 1 && !kScan) {  // S = 1: f[1][L][full] = value[full][L]
-    double v = 0.0;
-    for (int c = 0; c < C; ++c) v = rn_add(v, rn_mul((double)cnt[c], A.tab_mp[cfg[c] * Lu + (Lu - 1)]));
-    if (v > 1e-9) { tbest = v; twin = 1; }
-  }
+  if ((A.smask & 2u) && Smax >= 1 && !kScan && v1 > 1e-9) { tbest = v1; twin = 1; }  // S = 1
   for (int S = 2; S <= Smax; ++S) {
     if (!((A.smask >> S) & 1u)) continue;
     if (((cmask & A.nonmono[S]) != 0ull) != kScan) continue;  // the other pass's candidates at S
