@@ -46,6 +46,15 @@ def main():
         st = prob.h.stage_ms()
         rows.append(([1e3 * (b - a) for a, b in zip(t, t[1:])], 1e3 * (t[-1] - t[0]), st))
         del front, prob
+    bf = []
+    for it in range(8):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        front = build_frontier(w.configs, w.models, w.slos, caps, w.prices, regions=w.regions, ctx=ctx)
+        torch.cuda.synchronize()
+        bf.append(1e3 * (time.perf_counter() - t0))
+        del front
+    print("build_frontier ms:", " ".join(f"{x:.3f}" for x in bf))
     labels = ["meta+prices", "Stage1Problem", "tables()", "enumerate()", "evaluate()", "frontier()",
               "get_frontier", "materialise"]
     for d, tot, st in rows[2:]:
