@@ -39,13 +39,25 @@ def main():
             for mp, mk, a, b in ps:
                 units += [(mp, S, a, b) for S in range(1, 8) if mk >> S & 1]
             pred = _rank_load(units, F, Ld, Td)
+            # the serial sum and the slot count (fit of the overlap model)
+            groups = {}
+            seen = set()
+            for mp, S, a, b in units:
+                g = groups.get(mp, 0.0)
+                if (mp, a, b) not in seen:
+                    seen.add((mp, a, b))
+                    g += F[mp] * (b - a)
+                groups[mp] = g + Ld[mp].get(S, 0.0) + Td[mp].get(S, 0.0) * (b - a)
+            serial = sum(groups.values())
+            top = max(groups.values()) if groups else 0.0
             pieces = pieces_to_ranges(ps, prob.counts, NP)
             ms = []
             for _ in range(4):
                 prob.h.evaluate_pieces(pieces)
                 torch.cuda.synchronize()
                 ms.append(prob.h.stage_ms()["evaluate"])
-            print(f"world {world} rank {r}: predicted {pred:.3f} ms measured {min(ms[1:]):.3f} ms  pieces "
+            print(f"world {world} rank {r}: slots {len(groups)} serial {serial:.3f} top {top:.3f} "
+                  f"predicted {pred:.3f} ms measured {min(ms[1:]):.3f} ms  pieces "
                   + " ".join(f"(mp{mp} S{[S for S in range(1, 8) if mk >> S & 1]} {a:.3f}-{b:.3f})" for mp, mk, a, b in ps))
 
 
