@@ -2790,7 +2790,7 @@ static int frontier_run(coral_s1_handle* h, int num_regions, const double* price
     A.items = h->items.as<coral_s1_frontier_item>();
     A.nitems = h->nsel.as<unsigned long long>();
     int64_t nblocks = 0;
-    {  // only the models this device evaluated (all of them on one GPU), 256 per block;
+    {  // only the models this device evaluated (all of them on one GPU), kFrontBlock per block;
        // a run serves the model's evaluated phases together
       if (h->NP > kFrontPhases) return fail(CORAL_S1_EUNSUPPORTED, "frontier: at most 2 phases");
       std::vector<int64_t> boff(1, 0);
