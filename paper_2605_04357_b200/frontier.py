@@ -152,6 +152,13 @@ def _frontier_across_ranks(prob: Stage1Problem, pmat, tdist) -> int:
 
 _CALIBRATION: dict = {}
 _PIECES: dict = {}
+_MEMO_KEEP = 64  # distinct problems remembered (oldest dropped first)
+
+
+def _remember(memo: dict, key, value) -> None:
+    if len(memo) >= _MEMO_KEEP:
+        memo.pop(next(iter(memo)))
+    memo[key] = value
 
 
 def rank_pieces(prob: Stage1Problem, tdist) -> list:
@@ -181,10 +188,10 @@ def rank_pieces(prob: Stage1Problem, tdist) -> list:
             box = [costs]
             tdist.broadcast_object_list(box, src=0)
             costs = box[0]
-        _CALIBRATION[key] = costs
+        _remember(_CALIBRATION, key, costs)
     plan = plan_pieces(costs, world)
     pieces = pieces_to_ranges(plan[rank], prob.counts, NP)
-    _PIECES[pkey] = pieces
+    _remember(_PIECES, pkey, pieces)
     return pieces
 
 
