@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--c5", action="store_true", help="(default) also time BASELINE config 5")
     ap.add_argument("--no-c5", action="store_true", help="skip the BASELINE config 5 solve (seconds)")
     return ap.parse_args()
