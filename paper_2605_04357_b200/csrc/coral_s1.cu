@@ -2058,9 +2058,12 @@ int coral_s1_enumerate(coral_s1_handle* h) {
   h->counts.assign(NM, 0);
   h->koff.assign(NM + 1, 0);
   if (NM > 0 && U > 0) {
-    const int nblk = (int)((U + kEnumBlock - 1) / kEnumBlock);
+    const int64_t nblk64 = (U + kEnumBlock - 1) / kEnumBlock;
+    const int nblk = (int)std::min<int64_t>(nblk64, INT32_MAX);
     const int64_t nchunk = (U + kEnumChunk - 1) / kEnumChunk;
     const int64_t nb = (int64_t)NM * nchunk;
+    if (nb + 1 > (int64_t)INT32_MAX || nblk64 > INT32_MAX)  // one 32-bit-indexed scan over (model, chunk)
+      return fail(CORAL_S1_EUNSUPPORTED, "enumerate: models x universe chunks exceed 2^31");
     if ((rc = h->ukey_s.ensure(U * 8)) || (rc = h->umem_s.ensure(U * 8)) ||
         (rc = h->blkcnt.ensure((nb + 1) * 8)) || (rc = h->blkoff.ensure((nb + 1) * 8)))
       return rc;
