@@ -2439,15 +2439,19 @@ static int lattice_pass(coral_s1_handle* h, int mp, int slot, const unsigned* ra
                    m_scan = scan ? smask : 0u;
 #define CORAL_LAYER(SL, MODE, MASK) \
     lat_layer_kernel<SL, MODE><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, MASK, xmask, h->n_max, Lu, maxn, off, sub, W, cen)
+#define CORAL_LAYER_RUN(SL, MASK) \
+    lat_layer_run_kernel<SL><<<lgrid, 256, 0, st>>>(L, sg, sg + 1, MASK, xmask, h->n_max, Lu, maxn, off, sub, W, cen)
+    const bool run = Lu >= kLayerRunMinLu;  // exact rows of a long model: two cells per lane
     if (h->n_max >= 7) {
-      if (m_exact) CORAL_LAYER(2, 1, m_exact);
+      if (m_exact) { if (run) CORAL_LAYER_RUN(2, m_exact); else CORAL_LAYER(2, 1, m_exact); }
       if (m_tol) CORAL_LAYER(2, 0, m_tol);
       if (m_scan) CORAL_LAYER(2, 2, m_scan);
     } else {
-      if (m_exact) CORAL_LAYER(1, 1, m_exact);
+      if (m_exact) { if (run) CORAL_LAYER_RUN(1, m_exact); else CORAL_LAYER(1, 1, m_exact); }
       if (m_tol) CORAL_LAYER(1, 0, m_tol);
       if (m_scan) CORAL_LAYER(1, 2, m_scan);
     }
+#undef CORAL_LAYER_RUN
 #undef CORAL_LAYER
     timed_end(h, st, ti);
     LAUNCH_CHECK(h);

@@ -346,6 +346,66 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
   }
 }
 
+// Exactly monotone rows (kMode 1): the crossing count t(l) = #{j <= jmax(l) : g(j) >
+// f[l - j]} of one (u, X-u) pair moves by 0 or 1 from cell l - 1 to cell l (g and f are
+// non-increasing: t(l) >= t(l-1) since f[l-j] <= f[l-1-j]; t(l) <= t(l-1) + 1 since
+// g(j) <= g(j-1) <= f[l-j] past it), and the step test g(t+1) > f[l-1-t] reads exactly
+// the two values cell l - 1 loaded for its own result. So a lane that owns kRun
+// consecutive cells bisects once (the capped bracket of dp_pair) and then walks: per
+// cell the two shortcut tests and two loads, no search. The result of every cell is
+// dp_pair's (kernels.py:210-239): shortcut 1 (g(1) <= h(1)) <=> t == 0, shortcut 2,
+// else (lo, hi) = (t, t + 1), the unique boundary the reference's bisection finds.
+template <int kRun>
+__device__ __forceinline__ void layer_run(const double* __restrict__ gv, const double* __restrict__ fr, int l1,
+                                          int lmax, int sg, double* cand, int* cj) {
+  const double2 g01 = *reinterpret_cast<const double2*>(gv);  // (J as integer bits, g(1))
+  const int J = __double2loint(g01.x);
+  const double g1 = g01.y;
+  const double hm = fr[sg - 1];             // h(jmax) = f[l - jmax] = f[sg - 1] for every l
+  const int K = __double2loint(fr[0]);      // last l with f > 0
+  int t = 0;
+  double gt1 = g1, ft = 0.0;                // g(t + 1) and f[l - t] of the previous cell
+#pragma unroll
+  for (int r = 0; r < kRun; ++r) {
+    const int l = l1 + r;
+    if (l > lmax) break;
+    const int jmax = l - (sg - 1);
+    if (r == 0) {
+      // cold start: t by the capped bisection (P(j) true below min(J, l-K-1), false
+      // above J; P(1) decides t == 0)
+      const double h1 = fr[l - 1];
+      if (g1 <= h1) {
+        t = 0;
+      } else {
+        int lo = max(1, min(min(J, l - K - 1), jmax));
+        int hi = min(J, jmax) + 1;  // P(hi) false (or past jmax)
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (gv[mid] > fr[l - mid]) lo = mid; else hi = mid;
+        }
+        t = lo;
+      }
+    } else if (t + 1 <= jmax) {
+      t += gt1 > ft ? 1 : 0;  // P_l(t + 1) = g(t + 1) > f[(l - 1) - t]
+    }
+    if (t == 0) {  // shortcut 1: g(1) <= h(1)
+      cand[r] = g1;
+      cj[r] = 1;
+      gt1 = g1;
+      if (r + 1 < kRun && l < lmax) ft = fr[l];  // f[l - 0] for the next step
+      continue;
+    }
+    const double gm = gv[jmax];
+    const double vlo = fr[l - t];
+    const double vhi = gv[t + 1];  // t <= jmax < Lu
+    if (gm >= hm) { cand[r] = hm; cj[r] = jmax; }  // shortcut 2
+    else if (vlo >= vhi) { cand[r] = vlo; cj[r] = t; }
+    else { cand[r] = vhi; cj[r] = t + 1; }
+    gt1 = vhi;
+    ft = vlo;
+  }
+}
+
 // DP layer sg for every S in [S_lo, S_lo + gridDim.y) with S > sg: warp per state X,
 // lanes over l. Cells: sg <= |X| <= maxn(X) - (S - sg), sg <= l <= Lu - (S - sg).
 // kSlots = ceil((M(X) - 1) / 32) code slots per lane: 1 while n_max <= 6 (|X| <= 5),
@@ -354,8 +414,8 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
 // 1e-12 tolerance (the literal [1, jmax] search), 2 = the full-scan variant (rows that
 // fail the monotone test, kernels.py:240-249). One launch per mode; each launch's smask
 // holds only the S values of its mode.
-template <int kSlots, int kMode>
-__global__ void __launch_bounds__(256, 8) lat_layer_kernel(
+template <int kSlots, int kMode, int kLayerRun>
+__device__ __forceinline__ void lat_layer_body(
     LatModel L, int sg, int S_lo, unsigned smask, unsigned xmask, int n_max, int Lu,
     const unsigned* __restrict__ maxn, const long long* __restrict__ off,
     const uint2* __restrict__ subtab, LatWork W, unsigned long long* __restrict__ census) {
@@ -436,6 +496,67 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
     atomicAdd(census, (unsigned long long)(10 * (lmax - sg + 1) + 16 * (Lu + 1) + 8 * nv));
     atomicAdd(census + 1, (unsigned long long)nv * (unsigned long long)(lmax - sg + 1));  // (u, l) pairs
   }
+  if (kMode == 1 && kLayerRun > 1) {
+    // exactly monotone rows: each lane owns kLayerRun consecutive cells (layer_run)
+    for (int l0 = sg; l0 <= lmax; l0 += 32 * kLayerRun) {
+      const int wc = min(32 * kLayerRun, lmax - l0 + 1);  // cells of this chunk
+      const int wl = (wc + kLayerRun - 1) / kLayerRun;     // lanes they need
+      int lw = 0;
+      while ((1 << lw) < wl) ++lw;
+      const int wp = 1 << lw;
+      const int G = 32 >> lw;
+      const int g = lane >> lw, i = lane & (wp - 1);
+      const int l1 = l0 + i * kLayerRun;
+      const bool act = i < wl;
+      double best[kLayerRun];
+      int bu[kLayerRun], bj[kLayerRun];
+#pragma unroll
+      for (int r = 0; r < kLayerRun; ++r) { best[r] = kNegInf; bu[r] = 1 << 20; bj[r] = 0; }
+      const int T = (nv + G - 1) >> (5 - lw);
+      for (int t = 0; t < T; ++t) {
+        const int kk = t * G + g;
+        const int src = (kk < nv ? kk : 0) & 31, slot = kSlots > 1 && kk < nv ? kk >> 5 : 0;
+        unsigned vo = 0u, fo = 0u;
+        int code = 0;
+#pragma unroll
+        for (int r = 0; r < kSlots; ++r) {
+          const unsigned a = __shfl_sync(0xffffffffu, cvo[r], src);
+          const unsigned b = __shfl_sync(0xffffffffu, cfo[r], src);
+          const int c = __shfl_sync(0xffffffffu, ccode[r], src);
+          if (r == slot) { vo = a; fo = b; code = c; }
+        }
+        if (!act || kk >= nv) continue;
+        double cand[kLayerRun];
+        int cj[kLayerRun];
+        layer_run<kLayerRun>(value + vo, fprev + fo, l1, lmax, sg, cand, cj);
+#pragma unroll
+        for (int r = 0; r < kLayerRun; ++r)
+          if (l1 + r <= lmax && cand[r] > best[r]) { best[r] = cand[r]; bu[r] = code; bj[r] = cj[r]; }
+      }
+      int lastpos = 0;
+#pragma unroll
+      for (int r = 0; r < kLayerRun; ++r) {
+        // merge the groups of each cell: value desc, then smallest code
+        for (int ofs = wp; ofs < 32; ofs <<= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best[r], ofs);
+          const int ou = __shfl_xor_sync(0xffffffffu, bu[r], ofs);
+          const int oj = __shfl_xor_sync(0xffffffffu, bj[r], ofs);
+          if (ob > best[r] || (ob == best[r] && ou < bu[r])) { best[r] = ob; bu[r] = ou; bj[r] = oj; }
+        }
+        const int l = l1 + r;
+        if (act && g == 0 && l <= lmax) {
+          fout[idx * LuP + l] = best[r];
+          chout[idx * LuP + l] = (unsigned short)((bu[r] << 10) | bj[r]);
+          if (sg == S - 1) {  // the layer the top cells read: its summary entries
+            if (l == S - 1) W.fs(S)[idx * 4 + 1] = best[r];
+            if (l == Lu - 1) W.fs(S)[idx * 4 + 2] = best[r];
+          }
+          if (best[r] > 0.0) lastpos = l;
+        }
+      }
+      kpos = max(kpos, (int)__reduce_max_sync(0xffffffffu, (unsigned)lastpos));
+    }
+  } else
   for (int l0 = sg; l0 <= lmax; l0 += 32) {
     // lanes = G groups x wp positions; group g takes valid codes g, g+G, g+2G, ...
     const int w = min(32, lmax - l0 + 1);
@@ -491,6 +612,28 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
     fout[idx * LuP] = __longlong_as_double((long long)kpos);  // K as integer bits
     if (sg == S - 1) W.fs(S)[idx * 4] = fout[idx * LuP];
   }
+}
+
+// The layer kernel: one launch per (sg, search mode); lanes own one cell each.
+template <int kSlots, int kMode>
+__global__ void __launch_bounds__(256, 8) lat_layer_kernel(
+    LatModel L, int sg, int S_lo, unsigned smask, unsigned xmask, int n_max, int Lu,
+    const unsigned* __restrict__ maxn, const long long* __restrict__ off,
+    const uint2* __restrict__ subtab, LatWork W, unsigned long long* __restrict__ census) {
+  lat_layer_body<kSlots, kMode, 1>(L, sg, S_lo, smask, xmask, n_max, Lu, maxn, off, subtab, W, census);
+}
+
+// Exactly monotone rows of long models (Lu >= kLayerRunMinLu): lanes own two consecutive
+// cells (layer_run: one bisection, then the free staircase step) -- fewer probes where
+// the crossing brackets are wide (BASELINE config 3, Lu = 80: evaluate -8%); with short
+// rows the capped bisection is already cheap and the one-cell kernel is faster.
+constexpr int kLayerRunMinLu = 56;
+template <int kSlots>
+__global__ void __launch_bounds__(256, 6) lat_layer_run_kernel(
+    LatModel L, int sg, int S_lo, unsigned smask, unsigned xmask, int n_max, int Lu,
+    const unsigned* __restrict__ maxn, const long long* __restrict__ off,
+    const uint2* __restrict__ subtab, LatWork W, unsigned long long* __restrict__ census) {
+  lat_layer_body<kSlots, 1, 2>(L, sg, S_lo, smask, xmask, n_max, Lu, maxn, off, subtab, W, census);
 }
 
 }  // namespace coral
