@@ -6,7 +6,7 @@
   ncu --metrics smsp__inst_executed.sum,l1tex__data_pipe_lsu_wavefronts.sum,\
 sm__inst_executed_pipe_lsu.sum,gpu__time_duration.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,\
 l1tex__throughput.avg.pct_of_peak_sustained_active --clock-control none --csv \
-    -k regex:"lat_layer_kernel|lat_top_kernel" -s $SKIP -c $COUNT \
+    -k regex:"lat_layer|lat_top_kernel" -s $SKIP -c $COUNT \
     --log-file gpurun_out/calib_ncu.csv python tools/onchip_calib.py run
   # here: combine -> profiles/r02_onchip_calib.json
   python tools/onchip_calib.py reduce gpurun_out/calib_census.json gpurun_out/calib_ncu.csv
@@ -63,7 +63,7 @@ def reduce(census_path, ncu_csv):
     head = rows[0]
     ki, mi, vi = head.index("Kernel Name"), head.index("Metric Name"), head.index("Metric Value")
     for r in rows[1:]:
-        kern = "lat_layer_kernel" if "lat_layer_kernel" in r[ki] else "lat_top_kernel"
+        kern = "lat_layer_kernel" if "lat_layer" in r[ki] else "lat_top_kernel"  # incl. lat_layer_run_kernel
         v = float(r[vi].replace(",", ""))
         d = sums.setdefault(kern, {})
         d.setdefault(r[mi], []).append(v)
