@@ -1420,6 +1420,7 @@ __global__ void skyline_flags_kernel(const unsigned long long* __restrict__ seg,
 // survivors' ordinals; front_emit_kernel writes them compacted, segment by segment.
 // Segments larger than kSegCap items take the general path (frontier_from_items_general).
 constexpr int kSegThreads = 1024, kSegCap = 4096, kMaxParts = 32;
+constexpr int kSegPrefilter = 512;  // segments above this take a bucket prefilter before the sort
 
 struct SegKey {
   unsigned long long price;  // bit pattern of price >= 0 (orders like the value)
@@ -1543,10 +1544,62 @@ __global__ void __launch_bounds__(kSegThreads) front_segment_kernel(FrontParts F
     }
   }
   __syncthreads();
-  const int cnt = (int)s_cnt;
+  int cnt = (int)s_cnt;
   if (cnt > kSegCap) {
     if (tid == 0) { atomicOr(overflow, 1u); surv[seg] = 0u; }
     return;
+  }
+  if (cnt > kSegPrefilter) {
+    // a large segment (few segments, many items: the multi-GPU merge of a one-model
+    // config): the exact bucket prefilter of the frontier passes again, over this
+    // segment's union, before its sort -- per price bucket (top bits of the price's bit
+    // pattern over the segment's own range: a non-decreasing map) the max T; an item
+    // goes only if a strictly cheaper bucket holds a T >= its T (a cheaper item that
+    // precedes and dominates it). The kept set contains every survivor, so the sort
+    // and running-max skyline below stay exact on fewer items.
+    __shared__ unsigned long long s_bkt[kSegThreads];
+    unsigned long long lmx = 0ull, lmn = 0ull;  // max price bits, max of ~price bits
+    for (int i = tid; i < cnt; i += kSegThreads) {
+      const unsigned long long pb = s_keys[i].price;
+      lmx = pb > lmx ? pb : lmx;
+      lmn = ~pb > lmn ? ~pb : lmn;
+    }
+    unsigned long long hi_b = 0ull, lo_nb = 0ull;
+    block_excl_scan<true>(lmx, s_warp, &hi_b);
+    block_excl_scan<true>(lmn, s_warp, &lo_nb);
+    const unsigned long long lo_b = ~lo_nb;
+    int shift = 0;  // block-uniform
+    while (((hi_b >> shift) - (lo_b >> shift)) >= (unsigned long long)kSegThreads) ++shift;
+    const unsigned long long base = lo_b >> shift;
+    s_bkt[tid] = 0ull;
+    __syncthreads();
+    for (int i = tid; i < cnt; i += kSegThreads) {
+      const int b = (int)((s_keys[i].price >> shift) - base);
+      const unsigned long long tb = ~s_keys[i].neg_t;
+      if (s_bkt[b] < tb) atomicMax(&s_bkt[b], tb);
+    }
+    __syncthreads();
+    const unsigned long long pre = block_excl_scan<true>(s_bkt[tid], s_warp, nullptr);  // strictly cheaper
+    s_bkt[tid] = pre;
+    __syncthreads();
+    constexpr int kPer = kSegCap / kSegThreads;
+    SegKey mine[kPer];
+    unsigned live = 0u;
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int i = tid + r * kSegThreads;
+      if (i < cnt) {
+        mine[r] = s_keys[i];
+        if (~mine[r].neg_t > s_bkt[(int)((mine[r].price >> shift) - base)]) live |= 1u << r;
+      }
+    }
+    unsigned long long total = 0ull;
+    unsigned o = (unsigned)block_excl_scan<false>((unsigned long long)__popc(live), s_warp, &total);  // syncs
+#pragma unroll
+    for (int r = 0; r < kPer; ++r)
+      if ((live >> r) & 1u) s_keys[o++] = mine[r];
+    __syncthreads();
+    cnt = (int)total;
   }
   int np2 = 1;
   while (np2 < cnt) np2 <<= 1;
