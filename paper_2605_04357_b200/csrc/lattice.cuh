@@ -357,7 +357,7 @@ __global__ void lat_value_kernel(LatModel L, const int* __restrict__ inv_rank,
 // else (lo, hi) = (t, t + 1), the unique boundary the reference's bisection finds.
 template <int kRun>
 __device__ __forceinline__ void layer_run(const double* __restrict__ gv, const double* __restrict__ fr, int l1,
-                                          int lmax, int sg, double* cand, int* cj) {
+                                          int lmax, int sg, int code, double* best, int* bc) {
   const double2 g01 = *reinterpret_cast<const double2*>(gv);  // (J as integer bits, g(1))
   const int J = __double2loint(g01.x);
   const double g1 = g01.y;
@@ -389,8 +389,7 @@ __device__ __forceinline__ void layer_run(const double* __restrict__ gv, const d
       t += gt1 > ft ? 1 : 0;  // P_l(t + 1) = g(t + 1) > f[(l - 1) - t]
     }
     if (t == 0) {  // shortcut 1: g(1) <= h(1)
-      cand[r] = g1;
-      cj[r] = 1;
+      if (g1 > best[r]) { best[r] = g1; bc[r] = (code << 10) | 1; }
       gt1 = g1;
       if (r + 1 < kRun && l < lmax) ft = fr[l];  // f[l - 0] for the next step
       continue;
@@ -398,9 +397,12 @@ __device__ __forceinline__ void layer_run(const double* __restrict__ gv, const d
     const double gm = gv[jmax];
     const double vlo = fr[l - t];
     const double vhi = gv[t + 1];  // t <= jmax < Lu
-    if (gm >= hm) { cand[r] = hm; cj[r] = jmax; }  // shortcut 2
-    else if (vlo >= vhi) { cand[r] = vlo; cj[r] = t; }
-    else { cand[r] = vhi; cj[r] = t + 1; }
+    double c;
+    int j;
+    if (gm >= hm) { c = hm; j = jmax; }  // shortcut 2
+    else if (vlo >= vhi) { c = vlo; j = t; }
+    else { c = vhi; j = t + 1; }
+    if (c > best[r]) { best[r] = c; bc[r] = (code << 10) | j; }
     gt1 = vhi;
     ft = vlo;
   }
@@ -509,9 +511,9 @@ __device__ __forceinline__ void lat_layer_body(
       const int l1 = l0 + i * kLayerRun;
       const bool act = i < wl;
       double best[kLayerRun];
-      int bu[kLayerRun], bj[kLayerRun];
+      int bc[kLayerRun];  // code << 10 | j of the best
 #pragma unroll
-      for (int r = 0; r < kLayerRun; ++r) { best[r] = kNegInf; bu[r] = 1 << 20; bj[r] = 0; }
+      for (int r = 0; r < kLayerRun; ++r) { best[r] = kNegInf; bc[r] = (1 << 20) << 10; }
       const int T = (nv + G - 1) >> (5 - lw);
       for (int t = 0; t < T; ++t) {
         const int kk = t * G + g;
@@ -526,12 +528,7 @@ __device__ __forceinline__ void lat_layer_body(
           if (r == slot) { vo = a; fo = b; code = c; }
         }
         if (!act || kk >= nv) continue;
-        double cand[kLayerRun];
-        int cj[kLayerRun];
-        layer_run<kLayerRun>(value + vo, fprev + fo, l1, lmax, sg, cand, cj);
-#pragma unroll
-        for (int r = 0; r < kLayerRun; ++r)
-          if (l1 + r <= lmax && cand[r] > best[r]) { best[r] = cand[r]; bu[r] = code; bj[r] = cj[r]; }
+        layer_run<kLayerRun>(value + vo, fprev + fo, l1, lmax, sg, code, best, bc);
       }
       int lastpos = 0;
 #pragma unroll
@@ -539,14 +536,14 @@ __device__ __forceinline__ void lat_layer_body(
         // merge the groups of each cell: value desc, then smallest code
         for (int ofs = wp; ofs < 32; ofs <<= 1) {
           const double ob = __shfl_xor_sync(0xffffffffu, best[r], ofs);
-          const int ou = __shfl_xor_sync(0xffffffffu, bu[r], ofs);
-          const int oj = __shfl_xor_sync(0xffffffffu, bj[r], ofs);
-          if (ob > best[r] || (ob == best[r] && ou < bu[r])) { best[r] = ob; bu[r] = ou; bj[r] = oj; }
+          const int oc = __shfl_xor_sync(0xffffffffu, bc[r], ofs);
+          // value desc, then smallest code (bc orders by code first: j < 1024)
+          if (ob > best[r] || (ob == best[r] && oc < bc[r])) { best[r] = ob; bc[r] = oc; }
         }
         const int l = l1 + r;
         if (act && g == 0 && l <= lmax) {
           fout[idx * LuP + l] = best[r];
-          chout[idx * LuP + l] = (unsigned short)((bu[r] << 10) | bj[r]);
+          chout[idx * LuP + l] = (unsigned short)bc[r];
           if (sg == S - 1) {  // the layer the top cells read: its summary entries
             if (l == S - 1) W.fs(S)[idx * 4 + 1] = best[r];
             if (l == Lu - 1) W.fs(S)[idx * 4 + 2] = best[r];
@@ -624,12 +621,13 @@ __global__ void __launch_bounds__(256, 8) lat_layer_kernel(
 }
 
 // Exactly monotone rows of long models (Lu >= kLayerRunMinLu): lanes own two consecutive
-// cells (layer_run: one bisection, then the free staircase step) -- fewer probes where
-// the crossing brackets are wide (BASELINE config 3, Lu = 80: evaluate -8%); with short
-// rows the capped bisection is already cheap and the one-cell kernel is faster.
+// cells (layer_run: one bisection, then the free staircase step; the running best kept
+// as value + packed (code, j)) -- fewer probes where the crossing brackets are wide
+// (BASELINE config 3, Lu = 80: evaluate 3.56 -> 3.16 ms); with short rows the capped
+// bisection is already cheap and the one-cell kernel is faster.
 constexpr int kLayerRunMinLu = 56;
 template <int kSlots>
-__global__ void __launch_bounds__(256, 6) lat_layer_run_kernel(
+__global__ void __launch_bounds__(256, 8) lat_layer_run_kernel(
     LatModel L, int sg, int S_lo, unsigned smask, unsigned xmask, int n_max, int Lu,
     const unsigned* __restrict__ maxn, const long long* __restrict__ off,
     const uint2* __restrict__ subtab, LatWork W, unsigned long long* __restrict__ census) {
