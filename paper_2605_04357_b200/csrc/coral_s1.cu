@@ -593,6 +593,20 @@ __device__ __forceinline__ void warp_argmax_code(double& v, int& code, int& j) {
   v = wv;
 }
 
+// warp_argmax_code with the lane's (code, j) packed as code << 10 | j: among the lanes
+// holding the max value the smallest packed word is the smallest code (each code lives
+// on one lane), so one min-reduction carries the winner's j along.
+__device__ __forceinline__ void warp_argmax_packed(double& v, unsigned& bc) {
+  const bool ok = v >= 0.0;
+  const unsigned long long b = ok ? (unsigned long long)__double_as_longlong(v) : 0ull;
+  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const bool top = hi == mhi && lo == mlo;
+  bc = __reduce_min_sync(0xffffffffu, top ? bc : 0xFFFFFFFFu);
+  v = __hiloint2double((int)mhi, (int)mlo);
+}
+
 // --------------------------------------------------------------------------------
 // Lattice top cells: one warp per candidate of one (model, phase), every S in smask.
 // f_S[S][Lu][full] = max over u (lanes) of the crossing with f_S[S-1][.][full-u]
@@ -707,7 +721,7 @@ __global__ void __launch_bounds__(256, 6) lat_top_kernel(TopArgs A) {
   }
   // S ascending; strict improvement (templates.py:322) -> smaller S on ties
   double tbest = kNegInf;
-  int twin = 0, tcode = 0, tj = 0, npairs = 0;
+  int twin = 0, tbc = 0, npairs = 0;  // tbc: winner's u code << 10 | j
   if ((A.smask & 2u) && Smax >= 1 && !kScan && v1 > 1e-9) { tbest = v1; twin = 1; }  // S = 1
   for (int S = 2; S <= Smax; ++S) {
     if (!((A.smask >> S) & 1u)) continue;
@@ -717,7 +731,7 @@ __global__ void __launch_bounds__(256, 6) lat_top_kernel(TopArgs A) {
     const double* vsum = A.W.vs(S);
     const double* hsum = S == 2 ? vsum : A.W.fs(S);
     double best = kNegInf;
-    int bu = 1 << 20, bj = 0;
+    unsigned bc = 0xFFFFFFFFu;  // this lane's best: u code << 10 | j (code order = bc order)
     // S == 2 reads value rows on both sides: symmetric, search the lower half only
     const int chalf = (S == 2 && ((A.xmask >> 2) & 1u)) ? (M - 1) / 2 : M;
     const bool cap = (A.xmask >> S) & 1u;  // exactly monotone rows: capped crossing search
@@ -739,20 +753,20 @@ __global__ void __launch_bounds__(256, 6) lat_top_kernel(TopArgs A) {
                  __double2loint(gs.x), __double2loint(hs.x), Lu, jmax, cap, tbest > 1e-9 ? tbest : 1e-9, cand, cj);
       }
       ++npairs;
-      if (cand > best) { best = cand; bu = lane + 1 + 32 * k; bj = cj; }
+      if (cand > best) { best = cand; bc = ((unsigned)(lane + 1 + 32 * k) << 10) | (unsigned)cj; }
     }
     // an S only matters if some lane beats the best so far (strict, templates.py:322);
     // otherwise its winning code / j are never used: skip the reduction
     if (!__any_sync(0xffffffffu, best > tbest && best > 1e-9)) continue;
-    warp_argmax_code(best, bu, bj);
-    if (best > tbest && best > 1e-9) { tbest = best; twin = S; tcode = bu; tj = bj; }
+    warp_argmax_packed(best, bc);
+    if (best > tbest && best > 1e-9) { tbest = best; twin = S; tbc = (int)bc; }
   }
   if (A.census) {
     const unsigned np = __reduce_add_sync(0xffffffffu, (unsigned)npairs);
     if (lane == 0) atomicAdd(A.census + 2, (unsigned long long)np);
   }
   if (lane) return;
-  A.win[ci] = make_int4(__double2loint(tbest), __double2hiint(tbest), twin, (tcode << 10) | tj);
+  A.win[ci] = make_int4(__double2loint(tbest), __double2hiint(tbest), twin, tbc);
 }
 
 // Walk-back of each candidate's winning S (kernels.py:258-275) into its canonical
