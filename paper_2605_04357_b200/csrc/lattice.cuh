@@ -566,7 +566,7 @@ __device__ __forceinline__ void lat_layer_body(
     const bool act = i < w;
     const int jmax = l - (sg - 1);
     double best = kNegInf;
-    int bu = 1 << 20, bj = 0;
+    int bc = (1 << 20) << 10;  // best u code << 10 | j
     const int T = (nv + G - 1) >> (5 - lw);
     for (int t = 0; t < T; ++t) {
       const int kk = t * G + g;  // this group's kk-th valid code (ascending per group)
@@ -584,19 +584,18 @@ __device__ __forceinline__ void lat_layer_body(
       double cand;
       int cj;
       dp_pair(value + vo, fprev + fo, l, jmax, kMode != 2, cand, cj, kMode == 1);  // 2: kernels.py:240-249
-      if (cand > best) { best = cand; bu = code; bj = cj; }
+      if (cand > best) { best = cand; bc = (code << 10) | cj; }
     }
     // merge the groups of each l: value desc, then smallest code (the reference's
     // first strictly better u over the ascending code sequence)
     for (int ofs = wp; ofs < 32; ofs <<= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, best, ofs);
-      const int ou = __shfl_xor_sync(0xffffffffu, bu, ofs);
-      const int oj = __shfl_xor_sync(0xffffffffu, bj, ofs);
-      if (ob > best || (ob == best && ou < bu)) { best = ob; bu = ou; bj = oj; }
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, ofs);
+      if (ob > best || (ob == best && oc < bc)) { best = ob; bc = oc; }  // code first: j < 1024
     }
     if (act && g == 0) {
       fout[idx * LuP + l] = best;
-      chout[idx * LuP + l] = (unsigned short)((bu << 10) | bj);
+      chout[idx * LuP + l] = (unsigned short)bc;
       if (sg == S - 1) {  // the layer the top cells read: its summary entries
         if (l == S - 1) W.fs(S)[idx * 4 + 1] = best;
         if (l == Lu - 1) W.fs(S)[idx * 4 + 2] = best;
