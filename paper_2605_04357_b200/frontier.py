@@ -91,7 +91,7 @@ def _dist_info(dist):
 # Items per rank of the single all-gather. Grown (never shrunk) from the largest
 # partial frontier seen; every rank derives it from the same gathered headers, so all
 # ranks always agree on it without a separate exchange.
-_MERGE_CAP = [16384]
+_MERGE_CAP = [4096]
 _GATHER_BUFS: dict = {}
 
 

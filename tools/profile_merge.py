@@ -19,6 +19,9 @@ from paper_2605_04357_b200.library import GenContext, LibraryCaps, Stage1Problem
 
 
 def main():
+    if os.environ.get("MERGE_CAP_ENV"):  # A/B of the all-gather slot capacity
+        from paper_2605_04357_b200 import frontier as _fr
+        _fr._MERGE_CAP[0] = int(os.environ["MERGE_CAP_ENV"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
