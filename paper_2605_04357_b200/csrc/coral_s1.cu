@@ -678,7 +678,7 @@ __device__ __forceinline__ void top_pair(const double* __restrict__ gv, const do
 // kSlots code slots per lane (codes lane + 1 + 32k): 2 for candidates of <= 6 nodes
 // (M <= 64), 4 when a model has 7-node candidates (M <= 128).
 template <int kSlots, bool kScan>
-__global__ void __launch_bounds__(256, 6) lat_top_kernel(TopArgs A) {
+__global__ void __launch_bounds__(128, 12) lat_top_kernel(TopArgs A) {
   const int lane = threadIdx.x & 31;
   const long long ci = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= A.ncombo) return;
@@ -2545,13 +2545,13 @@ static int lattice_pass(coral_s1_handle* h, int mp, int slot, const unsigned* ra
   T.ranks = ranks;
   T.census = h->census_on ? h->census.as<unsigned long long>() : nullptr;
   const int ti = timed_begin(h, st, 0);
-  const unsigned tg = (unsigned)((ncombo * 32 + 255) / 256);
+  const unsigned tg = (unsigned)((ncombo * 32 + 127) / 128);  // 4 candidates (warps) per CTA
   if (h->n_max >= 7) {
-    if (scan) lat_top_kernel<4, true><<<tg, 256, 0, st>>>(T);
-    else lat_top_kernel<4, false><<<tg, 256, 0, st>>>(T);
+    if (scan) lat_top_kernel<4, true><<<tg, 128, 0, st>>>(T);
+    else lat_top_kernel<4, false><<<tg, 128, 0, st>>>(T);
   } else {
-    if (scan) lat_top_kernel<2, true><<<tg, 256, 0, st>>>(T);
-    else lat_top_kernel<2, false><<<tg, 256, 0, st>>>(T);
+    if (scan) lat_top_kernel<2, true><<<tg, 128, 0, st>>>(T);
+    else lat_top_kernel<2, false><<<tg, 128, 0, st>>>(T);
   }
   timed_end(h, st, ti);
   LAUNCH_CHECK(h);
